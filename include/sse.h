@@ -1,0 +1,188 @@
+/*
+ * libsse — B200-native (sm_100a) electron scattering self-energy Sigma^{<>}
+ * of the NEGF self-consistent Born loop (SSE phase), C ABI.
+ *
+ * This is the drop-in boundary for the reference's SSE entry point
+ *   negflow.sse.sse_sigma(variant, g, dc, dh, nmap, grid, counter=None)
+ *   (/root/reference/pkg/src/negflow/sse.py:305-329)
+ * Array conventions are the reference's (all complex128 as interleaved
+ * re,im doubles, C-contiguous):
+ *   G, Sigma  [Nkz, NE, NA, No, No]      gf.py:41, params.py:44-46
+ *   Dc        [Nqz, Nw, NA, NB, 3, 3]    sse.py:81, sse.py:317
+ *   dH        [NA, NB, 3, No, No]        device.py:73-75
+ *   nmap      int64 [NA, NB]             device.py:23-37 (idx[a, s] = f(a, s))
+ *   off, wt   [Nw] frequency_map offsets/weights, params.py:144,158-162
+ * Sigma[k,E,a] = i * sum_{q<Nqz, w<Nw, s<NB} G[(k-q) mod Nkz, E-off_w, f(a,s)]
+ *                    @ (wt_w sum_{i,j} Dc[q,w,a,s,i,j] dH[a,s,i] @ dH[a,s,j]),
+ * terms with E-off_w < 0 dropped (sse.py:58-76, 148-161).
+ *
+ * Return codes: 0 ok; 1 invalid argument (Python: ValueError, the reference's
+ * convention sse.py:315-318); 2 CUDA error; 3 NCCL/communication error;
+ * 4 out of device memory.  sse_last_error() gives the message of the last
+ * failing call on the calling thread.
+ * There is no CPU fallback: without a usable sm_100a device every compute
+ * entry point returns 2.
+ */
+#ifndef SSE_B200_SSE_H
+#define SSE_B200_SSE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSE_OK 0
+#define SSE_EINVAL 1
+#define SSE_ECUDA 2
+#define SSE_ECOMM 3
+#define SSE_ENOMEM 4
+
+/* SseVariant (sse.py:35-40).  All five produce the same Sigma (to rounding);
+ * LAYOUT_TRANSFORMED runs the atom-major layout-transform kernels around the
+ * fused kernel (sse.py:43-55, 244-261), the others read the grid-major
+ * tensors in place. */
+#define SSE_VARIANT_REFERENCE 0
+#define SSE_VARIANT_FISSIONED 1
+#define SSE_VARIANT_REDUNDANCY_REMOVED 2
+#define SSE_VARIANT_LAYOUT_TRANSFORMED 3
+#define SSE_VARIANT_BATCHED_FUSED 4
+
+typedef struct sse_ctx sse_ctx;
+
+/* SimParams shape fields used by the path (params.py:24-50). */
+typedef struct sse_dims {
+  int64_t nkz, nqz, ne, nw, na, nb, norb;
+} sse_dims;
+
+/* A device-resident atom slab of an electron tensor (G or Sigma).
+ * atom0/natoms: global index of the first atom held and how many.
+ * atom_major = 0: [Nkz, NE, natoms, No, No] (grid-major, the reference layout)
+ * atom_major = 1: [natoms, Nkz, NE, No, No] (to_atom_major, sse.py:48-50) */
+typedef struct sse_slab {
+  int64_t atom0, natoms;
+  int32_t atom_major;
+  int32_t reserved;
+} sse_slab;
+
+/* Per-call timing (CUDA events on the library's stream, milliseconds). */
+typedef struct sse_timing {
+  double h2d_ms;
+  double prep_ms;   /* M-operator build (and layout transforms) */
+  double sigma_ms;  /* fused Sigma kernel */
+  double d2h_ms;
+  double total_ms;
+  double flops;     /* algorithmic flops of the call (8 per complex MAC) */
+  int64_t h2d_bytes, d2h_bytes;
+  int32_t kernel_launches;
+  int32_t n_devices;
+} sse_timing;
+
+/* Context: owns a CUDA stream and cached device buffers per device.
+ * n_gpus devices 0..n_gpus-1 (atoms are split in contiguous chunks across
+ * them, distsim.py:117-120).  sse_ctx_create_on binds one given device. */
+int sse_ctx_create(int n_gpus, sse_ctx** out);
+int sse_ctx_create_on(int device, sse_ctx** out);
+void sse_ctx_destroy(sse_ctx* ctx);
+const char* sse_last_error(void);
+int sse_version(void);
+
+/* Host-memory drop-in for sse_sigma (sse.py:305-329).  All pointers are host
+ * pointers to C-contiguous caller-owned buffers (pinned or pageable); the
+ * call copies in, computes on the GPU(s) and copies Sigma back.
+ * off/wt: frequency_map offsets and weights.  t may be NULL. */
+int sse_sigma_c128(sse_ctx* ctx, const sse_dims* d, int variant,
+                   const double* G_l, const double* G_g,
+                   const double* Dc_l, const double* Dc_g,
+                   const double* dH, const int64_t* nmap,
+                   const int64_t* off, const double* wt,
+                   double* Sig_l, double* Sig_g, sse_timing* t);
+
+/* Host-memory call for an owned atom range (one rank's share; the multi-
+ * process drop-in).  g: host G slab (grid-major [Nkz, NE, g.natoms, No, No])
+ * holding every neighbour of the owned atoms; out: owned atoms, with
+ * Dc [Nqz, Nw, out.natoms, NB, 3, 3], dH [out.natoms, NB, 3, No, No],
+ * nmap [out.natoms, NB] (global ids), Sigma [Nkz, NE, out.natoms, No, No].
+ * sse_sigma_c128 is this call with both slabs = [0, NA). */
+int sse_sigma_c128_slab(sse_ctx* ctx, const sse_dims* d, int variant,
+                        const sse_slab* g, const sse_slab* out,
+                        const double* G_l, const double* G_g,
+                        const double* Dc_l, const double* Dc_g,
+                        const double* dH, const int64_t* nmap,
+                        const int64_t* off, const double* wt,
+                        double* Sig_l, double* Sig_g, sse_timing* t);
+
+/* Device-resident Sigma for an owned atom range (the multi-GPU shard call).
+ * g: slab holding every atom f(a, s) of the owned atoms (owned + halo).
+ * out: the owned atoms; Dc_*, dH, nmap cover exactly out.natoms rows:
+ *   Dc [Nqz, Nw, out.natoms, NB, 3, 3], dH [out.natoms, NB, 3, No, No],
+ *   nmap HOST int64 [out.natoms, NB] of GLOBAL atom indices.
+ * d->na is the global atom count.  Pointers other than nmap/off/wt are
+ * device pointers on the context's device; stream is a cudaStream_t (NULL =
+ * the library's stream).  Asynchronous unless t != NULL (then it syncs). */
+int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
+                     const sse_slab* out,
+                     const double* G_l, const double* G_g,
+                     const double* Dc_l, const double* Dc_g,
+                     const double* dH, const int64_t* nmap,
+                     const int64_t* off, const double* wt,
+                     double* Sig_l, double* Sig_g, void* stream,
+                     sse_timing* t);
+
+/* Layout transform K1 (to_atom_major / to_grid_major, sse.py:48-55):
+ * [Nkz, NE, NA, blk] <-> [NA, Nkz, NE, blk], blk = block_doubles doubles.
+ * to_atom_major = 1: grid -> atom major; 0: atom -> grid major.  Device ptrs. */
+int sse_layout_transform(sse_ctx* ctx, int64_t nkz, int64_t ne, int64_t na,
+                         int64_t block_doubles, int to_atom_major,
+                         const double* src, double* dst, void* stream);
+
+/* preprocess_D on the device (sse.py:91-115), one polarity per call:
+ * Dc[q,w,a,s] = D[q,w,b,1+rev(a,s)] - D[q,w,b,0] - D[q,w,a,0] + D[q,w,a,1+s],
+ * b = nmap[a,s], rev = reverse slot (device.py:53-66), same term order as the
+ * reference (bitwise equal).  D is an atom slab [Nqz, Nw, d_natoms, NB+1, 3, 3]
+ * holding atoms [d_atom0, d_atom0 + d_natoms) (it must contain every owned
+ * atom and all their neighbours); Dc is [Nqz, Nw, out_natoms, NB, 3, 3] for
+ * atoms [out_atom0, out_atom0 + out_natoms).  nmap: HOST int64 [NA, NB], the
+ * full map.  Returns 1 ("missing neighbor slot ...") when an owned edge has
+ * no reverse slot. */
+int sse_preprocess_D(sse_ctx* ctx, int64_t nqz, int64_t nw, int64_t na, int64_t nb,
+                     const int64_t* nmap, int64_t d_atom0, int64_t d_natoms,
+                     int64_t out_atom0, int64_t out_natoms, const double* D, double* Dc,
+                     void* stream);
+
+/* Atom-keyed synthetic input generator (device side of
+ * paper_1912_08810_b200.inputs.atom_keyed; not part of the reference).
+ * Each atom owns outer*inner complex values with local index o*inner + i;
+ * value(seed, tensor_id, atom, local index) is a counter-based hash turned
+ * into a unit-variance Irwin-Hall(4) deviate per real/imaginary part, times
+ * scale — independent of the slab bounds, so any atom sub-problem can be
+ * regenerated bit-exactly on the host.  Element (atom a, o, i) is written to
+ * dst[2 * ((a - atom0) * atom_stride + o * outer_stride + i)] (complex units
+ * for the strides). */
+int sse_fill_synthetic(sse_ctx* ctx, uint64_t seed, uint32_t tensor_id,
+                       int64_t atom0, int64_t natoms, int64_t outer,
+                       int64_t inner, int64_t atom_stride, int64_t outer_stride,
+                       double scale, double* dst, void* stream);
+
+/* Per-kernel CUDA-event profile of the context's launches (bench evidence).
+ * sse_profile_begin resets and enables recording on every device of ctx;
+ * sse_profile_end synchronises and returns, per kernel kind, the summed
+ * launch durations, launch counts and algorithmic flops since begin. */
+#define SSE_PROF_OPERATOR 0   /* K2 operator build */
+#define SSE_PROF_SIGMA 1      /* K3 fused Sigma (DMMA) */
+#define SSE_PROF_LAYOUT 2     /* K1 layout transform */
+#define SSE_PROF_PREPROCESS 3 /* preprocess_D */
+#define SSE_PROF_KINDS 4
+typedef struct sse_profile {
+  double ms[SSE_PROF_KINDS];
+  double flops[SSE_PROF_KINDS];
+  int64_t launches[SSE_PROF_KINDS];
+} sse_profile;
+int sse_profile_begin(sse_ctx* ctx);
+int sse_profile_end(sse_ctx* ctx, sse_profile* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSE_B200_SSE_H */

@@ -1,0 +1,765 @@
+// libsse C ABI (include/sse.h): context, validation, host and device entry points.
+//
+// Host entry sse_sigma_c128 / sse_sigma_c128_slab replaces negflow.sse.sse_sigma
+// (sse.py:305-329).  Per device it runs a three-stream pipeline over chunks of
+// owned atoms:
+//   copy stream   H2D of the G columns the chunk needs (grid-major rows are
+//                 strided by NA: cudaMemcpy2DAsync) + the chunk's Dc/dH rows
+//   compute       K2 operator build + K3 fused DMMA Sigma kernel of the chunk
+//   copy stream   D2H of the chunk's Sigma columns
+// so host<->device traffic hides behind the FP64 tensor-core work.
+// Multi-GPU: contiguous atom chunks per device (distsim.py:117-120), one host
+// thread per device; each device reads its halo straight from host memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/sse.h"
+#include "sse_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what, int line) {
+  cudaGetLastError();  // clear non-sticky errors
+  if (e == cudaErrorMemoryAllocation)
+    return fail(SSE_ENOMEM, "out of device memory: %s (line %d)", what, line);
+  return fail(SSE_ECUDA, "CUDA error %s: %s (line %d)", cudaGetErrorString(e), what, line);
+}
+
+#define CU(x)                                                  \
+  do {                                                         \
+    cudaError_t e_ = (x);                                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x, __LINE__); \
+  } while (0)
+
+#define CHECK(x)                   \
+  do {                             \
+    int rc_ = (x);                 \
+    if (rc_ != SSE_OK) return rc_; \
+  } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return SSE_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc", __LINE__);
+    bytes = need;
+    return SSE_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+  double flops;
+};
+
+struct DevState {
+  int device = 0;
+  cudaStream_t stream = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev[6] = {};
+  DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev;
+  // host copies of the small tables last uploaded (skip re-uploads: a pageable
+  // upload would otherwise serialise the host with the stream on every call)
+  std::vector<int> nbr_host, off_host, pp_nbr_host, pp_rev_host;
+  std::vector<double> wt_host;
+  // per-launch CUDA-event profile (sse_profile_begin / sse_profile_end)
+  bool profiling = false;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  std::vector<ProfRec> recs;
+  // pipeline events (grow-only pool)
+  std::vector<cudaEvent_t> pipe;
+
+  cudaEvent_t prof_event() {
+    if (pool_used == pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      pool.push_back(e);
+    }
+    return pool[pool_used++];
+  }
+};
+
+}  // namespace
+
+struct sse_ctx {
+  std::vector<DevState> devs;
+};
+
+namespace {
+
+// Record a profiled launch: `launch` is a callable returning cudaError_t.
+template <class F>
+int profiled(DevState& ds, cudaStream_t st, int kind, double flops, F&& launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (ds.profiling) {
+    a = ds.prof_event();
+    b = ds.prof_event();
+    if (!a || !b) return fail(SSE_ECUDA, "event creation failed");
+    CU(cudaEventRecord(a, st));
+  }
+  CU(launch());
+  if (ds.profiling) {
+    CU(cudaEventRecord(b, st));
+    ds.recs.push_back({kind, a, b, flops});
+  }
+  return SSE_OK;
+}
+
+template <class T>
+int upload_cached(DevBuf& buf, std::vector<T>& host_copy, const std::vector<T>& v, cudaStream_t st) {
+  if (buf.ptr && host_copy == v) return SSE_OK;
+  CHECK(buf.ensure(std::max<size_t>(v.size(), 1) * sizeof(T)));
+  // a pageable async copy stages the source before returning; later calls on
+  // the same stream are ordered after the kernels that read this table.
+  CU(cudaMemcpyAsync(buf.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  host_copy = v;
+  return SSE_OK;
+}
+
+int init_dev(DevState& d, int device) {
+  d.device = device;
+  CU(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(SSE_ECUDA, "device %d (%s, sm_%d%d) is not an sm_100 Blackwell GPU", device,
+                prop.name, prop.major, prop.minor);
+  CU(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&d.s_h2d, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&d.s_d2h, cudaStreamNonBlocking));
+  for (auto& e : d.ev) CU(cudaEventCreate(&e));
+  return SSE_OK;
+}
+
+void destroy_dev(DevState& d) {
+  cudaSetDevice(d.device);
+  for (DevBuf* b : {&d.g[0], &d.g[1], &d.s[0], &d.s[1], &d.dc[0], &d.dc[1], &d.dh, &d.op[0],
+                    &d.op[1], &d.nbr, &d.off, &d.wt, &d.tmp_g, &d.tmp_s, &d.pp_nbr, &d.pp_rev})
+    b->release();
+  for (auto& e : d.ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : d.pool) cudaEventDestroy(e);
+  for (auto& e : d.pipe) cudaEventDestroy(e);
+  for (cudaStream_t s : {d.stream, d.s_h2d, d.s_d2h})
+    if (s) cudaStreamDestroy(s);
+}
+
+int validate_dims(const sse_dims* d) {
+  if (!d) return fail(SSE_EINVAL, "dims is NULL");
+  const int64_t v[7] = {d->nkz, d->nqz, d->ne, d->nw, d->na, d->nb, d->norb};
+  const char* names[7] = {"n_kz", "n_qz", "n_E", "n_w", "n_A", "n_B", "n_orb"};
+  for (int i = 0; i < 7; ++i)
+    if (v[i] < 1) return fail(SSE_EINVAL, "%s must be >= 1, got %lld", names[i], (long long)v[i]);
+  if (d->nb > (1 << 20) || d->norb > 64 || d->nw > (1 << 20) || d->nkz > (1 << 16) ||
+      d->nqz > (1 << 16) || d->na > (1LL << 30))
+    return fail(SSE_EINVAL, "dimension out of supported range");
+  if (d->ne * d->norb > (1LL << 30)) return fail(SSE_EINVAL, "n_E * n_orb too large");
+  return SSE_OK;
+}
+
+int validate_grid(const sse_dims* d, const int64_t* off, const double* wt) {
+  if (!off || !wt) return fail(SSE_EINVAL, "frequency map is NULL");
+  for (int64_t w = 0; w < d->nw; ++w) {
+    if (off[w] < 0 || off[w] >= d->ne)
+      return fail(SSE_EINVAL, "frequency offset %lld (index %lld) outside [0, %lld)",
+                  (long long)off[w], (long long)w, (long long)d->ne);
+    if (!std::isfinite(wt[w]))
+      return fail(SSE_EINVAL, "frequency weight %g (index %lld) is not finite", wt[w], (long long)w);
+  }
+  return SSE_OK;
+}
+
+int validate_slab(const sse_dims* d, const sse_slab* s, const char* what) {
+  if (!s) return fail(SSE_EINVAL, "%s slab is NULL", what);
+  if (s->natoms < 1 || s->atom0 < 0 || s->atom0 + s->natoms > d->na)
+    return fail(SSE_EINVAL, "%s slab [%lld, %lld) outside [0, %lld)", what, (long long)s->atom0,
+                (long long)(s->atom0 + s->natoms), (long long)d->na);
+  return SSE_OK;
+}
+
+// Operator chunk: bound the per-polarity operator buffer to ~1 GiB.
+int64_t op_chunk_atoms(const sse_dims* d) {
+  const size_t per_atom = sse::operator_bytes((int)d->norb, (int)d->nb, (int)d->nqz, (int)d->nw, 1);
+  return std::max<int64_t>(1, (int64_t)((1ull << 30) / std::max<size_t>(per_atom, 1)));
+}
+
+struct SlabStrides {
+  long long sa, sk, se;
+};
+SlabStrides strides_of(const sse_dims* d, const sse_slab& slab) {
+  const long long no2 = d->norb * d->norb;
+  if (slab.atom_major) return {d->nkz * d->ne * no2, d->ne * no2, no2};
+  return {no2, d->ne * slab.natoms * no2, slab.natoms * no2};
+}
+
+double alg_flops(const sse_dims* d, const int64_t* off, int64_t natoms, int npol = 2) {
+  double terms = 0;
+  for (int64_t w = 0; w < d->nw; ++w) terms += (double)std::max<int64_t>(0, d->ne - off[w]);
+  const double no3 = (double)d->norb * d->norb * d->norb;
+  return 8.0 * npol * natoms * d->nb * d->nkz * d->nqz * no3 * terms;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Upload the neighbour (G-slab local), offset and weight tables of an owned range.
+int prepare_tables(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
+                   const int64_t* nmap, const int64_t* off, const double* wt, cudaStream_t st) {
+  std::vector<int> nbr((size_t)out.natoms * d->nb);
+  for (int64_t a = 0; a < out.natoms; ++a)
+    for (int64_t s = 0; s < d->nb; ++s) {
+      const int64_t b = nmap[a * d->nb + s];
+      if (b < 0 || b >= d->na)
+        return fail(SSE_EINVAL, "neighbor index %lld of atom %lld outside [0, %lld)", (long long)b,
+                    (long long)(out.atom0 + a), (long long)d->na);
+      if (b < g.atom0 || b >= g.atom0 + g.natoms)
+        return fail(SSE_EINVAL, "neighbor atom %lld of atom %lld is not in the G slab [%lld, %lld)",
+                    (long long)b, (long long)(out.atom0 + a), (long long)g.atom0,
+                    (long long)(g.atom0 + g.natoms));
+      nbr[a * d->nb + s] = (int)(b - g.atom0);
+    }
+  std::vector<int> offs(d->nw);
+  for (int64_t w = 0; w < d->nw; ++w) offs[w] = (int)off[w];
+  std::vector<double> wts(wt, wt + d->nw);
+  CHECK(upload_cached(ds.nbr, ds.nbr_host, nbr, st));
+  CHECK(upload_cached(ds.off, ds.off_host, offs, st));
+  CHECK(upload_cached(ds.wt, ds.wt_host, wts, st));
+  return SSE_OK;
+}
+
+struct DevPtrs {
+  const double2 *G_l, *G_g, *Dc_l, *Dc_g, *dH;
+  double2 *S_l, *S_g;
+};
+
+// K2 + K3 for owned atoms [a0, a0 + n) of the out slab (tables already uploaded).
+int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
+              const DevPtrs& p, const int64_t* off, int64_t a0, int64_t n, cudaStream_t st,
+              int npol, int* launches) {
+  const int no = (int)d->norb;
+  const size_t opb = sse::operator_bytes(no, (int)d->nb, (int)d->nqz, (int)d->nw, (int)n);
+  CHECK(ds.op[0].ensure(opb));
+  CHECK(ds.op[1].ensure(opb));
+  sse::OperatorArgs oa{};
+  oa.Dc[0] = p.Dc_l;
+  oa.Dc[1] = p.Dc_g;
+  oa.dH = p.dH;
+  oa.wt = ds.wt.as<double>();
+  oa.M[0] = ds.op[0].as<double2>();
+  oa.M[1] = ds.op[1].as<double2>();
+  oa.nqz = (int)d->nqz;
+  oa.nw = (int)d->nw;
+  oa.nb = (int)d->nb;
+  oa.no = no;
+  oa.dc_natoms = (int)out.natoms;
+  oa.atom_begin = (int)a0;
+  oa.chunk_atoms = (int)n;
+  oa.fragment_order = no <= sse::kMaxDmmaOrb ? 1 : 0;
+  oa.npol = npol;
+  CHECK(profiled(ds, st, SSE_PROF_OPERATOR, 0.0, [&] { return sse::launch_build_operator(oa, st); }));
+
+  const SlabStrides gs = strides_of(d, g), ss = strides_of(d, out);
+  sse::SigmaArgs sa{};
+  sa.G[0] = p.G_l;
+  sa.G[1] = p.G_g;
+  sa.M[0] = oa.M[0];
+  sa.M[1] = oa.M[1];
+  sa.S[0] = p.S_l;
+  sa.S[1] = p.S_g;
+  sa.nbr = ds.nbr.as<int>() + a0 * d->nb;
+  sa.off = ds.off.as<int>();
+  sa.nkz = (int)d->nkz;
+  sa.nqz = (int)d->nqz;
+  sa.ne = (int)d->ne;
+  sa.nw = (int)d->nw;
+  sa.nb = (int)d->nb;
+  sa.no = no;
+  sa.rows = (int)(d->ne * no);
+  sa.s_atom_begin = (int)a0;
+  sa.g_sa = gs.sa;
+  sa.g_sk = gs.sk;
+  sa.g_se = gs.se;
+  sa.s_sa = ss.sa;
+  sa.s_sk = ss.sk;
+  sa.s_se = ss.se;
+  sa.npol = npol;
+  CHECK(profiled(ds, st, SSE_PROF_SIGMA, alg_flops(d, off, n, npol),
+                 [&] { return sse::launch_sigma(sa, (int)n, st); }));
+  if (launches) *launches += 2;
+  return SSE_OK;
+}
+
+int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
+                    const DevPtrs& p, const int64_t* nmap, const int64_t* off, const double* wt,
+                    cudaStream_t st, int* launches, int npol = 2) {
+  CHECK(prepare_tables(ds, d, g, out, nmap, off, wt, st));
+  const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d), out.natoms);
+  for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk)
+    CHECK(run_chunk(ds, d, g, out, p, off, a0, std::min<int64_t>(chunk, out.natoms - a0), st, npol,
+                    launches));
+  return SSE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-memory call
+// ---------------------------------------------------------------------------
+struct HostCall {
+  const sse_dims* d;
+  int variant;
+  sse_slab hg, hs;  // host G slab and host out slab (grid-major)
+  const double *G_l, *G_g, *Dc_l, *Dc_g, *dH;
+  const int64_t *nmap, *off;  // nmap rows of hs atoms
+  const double* wt;
+  double *S_l, *S_g;
+};
+
+cudaEvent_t pipe_event(DevState& ds, size_t i) {
+  while (ds.pipe.size() <= i) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    ds.pipe.push_back(e);
+  }
+  return ds.pipe[i];
+}
+
+// One device's share of a host-memory call: owned atoms [lo, hi) (global ids).
+int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi, sse_timing* t) {
+  const sse_dims* d = c.d;
+  CU(cudaSetDevice(ds.device));
+  const int64_t on = hi - lo;
+  if (on <= 0) return SSE_OK;
+  const int64_t* rows_nmap = c.nmap + (lo - c.hs.atom0) * d->nb;
+  int64_t glo = lo, ghi = hi;
+  for (int64_t i = 0; i < on * d->nb; ++i) {
+    const int64_t b = rows_nmap[i];
+    if (b < 0 || b >= d->na)
+      return fail(SSE_EINVAL, "neighbor index %lld of atom %lld outside [0, %lld)", (long long)b,
+                  (long long)(lo + i / d->nb), (long long)d->na);
+    glo = std::min(glo, b);
+    ghi = std::max(ghi, b + 1);
+  }
+  if (glo < c.hg.atom0 || ghi > c.hg.atom0 + c.hg.natoms)
+    return fail(SSE_EINVAL, "host G slab [%lld, %lld) lacks neighbour atoms [%lld, %lld)",
+                (long long)c.hg.atom0, (long long)(c.hg.atom0 + c.hg.natoms), (long long)glo,
+                (long long)ghi);
+  const int64_t gn = ghi - glo;
+  const size_t blk = (size_t)d->norb * d->norb * 16;  // bytes per (k, E, atom) block
+  const size_t rows = (size_t)(d->nkz * d->ne);
+  const size_t dc_row = (size_t)d->nb * 9 * 16, dc_rows = (size_t)(d->nqz * d->nw);
+  const size_t dh_atom = (size_t)d->nb * 3 * blk;
+  const size_t g_bytes = rows * gn * blk, s_bytes = rows * on * blk;
+  const size_t dc_bytes = dc_rows * on * dc_row, dh_bytes = on * dh_atom;
+  const size_t hg_pitch = c.hg.natoms * blk, hs_pitch = c.hs.natoms * blk;
+  const size_t hdc_pitch = c.hs.natoms * dc_row;
+  const char* Gh[2] = {(const char*)c.G_l, (const char*)c.G_g};
+  const char* Dh[2] = {(const char*)c.Dc_l, (const char*)c.Dc_g};
+  char* Sh[2] = {(char*)c.S_l, (char*)c.S_g};
+  const char* dHh = (const char*)c.dH + (lo - c.hs.atom0) * dh_atom;
+  const bool am = c.variant == SSE_VARIANT_LAYOUT_TRANSFORMED;
+
+  for (int p = 0; p < 2; ++p) {
+    CHECK(ds.g[p].ensure(g_bytes));
+    CHECK(ds.s[p].ensure(s_bytes));
+    CHECK(ds.dc[p].ensure(dc_bytes));
+  }
+  CHECK(ds.dh.ensure(dh_bytes));
+  cudaStream_t st = ds.stream;
+  sse_slab gslab{glo, gn, 0, 0}, oslab{lo, on, 0, 0};
+  int launches = 0;
+  CU(cudaEventRecord(ds.ev[0], st));
+
+  if (am) {
+    // LAYOUT_TRANSFORMED (sse.py:244-261): copy everything, K1 to atom-major,
+    // atom-major accumulation, K1 back; polarities one after the other.
+    CHECK(ds.tmp_g.ensure(g_bytes));
+    CHECK(ds.tmp_s.ensure(s_bytes));
+    for (int p = 0; p < 2; ++p) {
+      CU(cudaMemcpy2DAsync(ds.g[p].ptr, gn * blk, Gh[p] + (glo - c.hg.atom0) * blk, hg_pitch,
+                           gn * blk, rows, cudaMemcpyHostToDevice, st));
+      CU(cudaMemcpy2DAsync(ds.dc[p].ptr, on * dc_row, Dh[p] + (lo - c.hs.atom0) * dc_row, hdc_pitch,
+                           on * dc_row, dc_rows, cudaMemcpyHostToDevice, st));
+    }
+    CU(cudaMemcpyAsync(ds.dh.ptr, dHh, dh_bytes, cudaMemcpyHostToDevice, st));
+    sse_slab ga{glo, gn, 1, 0}, oa{lo, on, 1, 0};
+    CHECK(prepare_tables(ds, d, ga, oa, rows_nmap, c.off, c.wt, st));
+    for (int p = 0; p < 2; ++p) {
+      CHECK(profiled(ds, st, SSE_PROF_LAYOUT, 0.0, [&] {
+        return sse::launch_layout_transform(d->nkz, d->ne, gn, d->norb * d->norb, 1,
+                                            ds.g[p].as<double2>(), ds.tmp_g.as<double2>(), st);
+      }));
+      DevPtrs ptr{ds.tmp_g.as<double2>(), ds.tmp_g.as<double2>(), ds.dc[p].as<double2>(),
+                  ds.dc[p].as<double2>(), ds.dh.as<double2>(), ds.tmp_s.as<double2>(),
+                  ds.tmp_s.as<double2>()};
+      const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d), on);
+      for (int64_t a0 = 0; a0 < on; a0 += chunk)
+        CHECK(run_chunk(ds, d, ga, oa, ptr, c.off, a0, std::min<int64_t>(chunk, on - a0), st, 1,
+                        &launches));
+      CHECK(profiled(ds, st, SSE_PROF_LAYOUT, 0.0, [&] {
+        return sse::launch_layout_transform(d->nkz, d->ne, on, d->norb * d->norb, 0,
+                                            ds.tmp_s.as<double2>(), ds.s[p].as<double2>(), st);
+      }));
+      launches += 2;
+    }
+    for (int p = 0; p < 2; ++p)
+      CU(cudaMemcpy2DAsync(Sh[p] + (lo - c.hs.atom0) * blk, hs_pitch, ds.s[p].ptr, on * blk,
+                           on * blk, rows, cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(ds.ev[1], st));
+  } else {
+    // pipelined over chunks of owned atoms
+    CHECK(prepare_tables(ds, d, gslab, oslab, rows_nmap, c.off, c.wt, st));
+    CU(cudaEventRecord(ds.ev[2], st));
+    CU(cudaStreamWaitEvent(ds.s_h2d, ds.ev[2], 0));
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(op_chunk_atoms(d), (on + 7) / 8));
+    const DevPtrs ptr{ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dc[0].as<double2>(),
+                      ds.dc[1].as<double2>(), ds.dh.as<double2>(), ds.s[0].as<double2>(),
+                      ds.s[1].as<double2>()};
+    int64_t copied = glo;  // G columns [glo, copied) are on their way
+    size_t ei = 0;
+    for (int64_t a0 = 0; a0 < on; a0 += chunk) {
+      const int64_t n = std::min<int64_t>(chunk, on - a0);
+      int64_t need = copied;
+      for (int64_t i = a0 * d->nb; i < (a0 + n) * d->nb; ++i) need = std::max(need, rows_nmap[i] + 1);
+      need = std::max(need, lo + a0 + n);
+      if (need > copied) {
+        for (int p = 0; p < 2; ++p)
+          CU(cudaMemcpy2DAsync((char*)ds.g[p].ptr + (copied - glo) * blk, gn * blk,
+                               Gh[p] + (copied - c.hg.atom0) * blk, hg_pitch, (need - copied) * blk,
+                               rows, cudaMemcpyHostToDevice, ds.s_h2d));
+        copied = need;
+      }
+      for (int p = 0; p < 2; ++p)
+        CU(cudaMemcpy2DAsync((char*)ds.dc[p].ptr + a0 * dc_row, on * dc_row,
+                             Dh[p] + (lo + a0 - c.hs.atom0) * dc_row, hdc_pitch, n * dc_row, dc_rows,
+                             cudaMemcpyHostToDevice, ds.s_h2d));
+      CU(cudaMemcpyAsync((char*)ds.dh.ptr + a0 * dh_atom, dHh + a0 * dh_atom, n * dh_atom,
+                         cudaMemcpyHostToDevice, ds.s_h2d));
+      cudaEvent_t in = pipe_event(ds, ei++), done = pipe_event(ds, ei++);
+      if (!in || !done) return fail(SSE_ECUDA, "event creation failed");
+      CU(cudaEventRecord(in, ds.s_h2d));
+      CU(cudaStreamWaitEvent(st, in, 0));
+      CHECK(run_chunk(ds, d, gslab, oslab, ptr, c.off, a0, n, st, 2, &launches));
+      CU(cudaEventRecord(done, st));
+      CU(cudaStreamWaitEvent(ds.s_d2h, done, 0));
+      for (int p = 0; p < 2; ++p)
+        CU(cudaMemcpy2DAsync(Sh[p] + (lo + a0 - c.hs.atom0) * blk, hs_pitch,
+                             (char*)ds.s[p].ptr + a0 * blk, on * blk, n * blk, rows,
+                             cudaMemcpyDeviceToHost, ds.s_d2h));
+    }
+    CU(cudaEventRecord(ds.ev[3], ds.s_d2h));
+    CU(cudaStreamWaitEvent(st, ds.ev[3], 0));
+    CU(cudaEventRecord(ds.ev[1], st));
+  }
+  CU(cudaEventSynchronize(ds.ev[1]));
+  if (t) {
+    t->total_ms = std::max(t->total_ms, (double)elapsed(ds.ev[0], ds.ev[1]));
+    t->h2d_bytes += 2 * (g_bytes + dc_bytes) + dh_bytes;
+    t->d2h_bytes += 2 * s_bytes;
+    t->kernel_launches += launches;
+  }
+  return SSE_OK;
+}
+
+int host_call(sse_ctx* ctx, const HostCall& c, sse_timing* t) {
+  const sse_dims* d = c.d;
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->flops = alg_flops(d, c.off, c.hs.natoms);
+  }
+  const int nd = (int)ctx->devs.size();
+  if (t) t->n_devices = nd;
+  const int64_t per = (c.hs.natoms + nd - 1) / nd;  // ceil-division chunks (distsim.py:117-120)
+  if (nd == 1) return host_call_on_device(ctx->devs[0], c, c.hs.atom0, c.hs.atom0 + c.hs.natoms, t);
+  std::vector<int> rcs(nd, SSE_OK);
+  std::vector<sse_timing> ts(nd);
+  std::vector<std::string> errs(nd);
+  std::vector<std::thread> th;
+  for (int i = 0; i < nd; ++i) {
+    th.emplace_back([&, i] {
+      std::memset(&ts[i], 0, sizeof(sse_timing));
+      const int64_t lo = c.hs.atom0 + std::min<int64_t>(i * per, c.hs.natoms);
+      const int64_t hi = c.hs.atom0 + std::min<int64_t>((i + 1) * per, c.hs.natoms);
+      rcs[i] = host_call_on_device(ctx->devs[i], c, lo, hi, &ts[i]);
+      if (rcs[i] != SSE_OK) errs[i] = g_last_error;
+    });
+  }
+  for (auto& x : th) x.join();
+  for (int i = 0; i < nd; ++i) {
+    if (rcs[i] != SSE_OK) {
+      g_last_error = errs[i];
+      return rcs[i];
+    }
+    if (t) {
+      t->total_ms = std::max(t->total_ms, ts[i].total_ms);
+      t->h2d_bytes += ts[i].h2d_bytes;
+      t->d2h_bytes += ts[i].d2h_bytes;
+      t->kernel_launches += ts[i].kernel_launches;
+    }
+  }
+  return SSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sse_last_error(void) { return g_last_error.c_str(); }
+
+int sse_version(void) { return 1; }
+
+int sse_ctx_create(int n_gpus, sse_ctx** out) {
+  if (!out) return fail(SSE_EINVAL, "out is NULL");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(SSE_ECUDA, "no CUDA device available (%s); libsse has no CPU fallback",
+                cudaGetErrorString(e));
+  if (n_gpus < 1 || n_gpus > count)
+    return fail(SSE_EINVAL, "n_gpus=%d but %d device(s) visible", n_gpus, count);
+  sse_ctx* ctx = new sse_ctx;
+  ctx->devs.resize(n_gpus);
+  for (int i = 0; i < n_gpus; ++i) {
+    int rc = init_dev(ctx->devs[i], i);
+    if (rc != SSE_OK) {
+      sse_ctx_destroy(ctx);
+      return rc;
+    }
+  }
+  *out = ctx;
+  return SSE_OK;
+}
+
+int sse_ctx_create_on(int device, sse_ctx** out) {
+  if (!out) return fail(SSE_EINVAL, "out is NULL");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(SSE_ECUDA, "no CUDA device available (%s); libsse has no CPU fallback",
+                cudaGetErrorString(e));
+  if (device < 0 || device >= count)
+    return fail(SSE_EINVAL, "device %d but %d device(s) visible", device, count);
+  sse_ctx* ctx = new sse_ctx;
+  ctx->devs.resize(1);
+  int rc = init_dev(ctx->devs[0], device);
+  if (rc != SSE_OK) {
+    sse_ctx_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return SSE_OK;
+}
+
+void sse_ctx_destroy(sse_ctx* ctx) {
+  if (!ctx) return;
+  for (auto& d : ctx->devs) destroy_dev(d);
+  delete ctx;
+}
+
+int sse_sigma_c128_slab(sse_ctx* ctx, const sse_dims* d, int variant, const sse_slab* g,
+                        const sse_slab* out, const double* G_l, const double* G_g,
+                        const double* Dc_l, const double* Dc_g, const double* dH,
+                        const int64_t* nmap, const int64_t* off, const double* wt, double* Sig_l,
+                        double* Sig_g, sse_timing* t) {
+  if (!ctx) return fail(SSE_EINVAL, "context is NULL");
+  CHECK(validate_dims(d));
+  CHECK(validate_grid(d, off, wt));
+  CHECK(validate_slab(d, g, "G"));
+  CHECK(validate_slab(d, out, "output"));
+  if (g->atom_major || out->atom_major)
+    return fail(SSE_EINVAL, "host slabs must be grid-major (the reference layout)");
+  if (variant < SSE_VARIANT_REFERENCE || variant > SSE_VARIANT_BATCHED_FUSED)
+    return fail(SSE_EINVAL, "unknown variant %d", variant);
+  if (!G_l || !G_g || !Dc_l || !Dc_g || !dH || !nmap || !Sig_l || !Sig_g)
+    return fail(SSE_EINVAL, "NULL tensor pointer");
+  HostCall c{d, variant, *g, *out, G_l, G_g, Dc_l, Dc_g, dH, nmap, off, wt, Sig_l, Sig_g};
+  return host_call(ctx, c, t);
+}
+
+int sse_sigma_c128(sse_ctx* ctx, const sse_dims* d, int variant, const double* G_l,
+                   const double* G_g, const double* Dc_l, const double* Dc_g, const double* dH,
+                   const int64_t* nmap, const int64_t* off, const double* wt, double* Sig_l,
+                   double* Sig_g, sse_timing* t) {
+  CHECK(validate_dims(d));
+  const sse_slab full{0, d->na, 0, 0};
+  return sse_sigma_c128_slab(ctx, d, variant, &full, &full, G_l, G_g, Dc_l, Dc_g, dH, nmap, off, wt,
+                             Sig_l, Sig_g, t);
+}
+
+int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
+                     const double* G_l, const double* G_g, const double* Dc_l, const double* Dc_g,
+                     const double* dH, const int64_t* nmap, const int64_t* off, const double* wt,
+                     double* Sig_l, double* Sig_g, void* stream, sse_timing* t) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
+  CHECK(validate_dims(d));
+  CHECK(validate_grid(d, off, wt));
+  CHECK(validate_slab(d, g, "G"));
+  CHECK(validate_slab(d, out, "output"));
+  if (!G_l || !G_g || !Dc_l || !Dc_g || !dH || !nmap || !Sig_l || !Sig_g)
+    return fail(SSE_EINVAL, "NULL tensor pointer");
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->flops = alg_flops(d, off, out->natoms);
+    t->n_devices = 1;
+    CU(cudaEventRecord(ds.ev[0], st));
+  }
+  int launches = 0;
+  const DevPtrs p{(const double2*)G_l, (const double2*)G_g, (const double2*)Dc_l,
+                  (const double2*)Dc_g, (const double2*)dH, (double2*)Sig_l, (double2*)Sig_g};
+  CHECK(sigma_on_device(ds, d, *g, *out, p, nmap, off, wt, st, &launches));
+  if (t) {
+    CU(cudaEventRecord(ds.ev[1], st));
+    CU(cudaEventSynchronize(ds.ev[1]));
+    t->sigma_ms = t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
+    t->kernel_launches = launches;
+  }
+  return SSE_OK;
+}
+
+int sse_layout_transform(sse_ctx* ctx, int64_t nkz, int64_t ne, int64_t na, int64_t block_doubles,
+                         int to_atom_major, const double* src, double* dst, void* stream) {
+  if (!ctx || ctx->devs.empty()) return fail(SSE_EINVAL, "context is NULL");
+  if (nkz < 1 || ne < 1 || na < 1 || block_doubles < 2 || block_doubles % 2)
+    return fail(SSE_EINVAL, "invalid layout-transform shape");
+  if (!src || !dst || src == dst) return fail(SSE_EINVAL, "layout transform needs distinct buffers");
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  CHECK(profiled(ds, st, SSE_PROF_LAYOUT, 0.0, [&] {
+    return sse::launch_layout_transform(nkz, ne, na, block_doubles / 2, to_atom_major,
+                                        (const double2*)src, (double2*)dst, st);
+  }));
+  if (!stream) CU(cudaStreamSynchronize(st));
+  return SSE_OK;
+}
+
+int sse_preprocess_D(sse_ctx* ctx, int64_t nqz, int64_t nw, int64_t na, int64_t nb,
+                     const int64_t* nmap, int64_t d_atom0, int64_t d_natoms, int64_t out_atom0,
+                     int64_t out_natoms, const double* D, double* Dc, void* stream) {
+  if (!ctx || ctx->devs.empty()) return fail(SSE_EINVAL, "context is NULL");
+  if (nqz < 1 || nw < 1 || na < 1 || nb < 1 || !nmap || !D || !Dc || d_natoms < 1 ||
+      out_natoms < 1 || d_atom0 < 0 || out_atom0 < 0 || d_atom0 + d_natoms > na ||
+      out_atom0 + out_natoms > na)
+    return fail(SSE_EINVAL, "invalid preprocess_D arguments");
+  // reverse-slot table of the owned edges (device.py:53-66): first r with idx[b, r] == a
+  std::vector<int> nbr(out_natoms * nb), rev(out_natoms * nb);
+  auto in_slab = [&](int64_t x) { return x >= d_atom0 && x < d_atom0 + d_natoms; };
+  for (int64_t la = 0; la < out_natoms; ++la) {
+    const int64_t a = out_atom0 + la;
+    if (!in_slab(a)) return fail(SSE_EINVAL, "atom %lld is not in the D slab", (long long)a);
+    for (int64_t s = 0; s < nb; ++s) {
+      const int64_t b = nmap[a * nb + s];
+      if (b < 0 || b >= na)
+        return fail(SSE_EINVAL, "neighbor index %lld of atom %lld outside [0, %lld)", (long long)b,
+                    (long long)a, (long long)na);
+      int64_t r = 0;
+      while (r < nb && nmap[b * nb + r] != a) ++r;
+      if (r == nb)
+        return fail(SSE_EINVAL, "missing neighbor slot: atom %lld not in neighbor list of %lld",
+                    (long long)a, (long long)b);
+      if (!in_slab(b)) return fail(SSE_EINVAL, "neighbor atom %lld is not in the D slab", (long long)b);
+      nbr[la * nb + s] = (int)(b - d_atom0);
+      rev[la * nb + s] = (int)r;
+    }
+  }
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  CHECK(upload_cached(ds.pp_nbr, ds.pp_nbr_host, nbr, st));
+  CHECK(upload_cached(ds.pp_rev, ds.pp_rev_host, rev, st));
+  CHECK(profiled(ds, st, SSE_PROF_PREPROCESS, 0.0, [&] {
+    return sse::launch_preprocess_D(nqz, nw, d_natoms, d_atom0, out_atom0, out_natoms, nb,
+                                    ds.pp_nbr.as<int>(), ds.pp_rev.as<int>(), (const double2*)D,
+                                    (double2*)Dc, st);
+  }));
+  if (!stream) CU(cudaStreamSynchronize(st));
+  return SSE_OK;
+}
+
+int sse_fill_synthetic(sse_ctx* ctx, uint64_t seed, uint32_t tensor_id, int64_t atom0,
+                       int64_t natoms, int64_t outer, int64_t inner, int64_t atom_stride,
+                       int64_t outer_stride, double scale, double* dst, void* stream) {
+  if (!ctx || ctx->devs.empty()) return fail(SSE_EINVAL, "context is NULL");
+  if (atom0 < 0 || natoms < 0 || outer < 1 || inner < 1 || !dst)
+    return fail(SSE_EINVAL, "invalid fill arguments");
+  if (natoms == 0) return SSE_OK;
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  CU(sse::launch_fill_synthetic(seed, tensor_id, atom0, natoms, outer, inner, atom_stride,
+                                outer_stride, scale, (double2*)dst, st));
+  if (!stream) CU(cudaStreamSynchronize(st));
+  return SSE_OK;
+}
+
+int sse_profile_begin(sse_ctx* ctx) {
+  if (!ctx) return fail(SSE_EINVAL, "context is NULL");
+  for (auto& ds : ctx->devs) {
+    ds.profiling = true;
+    ds.pool_used = 0;
+    ds.recs.clear();
+  }
+  return SSE_OK;
+}
+
+int sse_profile_end(sse_ctx* ctx, sse_profile* out) {
+  if (!ctx || !out) return fail(SSE_EINVAL, "NULL argument");
+  std::memset(out, 0, sizeof(*out));
+  for (auto& ds : ctx->devs) {
+    CU(cudaSetDevice(ds.device));
+    for (const ProfRec& r : ds.recs) {
+      CU(cudaEventSynchronize(r.b));
+      out->ms[r.kind] += elapsed(r.a, r.b);
+      out->launches[r.kind] += 1;
+      out->flops[r.kind] += r.flops;
+    }
+    ds.profiling = false;
+    ds.recs.clear();
+    ds.pool_used = 0;
+  }
+  return SSE_OK;
+}
+
+}  // extern "C"

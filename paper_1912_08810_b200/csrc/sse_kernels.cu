@@ -1,0 +1,450 @@
+// libsse kernels for B200 (sm_100a).
+//
+//   K1 layout transform      [Nkz,NE,NA,blk] <-> [NA,Nkz,NE,blk]    HBM-bound
+//   K2 operator build        M[q,w,a,s] = wt_w sum_ij Dc_ij dH_i@dH_j (fragment order)
+//   K3 fused Sigma kernel    Sigma[k,E,a] = i sum_{q,s,w} G[k-q,E-off_w,f(a,s)] @ M[q,w,a,s]
+//                            on FP64 tensor cores (mma.sync m8n8k4 -> DMMA.8x8x4)
+//   K3g generic Sigma        same contraction with DFMA, for No > kMaxDmmaOrb
+//   preprocess_D             Dc = D_ba - D_bb - D_aa + D_ab            (sse.py:91-115)
+//   fill_synthetic           atom-keyed counter-based inputs (bench / parity at scale)
+//
+// Reference semantics (sse.py:58-76, 127-161): momentum wraps mod Nkz, energy
+// terms with E - off_w < 0 are dropped, neighbour indirection f(a,s) = nmap[a,s],
+// final factor i.  The reassociation G@dH_i@Xi_i summed over i == G@M is exact
+// algebra; results agree with the reference to rounding (tests/).
+#include "sse_kernels.cuh"
+
+namespace sse {
+
+// --------------------------------------------------------------------------
+// K1: layout transform.  One warp per (k, E, a) block of blk_vec 16-byte
+// vectors; reads and writes are contiguous 16-byte runs per block.
+// --------------------------------------------------------------------------
+__global__ void layout_transform_kernel(long long nkz, long long ne, long long na, long long blk_vec,
+                                        int to_atom_major, const double2* __restrict__ src,
+                                        double2* __restrict__ dst) {
+  const long long nblocks = nkz * ne * na;
+  const int lane = threadIdx.x & 31;
+  long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (; warp < nblocks; warp += nwarps) {
+    // warp indexes the grid-major block (k, e, a)
+    const long long a = warp % na;
+    const long long ke = warp / na;             // k * ne + e
+    const long long am = a * (nkz * ne) + ke;   // atom-major block index
+    const long long from = to_atom_major ? warp : am;
+    const long long to = to_atom_major ? am : warp;
+    const double2* s = src + from * blk_vec;
+    double2* d = dst + to * blk_vec;
+    for (long long v = lane; v < blk_vec; v += 32) d[v] = __ldg(s + v);
+  }
+}
+
+// --------------------------------------------------------------------------
+// K2: operator build.  One CTA per (atom, neighbour slot) of the chunk:
+//   stage dH[a,s,0..2] and P_ij = dH_i @ dH_j (9 blocks) in shared memory,
+//   then every thread produces output doubles of
+//   M[q,w] = wt_w * sum_ij Dc[q,w,a,s,i,j] * P_ij
+// for both polarities, either in DMMA B-fragment order or compact [p][n].
+// --------------------------------------------------------------------------
+__global__ void build_operator_kernel(OperatorArgs p) {
+  extern __shared__ double2 smem[];
+  const int no = p.no, no2 = no * no;
+  double2* s_dh = smem;              // [3][no][no]
+  double2* s_p = smem + 3 * no2;     // [9][no][no]
+  const int la = blockIdx.x / p.nb;  // chunk-local atom
+  const int s = blockIdx.x % p.nb;
+  const int a_slab = p.atom_begin + la;
+
+  const double2* dh = p.dH + ((long long)a_slab * p.nb + s) * 3 * no2;
+  for (int x = threadIdx.x; x < 3 * no2; x += blockDim.x) s_dh[x] = dh[x];
+  __syncthreads();
+  for (int x = threadIdx.x; x < 9 * no2; x += blockDim.x) {
+    const int ij = x / no2, pn = x % no2;
+    const int i = ij / 3, j = ij % 3, pr = pn / no, n = pn % no;
+    double re = 0.0, im = 0.0;
+    for (int t = 0; t < no; ++t) {
+      const double2 u = s_dh[i * no2 + pr * no + t];
+      const double2 v = s_dh[j * no2 + t * no + n];
+      re = fma(u.x, v.x, re);
+      re = fma(-u.y, v.y, re);
+      im = fma(u.x, v.y, im);
+      im = fma(u.y, v.x, im);
+    }
+    s_p[x] = make_double2(re, im);
+  }
+  __syncthreads();
+
+  const FragGeom fg = frag_geom(no);
+  const int per_qw_vec = p.fragment_order ? fg.fv * 32 : no2;  // double2 per (q,w)
+  const long long qw_total = (long long)p.nqz * p.nw;
+  const long long out_base = (long long)blockIdx.x * qw_total * per_qw_vec;  // (la*nb+s)
+  for (int pol = 0; pol < p.npol; ++pol) {
+    const double2* dc_base = p.Dc[pol];
+    double2* out = p.M[pol] + out_base;
+    for (long long x = threadIdx.x; x < qw_total * per_qw_vec; x += blockDim.x) {
+      const int qw = (int)(x / per_qw_vec);
+      const int v = (int)(x % per_qw_vec);
+      const int q = qw / p.nw, w = qw % p.nw;
+      const double2* dc = dc_base + (((long long)(q * p.nw + w) * p.dc_natoms + a_slab) * p.nb + s) * 9;
+      const double wt = p.wt[w];
+      if (!p.fragment_order) {
+        double re = 0.0, im = 0.0;
+        for (int ij = 0; ij < 9; ++ij) {
+          const double2 c = dc[ij], m = s_p[ij * no2 + v];
+          re = fma(c.x, m.x, re);
+          re = fma(-c.y, m.y, re);
+          im = fma(c.x, m.y, im);
+          im = fma(c.y, m.x, im);
+        }
+        out[x] = make_double2(wt * re, wt * im);
+        continue;
+      }
+      // fragment order: v = j * 32 + lane, vector j holds fragments 2j, 2j+1,
+      // fragment f = kk * NT + nt; lane holds B'[4kk + (lane&3)][8nt + (lane>>2)].
+      const int j = v >> 5, lane = v & 31;
+      double vals[2];
+      for (int h = 0; h < 2; ++h) {
+        const int f = 2 * j + h;
+        const int kk = f / fg.nt, nt = f % fg.nt;
+        const int kr = 4 * kk + (lane & 3), nc = 8 * nt + (lane >> 2);
+        const bool im_row = kr >= fg.nop;
+        const int pr = im_row ? kr - fg.nop : kr;
+        const int n = nc >> 1, part = nc & 1;
+        double val = 0.0;
+        if (pr < no && n < no) {
+          double re = 0.0, im = 0.0;
+          for (int ij = 0; ij < 9; ++ij) {
+            const double2 c = dc[ij], m = s_p[ij * no2 + pr * no + n];
+            re = fma(c.x, m.x, re);
+            re = fma(-c.y, m.y, re);
+            im = fma(c.x, m.y, im);
+            im = fma(c.y, m.x, im);
+          }
+          re *= wt;
+          im *= wt;
+          // B'[re-row p][2n] = Re M, B'[re-row p][2n+1] = Im M,
+          // B'[im-row p][2n] = -Im M, B'[im-row p][2n+1] = Re M.
+          val = !im_row ? (part == 0 ? re : im) : (part == 0 ? -im : re);
+        }
+        vals[h] = val;
+      }
+      out[x] = make_double2(vals[0], vals[1]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K3: fused Sigma on FP64 tensor cores.
+// Grid: x = (row chunk, k, chunk atom), y = polarity.  Each warp owns
+// kRowTiles 8-row tiles of the [NE*No, No] output matrix of (atom, k) and
+// accumulates, in registers, over (q, s, w) in that fixed order the real-
+// embedded products  C' += A'(G rows shifted by off_w) * B'(M[q,w,a,s]).
+// Per (q,s,w) and tile: KH 16-byte A loads, FV 16-byte B loads shared by the
+// warp's tiles, KSTEPS*NT DMMAs.  Nothing but Sigma is written to HBM.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int NO>
+__global__ void __launch_bounds__(kSigmaWarps * 32)
+sigma_dmma_kernel(SigmaArgs p) {
+  constexpr FragGeom FG = frag_geom(NO);
+  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
+  const int pol = blockIdx.y;
+  int bx = blockIdx.x;
+  const int rc = bx % p.ctas_per_ak;
+  bx /= p.ctas_per_ak;
+  const int k = bx % p.nkz;
+  const int la = bx / p.nkz;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rbase = rc * kRowsPerCta + warp * (kRowTiles * 8);
+  const int pcol = lane & 3;
+
+  const double2* __restrict__ G = p.G[pol];
+  const double2* __restrict__ Mf = p.M[pol];
+
+  int e_row[kRowTiles], m_row[kRowTiles];
+  bool v_row[kRowTiles];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t) {
+    const int row = rbase + t * 8 + (lane >> 2);
+    v_row[t] = row < p.rows;
+    e_row[t] = row / NO;
+    m_row[t] = row - e_row[t] * NO;
+  }
+
+  double acc[kRowTiles][NT][2];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+
+  for (int q = 0; q < p.nqz; ++q) {
+    int kp = (k - q) % p.nkz;
+    if (kp < 0) kp += p.nkz;
+    for (int s = 0; s < p.nb; ++s) {
+      const int lb = __ldg(p.nbr + la * p.nb + s);
+      long long rowoff[kRowTiles];
+#pragma unroll
+      for (int t = 0; t < kRowTiles; ++t)
+        rowoff[t] = lb * p.g_sa + kp * p.g_sk + (long long)e_row[t] * p.g_se + m_row[t] * NO + pcol;
+      const double2* mf = Mf + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw) * (FV * 32) + lane;
+      for (int w = 0; w < p.nw; ++w) {
+        const int off = __ldg(p.off + w);
+        double2 bv[FV];
+#pragma unroll
+        for (int j = 0; j < FV; ++j) bv[j] = __ldg(mf + (w * FV + j) * 32);
+#pragma unroll
+        for (int t = 0; t < kRowTiles; ++t) {
+          const int tile_row0 = rbase + t * 8;
+          // warp-uniform skip: tile past the end, or every row has E < off
+          if (tile_row0 >= p.rows || (tile_row0 + 7) / NO < off) continue;
+          const bool ok = v_row[t] && e_row[t] >= off;
+          double2 av[KH];
+#pragma unroll
+          for (int kk = 0; kk < KH; ++kk) {
+            av[kk] = make_double2(0.0, 0.0);
+            if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO))
+              av[kk] = __ldg(G + rowoff[t] - (long long)off * p.g_se + 4 * kk);
+          }
+#pragma unroll
+          for (int kk = 0; kk < KSTEPS; ++kk) {
+            const double a = kk < KH ? av[kk].x : av[kk - KH].y;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const int f = kk * NT + nt;
+              const double b = (f & 1) ? bv[f >> 1].y : bv[f >> 1].x;
+              dmma884(acc[t][nt], a, b);
+            }
+          }
+        }
+      }
+    }
+  }
+
+  // epilogue: lane holds (Re, Im) of C[row][n = 4 nt + (lane & 3)]; Sigma = i C
+  double2* __restrict__ S = p.S[pol];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t) {
+    if (!v_row[t]) continue;
+    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
+                   (long long)e_row[t] * p.s_se + m_row[t] * NO;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int n = 4 * nt + (lane & 3);
+      if (n < NO) dst[n] = make_double2(-acc[t][nt][1], acc[t][nt][0]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K3g: generic Sigma with DFMA (any No).  One thread per output element
+// (k, E, atom, m, n); compact operator M[q,w][p][n]; same (q, s, w) order.
+// --------------------------------------------------------------------------
+__global__ void sigma_generic_kernel(SigmaArgs p, int chunk_atoms) {
+  const int no = p.no, no2 = no * no;
+  const long long per_atom = (long long)p.nkz * p.ne * no2;
+  const long long total = per_atom * chunk_atoms;
+  const int pol = blockIdx.y;
+  const double2* __restrict__ G = p.G[pol];
+  const double2* __restrict__ M = p.M[pol];
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const int la = (int)(x / per_atom);
+    long long r = x % per_atom;
+    const int n = (int)(r % no);
+    r /= no;
+    const int m = (int)(r % no);
+    r /= no;
+    const int e = (int)(r % p.ne);
+    const int k = (int)(r / p.ne);
+    double re = 0.0, im = 0.0;
+    for (int q = 0; q < p.nqz; ++q) {
+      int kp = (k - q) % p.nkz;
+      if (kp < 0) kp += p.nkz;
+      for (int s = 0; s < p.nb; ++s) {
+        const int lb = p.nbr[la * p.nb + s];
+        const double2* mq = M + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw) * no2;
+        for (int w = 0; w < p.nw; ++w) {
+          const int es = e - p.off[w];
+          if (es < 0) continue;
+          const double2* g = G + lb * p.g_sa + kp * p.g_sk + (long long)es * p.g_se + m * no;
+          const double2* mm = mq + (long long)w * no2 + n;
+          for (int t = 0; t < no; ++t) {
+            const double2 u = g[t], v = mm[t * no];
+            re = fma(u.x, v.x, re);
+            re = fma(-u.y, v.y, re);
+            im = fma(u.x, v.y, im);
+            im = fma(u.y, v.x, im);
+          }
+        }
+      }
+    }
+    double2* dst = p.S[pol] + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
+                   (long long)e * p.s_se + m * no + n;
+    *dst = make_double2(-im, re);
+  }
+}
+
+// --------------------------------------------------------------------------
+// preprocess_D (sse.py:105-113), same term order as the reference:
+//   Dc = D[b, 1+rev] - D[b, 0] - D[a, 0] + D[a, 1+s]
+// --------------------------------------------------------------------------
+__global__ void preprocess_D_kernel(long long nqw, long long d_natoms, long long d_atom0,
+                                    long long out_atom0, long long out_natoms, long long nb,
+                                    const int* __restrict__ nbr, const int* __restrict__ rev,
+                                    const double2* __restrict__ D, double2* __restrict__ Dc) {
+  const long long total = nqw * out_natoms * nb * 9;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const int ij = (int)(x % 9);
+    long long r = x / 9;
+    const long long s = r % nb;
+    r /= nb;
+    const long long la = r % out_natoms;
+    const long long qw = r / out_natoms;
+    const long long a = out_atom0 + la - d_atom0;  // D-slab index of a
+    const long long b = nbr[la * nb + s];          // D-slab index of f(a, s)
+    const long long rv = rev[la * nb + s];
+    const double2* base = D + qw * d_natoms * (nb + 1) * 9;
+    const double2 d_ba = base[(b * (nb + 1) + 1 + rv) * 9 + ij];
+    const double2 d_bb = base[(b * (nb + 1)) * 9 + ij];
+    const double2 d_aa = base[(a * (nb + 1)) * 9 + ij];
+    const double2 d_ab = base[(a * (nb + 1) + 1 + s) * 9 + ij];
+    const double re = __dadd_rn(__dsub_rn(__dsub_rn(d_ba.x, d_bb.x), d_aa.x), d_ab.x);
+    const double im = __dadd_rn(__dsub_rn(__dsub_rn(d_ba.y, d_bb.y), d_aa.y), d_ab.y);
+    Dc[x] = make_double2(re, im);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Atom-keyed synthetic inputs: splitmix64 counter hash -> Irwin-Hall(4) of
+// 16-bit digits, unit variance.  Integer sums are exact and there is a single
+// rounding per product, so inputs.atom_keyed (numpy) reproduces it bit-exactly.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double irwin_hall4(uint64_t h, double scale) {
+  const long long s = (long long)(h & 0xFFFF) + (long long)((h >> 16) & 0xFFFF) +
+                      (long long)((h >> 32) & 0xFFFF) + (long long)(h >> 48);
+  const double x = __dmul_rn((double)(s - 131070), 0x1.bb67ae86627e7p-16);
+  return __dmul_rn(x, scale);
+}
+
+__global__ void fill_synthetic_kernel(uint64_t seed, uint32_t tensor_id, long long atom0,
+                                      long long natoms, long long outer, long long inner,
+                                      long long atom_stride, long long outer_stride, double scale,
+                                      double2* __restrict__ dst) {
+  const long long per_atom = outer * inner;
+  const long long total = per_atom * natoms;
+  const uint64_t k0 = splitmix64(splitmix64(seed) ^ (uint64_t)tensor_id);
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long la = x / per_atom;
+    const long long local = x % per_atom;
+    const long long o = local / inner, i = local % inner;
+    const uint64_t key = splitmix64(k0 ^ (uint64_t)(atom0 + la));
+    const double re = irwin_hall4(splitmix64(key ^ (uint64_t)(2 * local)), scale);
+    const double im = irwin_hall4(splitmix64(key ^ (uint64_t)(2 * local + 1)), scale);
+    dst[la * atom_stride + o * outer_stride + i] = make_double2(re, im);
+  }
+}
+
+// --------------------------------------------------------------------------
+// launchers
+// --------------------------------------------------------------------------
+static int grid_for(long long work, int threads) {
+  long long g = (work + threads - 1) / threads;
+  const long long cap = 148LL * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+cudaError_t launch_layout_transform(long long nkz, long long ne, long long na, long long blk_vec,
+                                    int to_atom_major, const double2* src, double2* dst,
+                                    cudaStream_t st) {
+  const long long warps = nkz * ne * na;
+  layout_transform_kernel<<<grid_for(warps * 32, 256), 256, 0, st>>>(nkz, ne, na, blk_vec,
+                                                                     to_atom_major, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)12 * a.no * a.no * sizeof(double2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(build_operator_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  build_operator_kernel<<<a.chunk_atoms * a.nb, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NO>
+static void launch_dmma(const SigmaArgs& a, int chunk_atoms, cudaStream_t st) {
+  dim3 grid((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
+  sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
+}
+
+cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
+  SigmaArgs a = a0;
+  if (a.no <= kMaxDmmaOrb) {
+    a.ctas_per_ak = (a.rows + kRowsPerCta - 1) / kRowsPerCta;
+    switch (a.no) {
+      case 1: launch_dmma<1>(a, chunk_atoms, st); break;
+      case 2: launch_dmma<2>(a, chunk_atoms, st); break;
+      case 3: launch_dmma<3>(a, chunk_atoms, st); break;
+      case 4: launch_dmma<4>(a, chunk_atoms, st); break;
+      case 5: launch_dmma<5>(a, chunk_atoms, st); break;
+      case 6: launch_dmma<6>(a, chunk_atoms, st); break;
+      case 7: launch_dmma<7>(a, chunk_atoms, st); break;
+      case 8: launch_dmma<8>(a, chunk_atoms, st); break;
+      case 9: launch_dmma<9>(a, chunk_atoms, st); break;
+      case 10: launch_dmma<10>(a, chunk_atoms, st); break;
+      case 11: launch_dmma<11>(a, chunk_atoms, st); break;
+      case 12: launch_dmma<12>(a, chunk_atoms, st); break;
+      case 13: launch_dmma<13>(a, chunk_atoms, st); break;
+      case 14: launch_dmma<14>(a, chunk_atoms, st); break;
+      case 15: launch_dmma<15>(a, chunk_atoms, st); break;
+      case 16: launch_dmma<16>(a, chunk_atoms, st); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    const long long total = (long long)a.nkz * a.ne * a.no * a.no * chunk_atoms;
+    dim3 grid(grid_for(total, 256), a.npol);
+    sigma_generic_kernel<<<grid, 256, 0, st>>>(a, chunk_atoms);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess_D(long long nqz, long long nw, long long d_natoms, long long d_atom0,
+                                long long out_atom0, long long out_natoms, long long nb,
+                                const int* nbr, const int* rev, const double2* D, double2* Dc,
+                                cudaStream_t st) {
+  const long long total = nqz * nw * out_natoms * nb * 9;
+  preprocess_D_kernel<<<grid_for(total, 256), 256, 0, st>>>(nqz * nw, d_natoms, d_atom0, out_atom0,
+                                                            out_natoms, nb, nbr, rev, D, Dc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_synthetic(uint64_t seed, uint32_t tensor_id, long long atom0,
+                                  long long natoms, long long outer, long long inner,
+                                  long long atom_stride, long long outer_stride, double scale,
+                                  double2* dst, cudaStream_t st) {
+  const long long total = natoms * outer * inner;
+  fill_synthetic_kernel<<<grid_for(total, 256), 256, 0, st>>>(
+      seed, tensor_id, atom0, natoms, outer, inner, atom_stride, outer_stride, scale, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace sse

@@ -1,0 +1,82 @@
+// Kernel declarations and launch helpers for libsse (sm_100a).
+// See DESIGN.md for the data layout and the roofline of each kernel.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sse {
+
+// Largest orbital count served by the DMMA (tensor-core FP64) Sigma kernel.
+// Larger blocks use the DFMA fallback kernel.
+constexpr int kMaxDmmaOrb = 16;
+
+// Sigma kernel CTA shape: 8 warps, each owning kRowTiles 8-row tiles of the
+// per-(atom, k) output matrix [NE*No rows, No cols].
+constexpr int kSigmaWarps = 8;
+constexpr int kRowTiles = 3;
+constexpr int kRowsPerCta = kSigmaWarps * kRowTiles * 8;
+
+// Fragment geometry of the real embedding of an No x No complex block
+// product for mma.sync.m8n8k4.f64 (DMMA.8x8x4):
+//   A' = [Re G | Im G]          rows x 2*NOP  (K' order: real half, then imag)
+//   B' = [[Re M, Im M] interleaved per column; [-Im M, Re M]]  2*NOP x 2*No
+//   C' columns interleave (Re, Im) of each output column n.
+struct FragGeom {
+  int no, nop, ksteps, kh, nt, fr, fv;
+};
+__host__ __device__ constexpr FragGeom frag_geom(int no) {
+  return FragGeom{no, (no + 3) / 4 * 4, ((no + 3) / 4 * 4) / 2, ((no + 3) / 4 * 4) / 4,
+                  (2 * no + 7) / 8, (((no + 3) / 4 * 4) / 2) * ((2 * no + 7) / 8),
+                  (((no + 3) / 4 * 4) / 2) * ((2 * no + 7) / 8) / 2};
+}
+
+struct OperatorArgs {
+  const double2* Dc[2];   // [Nqz][Nw][dc_natoms][NB][3][3] (slab), per polarity
+  const double2* dH;      // [dh_natoms][NB][3][No][No]
+  const double* wt;       // [Nw] device
+  double2* M[2];          // output: fragment order or compact, per polarity
+  int nqz, nw, nb, no;
+  int dc_natoms;          // atoms in the Dc slab (its atom stride)
+  int atom_begin;         // first slab atom of this chunk
+  int chunk_atoms;
+  int fragment_order;     // 1: DMMA fragment order, 0: compact [p][n]
+  int npol;               // polarities to process (1 or 2)
+};
+
+struct SigmaArgs {
+  const double2* G[2];
+  const double2* M[2];    // operator of the chunk (layout per kernel)
+  double2* S[2];
+  const int* nbr;         // [chunk][NB] index of f(a,s) within the G slab
+  const int* off;         // [Nw]
+  int nkz, nqz, ne, nw, nb, no;
+  int rows;               // NE * No
+  int ctas_per_ak;
+  int s_atom_begin;       // Sigma slab atom of the chunk's first atom
+  long long g_sa, g_sk, g_se;  // G slab strides in complex elements
+  long long s_sa, s_sk, s_se;  // Sigma slab strides in complex elements
+  int npol;               // polarities to process (1 or 2)
+};
+
+cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st);
+cudaError_t launch_sigma(const SigmaArgs& a, int chunk_atoms, cudaStream_t st);
+cudaError_t launch_layout_transform(long long nkz, long long ne, long long na, long long blk_vec,
+                                    int to_atom_major, const double2* src, double2* dst,
+                                    cudaStream_t st);
+cudaError_t launch_preprocess_D(long long nqz, long long nw, long long d_natoms, long long d_atom0,
+                                long long out_atom0, long long out_natoms, long long nb,
+                                const int* nbr, const int* rev, const double2* D, double2* Dc,
+                                cudaStream_t st);
+cudaError_t launch_fill_synthetic(uint64_t seed, uint32_t tensor_id, long long atom0,
+                                  long long natoms, long long outer, long long inner,
+                                  long long atom_stride, long long outer_stride, double scale,
+                                  double2* dst, cudaStream_t st);
+
+// Bytes of the per-chunk operator buffer (one polarity).
+inline size_t operator_bytes(int no, int nb, int nqz, int nw, int chunk_atoms) {
+  size_t per = (no <= kMaxDmmaOrb) ? (size_t)frag_geom(no).fv * 32 : (size_t)no * no;
+  return per * 16 * (size_t)nb * nqz * nw * chunk_atoms;
+}
+
+}  // namespace sse

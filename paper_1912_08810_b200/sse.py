@@ -1,0 +1,358 @@
+"""Drop-in SSE electron self-energy on B200: ``sse_sigma`` and device helpers.
+
+``sse_sigma(variant, g, dc, dh, nmap, grid, counter=None)`` keeps the
+signature, argument meaning, array conventions and error behaviour of the
+reference entry point ``negflow.sse.sse_sigma`` (sse.py:305-329) and
+computes Sigma^{<>} with libsse's sm_100a kernels (K2 operator build, K3
+fused DMMA Sigma kernel; K1 layout transforms for LAYOUT_TRANSFORMED).
+There is no CPU path: without libsse.so and a B200 it raises.
+
+Device-resident entry points (torch CUDA tensors, used by the bench and the
+multi-GPU shard driver) are ``sigma_device``, ``layout_transform``,
+``preprocess_D_device`` and ``fill_synthetic``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _lib
+from .types import (
+    VARIANT_CODES,
+    CombinedD,
+    FlopCounter,
+    SelfEnergyTensor,
+    SseVariant,
+)
+
+Array = np.ndarray
+
+__all__ = [
+    "sse_sigma",
+    "sigma_tallies",
+    "sigma_device",
+    "layout_transform",
+    "preprocess_D_device",
+    "fill_synthetic",
+    "alg_flops",
+]
+
+
+def _resolve_variant(variant) -> SseVariant:
+    """Accept this package's or the reference's SseVariant (matched by value)."""
+    if isinstance(variant, SseVariant):
+        return variant
+    value = getattr(variant, "value", None)
+    for v in SseVariant:
+        if value == v.value:
+            return v
+    raise ValueError(f"unknown variant {variant!r}")
+
+
+def sigma_tallies(variant: SseVariant, n_kz, n_qz, n_e, n_w, n_a, n_b, n_o) -> dict[str, int]:
+    """Complex MAC tallies the reference FlopCounter records for Sigma.
+
+    add_matmul call sites sse.py:159-160 (REFERENCE), 183/213 (FISSIONED),
+    231/235/260 (REDUNDANCY_REMOVED / LAYOUT_TRANSFORMED), 289/301
+    (BATCHED_FUSED), both polarities.
+    """
+    base = 2 * 3 * n_a * n_b * n_kz * n_e * n_o**3
+    qw = n_qz * n_w
+    redundant = variant in (SseVariant.REFERENCE, SseVariant.FISSIONED)
+    return {"sigma.dhg": base * (qw if redundant else 1), "sigma.accumulate": base * qw}
+
+
+def alg_flops(n_kz, n_qz, n_e, n_a, n_b, n_o, offsets) -> int:
+    """F_alg = 16 NA NB Nkz Nqz No^3 sum_w max(0, NE - off_w) (both polarities)."""
+    terms = sum(max(0, n_e - int(o)) for o in offsets)
+    return 16 * n_a * n_b * n_kz * n_qz * n_o**3 * terms
+
+
+def _f64(arr: Array) -> Array:
+    return np.ascontiguousarray(arr, dtype=np.complex128)
+
+
+def _ptr(arr: Array):
+    return arr.ctypes.data_as(ctypes.c_void_p)
+
+
+def _default_gpus() -> int:
+    return int(os.environ.get("SSE_N_GPUS", "1"))
+
+
+def sse_sigma(
+    variant,
+    g,
+    dc,
+    dh: Array,
+    nmap,
+    grid,
+    counter: FlopCounter | None = None,
+    *,
+    n_gpus: int | None = None,
+    timing: dict | None = None,
+) -> SelfEnergyTensor:
+    """Electron self-energy Sigma^{<>} (drop-in for sse.py:305-329).
+
+    ``n_gpus`` (default ``$SSE_N_GPUS`` or 1) splits atoms over that many
+    devices of this process.  ``timing``, if given, is filled with the
+    library's per-call timing (milliseconds, bytes, flops).
+    """
+    if g.kind != "electron":
+        raise ValueError("sse_sigma expects an electron tensor")
+    if dc.lesser.shape[2:4] != (nmap.n_A, nmap.n_B):
+        raise ValueError("combined phonon tensor does not match the neighbor map")
+    var = _resolve_variant(variant)
+
+    g_l, g_g = g.lesser, g.greater
+    n_kz, n_e, n_a, n_o, n_o2 = g_l.shape
+    n_qz, n_w = dc.lesser.shape[:2]
+    n_b = nmap.n_B
+    if n_o != n_o2:
+        raise ValueError(f"electron blocks must be square, got {n_o}x{n_o2}")
+    if n_a != nmap.n_A:
+        raise ValueError(f"electron tensor has {n_a} atoms but the neighbor map has {nmap.n_A}")
+    if dc.lesser.shape[4:] != (3, 3):
+        raise ValueError("combined phonon tensor must end in 3x3 blocks")
+    dh = np.asarray(dh)
+    if dh.shape != (n_a, n_b, 3, n_o, n_o):
+        raise ValueError(f"dH must have shape {(n_a, n_b, 3, n_o, n_o)}, got {dh.shape}")
+    fmap = grid.frequency_map
+    if len(fmap) < n_w:
+        raise ValueError(f"frequency map has {len(fmap)} entries for n_w={n_w}")
+    offsets = np.array([int(fmap[w][0]) for w in range(n_w)], dtype=np.int64)
+    weights = np.array([float(fmap[w][1]) for w in range(n_w)], dtype=np.float64)
+
+    if counter is not None:
+        for stage, n in sigma_tallies(var, n_kz, n_qz, n_e, n_w, n_a, n_b, n_o).items():
+            counter.stages[stage] = counter.stages.get(stage, 0) + n
+
+    out_l = np.zeros(g_l.shape, dtype=np.complex128)
+    out_g = np.zeros(g_g.shape, dtype=np.complex128)
+    if out_l.size == 0 or dc.lesser.size == 0:
+        return SelfEnergyTensor(lesser=out_l, greater=out_g)
+
+    idx = np.ascontiguousarray(nmap.idx, dtype=np.int64)
+    if idx.size and (idx.min() < 0 or idx.max() >= n_a):
+        raise ValueError(f"neighbor map entries must lie in [0, {n_a})")
+    arrays = [_f64(g_l), _f64(g_g), _f64(dc.lesser), _f64(dc.greater), _f64(dh)]
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    tim = _lib.SseTiming()
+    ctx = _lib.context(n_gpus=n_gpus or _default_gpus())
+    rc = _lib.load().sse_sigma_c128(
+        ctx.handle,
+        ctypes.byref(dims),
+        VARIANT_CODES[var],
+        *[_ptr(a) for a in arrays],
+        _ptr(idx),
+        _ptr(offsets),
+        _ptr(weights),
+        _ptr(out_l),
+        _ptr(out_g),
+        ctypes.byref(tim),
+    )
+    _lib.check(rc)
+    if timing is not None:
+        timing.update(tim.as_dict())
+    return SelfEnergyTensor(lesser=out_l, greater=out_g)
+
+
+# ---------------------------------------------------------------------------
+# device-resident API (torch CUDA tensors, complex128)
+# ---------------------------------------------------------------------------
+
+
+def _dptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device API expects CUDA tensors")
+    if not t.is_contiguous():
+        raise ValueError("device API expects contiguous tensors")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _device_ctx(t):
+    return _lib.context(device=t.device.index if t.device.index is not None else 0)
+
+
+def sigma_device(
+    g_l,
+    g_g,
+    dc_l,
+    dc_g,
+    dh,
+    nmap_rows: Array,
+    offsets,
+    weights,
+    out_l,
+    out_g,
+    *,
+    n_a: int,
+    g_atom0: int = 0,
+    out_atom0: int = 0,
+    atom_major: bool = False,
+    stream=None,
+    sync_timing: bool = False,
+) -> dict | None:
+    """Sigma for an owned atom range, all tensors resident on one GPU.
+
+    g_*: [Nkz, NE, gA, No, No] (grid-major) or [gA, Nkz, NE, No, No]
+    (atom_major) holding atoms [g_atom0, g_atom0 + gA) — every f(a, s) of
+    the owned atoms.  out_*: same layout for the owned atoms
+    [out_atom0, out_atom0 + oA).  dc_*: [Nqz, Nw, oA, NB, 3, 3];
+    dh: [oA, NB, 3, No, No]; nmap_rows: host int64 [oA, NB] (global ids).
+    Launches on ``stream`` (default: torch's current stream) and returns
+    without synchronising unless ``sync_timing``.
+    """
+    if atom_major:
+        g_atoms, n_kz, n_e, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
+        o_atoms = out_l.shape[0]
+    else:
+        n_kz, n_e, g_atoms, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
+        o_atoms = out_l.shape[2]
+    n_qz, n_w, dc_atoms, n_b = dc_l.shape[:4]
+    if dc_atoms != o_atoms or dh.shape[0] != o_atoms:
+        raise ValueError("Dc/dH rows must match the owned atom count")
+    idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    if idx.shape != (o_atoms, n_b):
+        raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    wts = np.ascontiguousarray(weights, dtype=np.float64)
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    gs = _lib.SseSlab(g_atom0, g_atoms, int(atom_major), 0)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, int(atom_major), 0)
+    tim = _lib.SseTiming()
+    ctx = _device_ctx(g_l)
+    rc = _lib.load().sse_sigma_device(
+        ctx.handle, ctypes.byref(dims), ctypes.byref(gs), ctypes.byref(os_),
+        _dptr(g_l), _dptr(g_g), _dptr(dc_l), _dptr(dc_g), _dptr(dh),
+        _ptr(idx), _ptr(offs), _ptr(wts), _dptr(out_l), _dptr(out_g),
+        _stream_ptr(stream), ctypes.byref(tim) if sync_timing else None,
+    )
+    _lib.check(rc)
+    return tim.as_dict() if sync_timing else None
+
+
+def layout_transform(src, dst, to_atom_major: bool, stream=None) -> None:
+    """K1 (sse.py:48-55): [Nkz,NE,NA,No,No] <-> [NA,Nkz,NE,No,No] on the GPU."""
+    if to_atom_major:
+        n_kz, n_e, n_a = src.shape[:3]
+    else:
+        n_a, n_kz, n_e = src.shape[:3]
+    blk = int(np.prod(src.shape[3:])) * 2
+    rc = _lib.load().sse_layout_transform(
+        _device_ctx(src).handle, n_kz, n_e, n_a, blk, int(to_atom_major), _dptr(src), _dptr(dst),
+        _stream_ptr(stream),
+    )
+    _lib.check(rc)
+
+
+def preprocess_D_device(d, dc, nmap_idx: Array, *, d_atom0: int = 0, out_atom0: int = 0,
+                        stream=None) -> None:
+    """preprocess_D (sse.py:91-115) for one polarity on the GPU, raw D -> Dc.
+
+    d: [Nqz, Nw, dA, NB+1, 3, 3] holding atoms [d_atom0, d_atom0 + dA);
+    dc: [Nqz, Nw, oA, NB, 3, 3] for atoms [out_atom0, out_atom0 + oA);
+    nmap_idx: the full host map [NA, NB].
+    """
+    n_qz, n_w, d_atoms, n_slots = d.shape[:4]
+    o_atoms = dc.shape[2]
+    idx = np.ascontiguousarray(nmap_idx, dtype=np.int64)
+    if idx.ndim != 2 or n_slots != idx.shape[1] + 1:
+        raise ValueError(
+            f"missing neighbor slot: tensor has {n_slots - 1} slots for {idx.shape[-1]} neighbors"
+        )
+    rc = _lib.load().sse_preprocess_D(
+        _device_ctx(d).handle, n_qz, n_w, idx.shape[0], idx.shape[1], _ptr(idx), d_atom0, d_atoms,
+        out_atom0, o_atoms, _dptr(d), _dptr(dc), _stream_ptr(stream),
+    )
+    _lib.check(rc)
+
+
+def fill_synthetic(dst, seed: int, tensor_id: int, atom0: int, natoms: int, outer: int, inner: int,
+                   atom_stride: int, outer_stride: int, scale: float = 1.0, stream=None) -> None:
+    """Device side of :func:`paper_1912_08810_b200.inputs.atom_keyed_values`."""
+    rc = _lib.load().sse_fill_synthetic(
+        _device_ctx(dst).handle, ctypes.c_uint64(seed), ctypes.c_uint32(tensor_id), atom0, natoms,
+        outer, inner, atom_stride, outer_stride, float(scale), _dptr(dst), _stream_ptr(stream),
+    )
+    _lib.check(rc)
+
+
+def _host_ptr(a):
+    """ctypes pointer of a C-contiguous numpy array or CPU (pinned) torch tensor."""
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("host arrays must be C-contiguous")
+        return _ptr(a)
+    if getattr(a, "is_cuda", False):
+        raise ValueError("host API expects host memory")
+    if not a.is_contiguous():
+        raise ValueError("host arrays must be contiguous")
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def sigma_host_slab(
+    g_l, g_g, dc_l, dc_g, dh, nmap_rows, offsets, weights, out_l, out_g, *,
+    n_a: int, g_atom0: int, out_atom0: int, variant=SseVariant.BATCHED_FUSED,
+    device: int | None = None, n_gpus: int | None = None,
+) -> dict:
+    """Host-memory Sigma of an owned atom range (libsse sse_sigma_c128_slab).
+
+    Grid-major host slabs (numpy or pinned torch CPU tensors):
+    g_* [Nkz, NE, gA, No, No] for atoms [g_atom0, g_atom0 + gA);
+    out_* [Nkz, NE, oA, No, No], dc_* [Nqz, Nw, oA, NB, 3, 3],
+    dh [oA, NB, 3, No, No] for atoms [out_atom0, out_atom0 + oA).
+    Copies in, computes on the GPU(s) (pipelined), copies Sigma out; returns
+    the library's timing.
+    """
+    n_kz, n_e, g_atoms, n_o = (int(x) for x in g_l.shape[:4])
+    o_atoms = int(out_l.shape[2])
+    n_qz, n_w, _, n_b = (int(x) for x in dc_l.shape[:4])
+    idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    wts = np.ascontiguousarray(weights, dtype=np.float64)
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    gs = _lib.SseSlab(g_atom0, g_atoms, 0, 0)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, 0, 0)
+    tim = _lib.SseTiming()
+    ctx = _lib.context(device=device) if device is not None else _lib.context(n_gpus=n_gpus or _default_gpus())
+    rc = _lib.load().sse_sigma_c128_slab(
+        ctx.handle, ctypes.byref(dims), VARIANT_CODES[_resolve_variant(variant)], ctypes.byref(gs),
+        ctypes.byref(os_), *[_host_ptr(a) for a in (g_l, g_g, dc_l, dc_g, dh)], _ptr(idx), _ptr(offs),
+        _ptr(wts), _host_ptr(out_l), _host_ptr(out_g), ctypes.byref(tim),
+    )
+    _lib.check(rc)
+    return tim.as_dict()
+
+
+class Profile:
+    """CUDA-event profile of libsse launches on one context (per kernel kind).
+
+    with Profile(device=0) as prof: ...  ->  prof.result["sigma"]["ms"], ...
+    """
+
+    def __init__(self, device: int | None = 0, n_gpus: int | None = None):
+        self.ctx = _lib.context(device=device) if device is not None else _lib.context(n_gpus=n_gpus or 1)
+        self.result: dict = {}
+
+    def __enter__(self):
+        _lib.check(_lib.load().sse_profile_begin(self.ctx.handle))
+        return self
+
+    def __exit__(self, *exc):
+        prof = _lib.SseProfile()
+        _lib.check(_lib.load().sse_profile_end(self.ctx.handle, ctypes.byref(prof)))
+        self.result = prof.as_dict()
+        return False

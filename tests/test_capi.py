@@ -1,0 +1,114 @@
+"""C-ABI boundary checks that need no GPU: symbols, loading, error mapping."""
+
+import ctypes
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1912_08810_b200 import _lib, build
+from paper_1912_08810_b200.sse import sse_sigma
+from paper_1912_08810_b200.types import (
+    CombinedD,
+    GreensTensor,
+    SimParams,
+    build_neighbor_map,
+    default_grid,
+)
+
+HEADER = build.HEADERS[1]
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(sse_\w+)\s*\(", text, re.M)))
+
+
+def test_library_builds_and_is_current():
+    build.build()
+    assert build.up_to_date()
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(_lib.EXPORTED)
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (sse_\w+)", out))
+    assert set(header_functions()) <= exported
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_fp64_tensor_core_sass_present():
+    """The Sigma kernel issues DMMA.8x8x4 (FP64 tensor cores), not a CPU/DFMA fallback."""
+    out = subprocess.run(
+        ["cuobjdump", "-sass", "-fun", "_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", _lib.LIB_PATH],
+        capture_output=True, text=True,
+    ).stdout
+    assert out.count("DMMA.8x8x4") >= 54
+
+
+def test_version_and_no_cpu_fallback():
+    lib = _lib.load()
+    assert lib.sse_version() == 1
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    handle = ctypes.c_void_p()
+    rc = lib.sse_ctx_create(1, ctypes.byref(handle))
+    assert rc == _lib.SSE_ECUDA
+    assert "no CUDA device" in lib.sse_last_error().decode()
+    with pytest.raises(_lib.SseError):
+        _lib.Context(1)
+
+
+def _instance():
+    p = SimParams(n_kz=2, n_qz=1, n_E=4, n_w=2, n_A=4, n_B=2, n_orb=2)
+    rng = np.random.default_rng(0)
+    z = lambda s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
+    g = GreensTensor(z(p.electron_shape), z(p.electron_shape))
+    dc = CombinedD(z(p.combined_shape), z(p.combined_shape))
+    return p, g, dc, z(p.dh_shape), build_neighbor_map(4, 2), default_grid(p)
+
+
+def test_sse_sigma_argument_errors_match_reference():
+    """sse.py:315-318, 329: ValueError before any device work."""
+    p, g, dc, dh, nmap, grid = _instance()
+    from paper_1912_08810_b200.types import SseVariant
+
+    with pytest.raises(ValueError, match="expects an electron tensor"):
+        sse_sigma(SseVariant.REFERENCE, GreensTensor(np.zeros((1, 1, 4, 1, 3, 3)), np.zeros((1, 1, 4, 1, 3, 3))),
+                  dc, dh, nmap, grid)
+    with pytest.raises(ValueError, match="does not match the neighbor map"):
+        sse_sigma(SseVariant.REFERENCE, g, dc, dh, build_neighbor_map(4, 1), grid)
+    with pytest.raises(ValueError, match="unknown variant"):
+        sse_sigma("no-such-variant", g, dc, dh, nmap, grid)
+    with pytest.raises(ValueError, match="dH must have shape"):
+        sse_sigma(SseVariant.REFERENCE, g, dc, dh[:, :1], nmap, grid)
+
+
+def test_types_mirror_reference_validation():
+    with pytest.raises(ValueError, match="combined phonon tensor must be a matching 6-D pair"):
+        CombinedD(np.zeros((1, 1, 1, 1, 3, 3)), np.zeros((1, 1, 1, 2, 3, 3)))
+    with pytest.raises(ValueError, match="lesser/greater shape mismatch"):
+        GreensTensor(np.zeros((1, 1, 1, 1, 1)), np.zeros((1, 1, 2, 1, 1)))
+    from paper_1912_08810_b200.types import EnergyGrid, NeighborMap
+
+    with pytest.raises(ValueError, match="2-D integer"):
+        NeighborMap(np.zeros((2, 2)))
+    with pytest.raises(ValueError, match="outside"):
+        EnergyGrid(values=(0.0, 1.0), frequency_map=((2, 1.0),), energy_weight=1.0)

@@ -1,0 +1,303 @@
+"""Parity of the CUDA path (through the C ABI) with the reference's outputs.
+
+Tolerance: the reference's own metric, max|out - ref| / max(max|ref<|, max|ref>|)
+<= 1e-10 in complex128 (BASELINE.json north_star; test_acceptance.py:162-171).
+Golden outputs come from the reference itself (tests/golden/make_golden.py).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import sse_oracle as orc
+from paper_1912_08810_b200 import inputs
+from paper_1912_08810_b200.sse import sse_sigma
+from paper_1912_08810_b200.types import (
+    CombinedD,
+    EnergyGrid,
+    FlopCounter,
+    GreensTensor,
+    NeighborMap,
+    SimParams,
+    SseVariant,
+    build_neighbor_map,
+    default_grid,
+)
+from tests.golden_cases import criterion5_instances, kat_scalar, load_case, stream_case_names
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _grid(case):
+    n_e = case.p.n_E
+    return EnergyGrid(
+        values=tuple(np.linspace(-1, 1, n_e)) if n_e > 1 else (0.0,),
+        frequency_map=tuple(zip(case.offsets.tolist(), case.weights.tolist())),
+        energy_weight=1.0,
+    )
+
+
+def _dc(case):
+    return CombinedD(*orc.preprocess_D(case.d_l, case.d_g, case.idx))
+
+
+@pytest.fixture(scope="module", params=stream_case_names())
+def case(request):
+    c = load_case(request.param)
+    assert c.inputs_ok
+    return c
+
+
+@pytest.mark.parametrize("variant", list(SseVariant))
+def test_golden_parity_all_variants(case, variant):
+    counter = FlopCounter()
+    out = sse_sigma(variant, GreensTensor(case.g_l, case.g_g), _dc(case), case.dh, NeighborMap(case.idx),
+                    _grid(case), counter=counter)
+    dev = orc.parity_dev(out.lesser, out.greater, case.arrays["sigma_l"], case.arrays["sigma_g"])
+    assert dev <= TOL, (case.name, variant, dev)
+    p = case.p
+    assert counter.stages == orc.sigma_tallies(variant.value, p.n_kz, p.n_qz, p.n_E, p.n_w, p.n_A, p.n_B,
+                                               p.n_orb)
+
+
+def test_kat_scalar():
+    g_l, g_g, dc_l, dc_g, dh, idx, off, wt, ref_l, ref_g = kat_scalar()
+    grid = EnergyGrid(values=(0.0,), frequency_map=((0, 0.37),), energy_weight=1.0)
+    out = sse_sigma(SseVariant.REFERENCE, GreensTensor(g_l, g_g), CombinedD(dc_l, dc_g), dh, NeighborMap(idx), grid)
+    assert np.max(np.abs(out.lesser - ref_l)) <= 1e-13 * np.max(np.abs(ref_l))
+    assert np.max(np.abs(out.greater - ref_g)) <= 1e-13 * np.max(np.abs(ref_g))
+
+
+def test_criterion5_fifty_instances_all_variants():
+    worst = 0.0
+    for p, grid, nmap, g_l, g_g, d_l, d_g, dh, ref_l, ref_g in criterion5_instances():
+        dc = CombinedD(*orc.preprocess_D(d_l, d_g, nmap.idx))
+        for variant in SseVariant:
+            out = sse_sigma(variant, GreensTensor(g_l, g_g), dc, dh, nmap, grid)
+            worst = max(worst, orc.parity_dev(out.lesser, out.greater, ref_l, ref_g))
+    assert worst <= TOL
+
+
+def test_zero_phonon_input_gives_exact_zero():
+    """test_sse.py:165-172."""
+    c = load_case("test_tiny_s3")
+    zero = CombinedD(np.zeros(c.p.combined_shape, complex), np.zeros(c.p.combined_shape, complex))
+    out = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(c.g_l, c.g_g), zero, c.dh, NeighborMap(c.idx), _grid(c))
+    assert np.all(out.lesser == 0) and np.all(out.greater == 0)
+
+
+def test_linearity_in_g_and_dc():
+    """test_sse.py:253-272 at the kernel's No=12 shape."""
+    c = load_case("orb12_s5")
+    rng = np.random.default_rng(42)
+    z = lambda s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
+    nmap, grid, dc = NeighborMap(c.idx), _grid(c), _dc(c)
+    g2 = GreensTensor(z(c.g_l.shape), z(c.g_g.shape))
+    d2 = CombinedD(z(dc.lesser.shape), z(dc.greater.shape))
+
+    def run(g, d):
+        return sse_sigma(SseVariant.BATCHED_FUSED, g, d, c.dh, nmap, grid).lesser
+
+    g1 = GreensTensor(c.g_l, c.g_g)
+    lhs = run(GreensTensor(c.g_l + g2.lesser, c.g_g + g2.greater), dc)
+    rhs = run(g1, dc) + run(g2, dc)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * np.max(np.abs(rhs))
+    lhs = run(g1, CombinedD(dc.lesser + d2.lesser, dc.greater + d2.greater))
+    rhs = run(g1, dc) + run(g1, d2)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * np.max(np.abs(rhs))
+
+
+def test_deterministic_bitwise():
+    c = load_case("orb10_s6")
+    args = (GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx), _grid(c))
+    a = sse_sigma(SseVariant.BATCHED_FUSED, *args)
+    b = sse_sigma(SseVariant.BATCHED_FUSED, *args)
+    assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+
+
+def test_layout_transformed_equals_grid_major_bitwise():
+    """K1 round trip is lossless and the atom-major accumulation has the same order."""
+    c = load_case("orb12_s5")
+    args = (GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx), _grid(c))
+    a = sse_sigma(SseVariant.BATCHED_FUSED, *args)
+    b = sse_sigma(SseVariant.LAYOUT_TRANSFORMED, *args)
+    assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+
+
+def test_multi_gpu_split_is_bitwise_identical():
+    import torch
+
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    c = load_case("cli_small_s2")
+    args = (GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx), _grid(c))
+    a = sse_sigma(SseVariant.BATCHED_FUSED, *args, n_gpus=1)
+    for k in range(2, n + 1):
+        b = sse_sigma(SseVariant.BATCHED_FUSED, *args, n_gpus=k)
+        assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+
+
+def test_timing_and_launch_accounting():
+    c = load_case("orb12_s5")
+    timing = {}
+    sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx),
+              _grid(c), timing=timing)
+    assert timing["kernel_launches"] >= 2
+    assert timing["h2d_bytes"] > 2 * c.g_l.nbytes
+    assert timing["d2h_bytes"] == 2 * c.g_l.nbytes
+    assert timing["flops"] > 0
+
+
+def test_invalid_neighbor_index_raises_value_error():
+    c = load_case("test_tiny_s3")
+    bad = c.idx.copy()
+    bad[0, 0] = c.p.n_A
+    with pytest.raises(ValueError):
+        sse_sigma(SseVariant.REFERENCE, GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(bad), _grid(c))
+
+
+# ---------------------------------------------------------------------------
+# device-resident API
+# ---------------------------------------------------------------------------
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def test_device_api_slabs_and_layouts_bitwise():
+    """Owned-range shards with halos, grid- and atom-major, equal the full call bitwise."""
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    c = load_case("orb12_s5")
+    p = c.p
+    dc = _dc(c)
+    full = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(c.g_l, c.g_g), dc, c.dh, NeighborMap(c.idx), _grid(c))
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    for lo, hi in ((0, 3), (3, 6), (2, 4)):
+        need = c.idx[lo:hi]
+        glo, ghi = int(need.min()), int(need.max()) + 1
+        for atom_major in (False, True):
+            gl, gg = c.g_l[:, :, glo:ghi], c.g_g[:, :, glo:ghi]
+            if atom_major:
+                gl, gg = np.moveaxis(gl, 2, 0), np.moveaxis(gg, 2, 0)
+            gl, gg = cu(gl), cu(gg)
+            shape = (hi - lo, p.n_kz, p.n_E, p.n_orb, p.n_orb) if atom_major else (p.n_kz, p.n_E, hi - lo, p.n_orb, p.n_orb)
+            ol = torch.zeros(shape, dtype=torch.complex128, device="cuda")
+            og = torch.zeros_like(ol)
+            dev.sigma_device(gl, gg, cu(dc.lesser[:, :, lo:hi]), cu(dc.greater[:, :, lo:hi]), cu(c.dh[lo:hi]),
+                             need, c.offsets, c.weights, ol, og, n_a=p.n_A, g_atom0=glo, out_atom0=lo,
+                             atom_major=atom_major)
+            torch.cuda.synchronize()
+            got_l, got_g = ol.cpu().numpy(), og.cpu().numpy()
+            if atom_major:
+                got_l, got_g = np.moveaxis(got_l, 0, 2), np.moveaxis(got_g, 0, 2)
+            assert np.array_equal(got_l, full.lesser[:, :, lo:hi])
+            assert np.array_equal(got_g, full.greater[:, :, lo:hi])
+
+
+def test_layout_transform_kernel_bitwise():
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    c = load_case("orb10_s6")
+    g = torch.from_numpy(c.g_l).cuda()
+    am = torch.empty((c.p.n_A, c.p.n_kz, c.p.n_E, c.p.n_orb, c.p.n_orb), dtype=torch.complex128, device="cuda")
+    back = torch.empty_like(g)
+    dev.layout_transform(g, am, to_atom_major=True)
+    dev.layout_transform(am, back, to_atom_major=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(am.cpu().numpy(), np.moveaxis(c.g_l, 2, 0))
+    assert np.array_equal(back.cpu().numpy(), c.g_l)
+
+
+def test_preprocess_D_device_bitwise():
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    for name in ("cli_small_s2", "orb10_s6", "orb5_nb1_s7"):
+        c = load_case(name)
+        ref_l, _ = orc.preprocess_D(c.d_l, c.d_g, c.idx)
+        out = torch.empty(ref_l.shape, dtype=torch.complex128, device="cuda")
+        dev.preprocess_D_device(torch.from_numpy(c.d_l).cuda(), out, c.idx)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref_l), name
+
+
+def test_preprocess_D_device_missing_slot():
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    idx = np.array([[1], [0], [1]], dtype=np.int64)
+    d = torch.ones((1, 1, 3, 2, 3, 3), dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError, match="missing neighbor slot"):
+        dev.preprocess_D_device(d, torch.empty((1, 1, 3, 1, 3, 3), dtype=torch.complex128, device="cuda"), idx)
+
+
+def test_fill_synthetic_matches_host_generator_bitwise():
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    p = SimParams(n_kz=2, n_qz=2, n_E=5, n_w=2, n_A=7, n_B=2, n_orb=3)
+    g = torch.empty(p.electron_shape, dtype=torch.complex128, device="cuda")
+    no2 = p.n_orb**2
+    dev.fill_synthetic(g, 11, inputs.G_LESSER, 0, p.n_A, p.n_kz * p.n_E, no2, no2, p.n_A * no2)
+    torch.cuda.synchronize()
+    host = inputs.atom_keyed_electron(11, inputs.G_LESSER, p, np.arange(p.n_A))
+    assert np.array_equal(g.cpu().numpy(), host)
+    # a slab of atoms [2, 5) holds the same values as the full tensor
+    s = torch.empty((p.n_kz, p.n_E, 3, p.n_orb, p.n_orb), dtype=torch.complex128, device="cuda")
+    dev.fill_synthetic(s, 11, inputs.G_LESSER, 2, 3, p.n_kz * p.n_E, no2, no2, 3 * no2)
+    torch.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy(), host[:, :, 2:5])
+    dh = torch.empty(p.dh_shape, dtype=torch.complex128, device="cuda")
+    inner = p.n_B * 3 * no2
+    dev.fill_synthetic(dh, 11, inputs.DH, 0, p.n_A, 1, inner, inner, 0, scale=inputs.DH_SCALE)
+    torch.cuda.synchronize()
+    assert np.array_equal(dh.cpu().numpy(), inputs.atom_keyed_dh(11, p, np.arange(p.n_A)))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs at full size: sampled points vs the pointwise oracle
+# ---------------------------------------------------------------------------
+
+
+def _full_scale_points(name, seed, points_per_atom, atoms):
+    """Device-resident full-config Sigma; sampled (atom, k, E) blocks vs oracle."""
+    torch = _torch()
+    from tests.scale_helpers import DeviceProblem, host_point
+
+    prob = DeviceProblem(name, seed)
+    prob.run()
+    p = prob.p
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for a in atoms:
+        es = sorted({0, 1, p.n_E - 1, int(prob.offsets.max()), *rng.integers(0, p.n_E, points_per_atom).tolist()})
+        for e in es:
+            k = int(rng.integers(0, p.n_kz))
+            for pol in (0, 1):
+                got = prob.sigma_block(pol, k, e, a)
+                ref = host_point(prob, pol, k, e, a)
+                scale = max(np.max(np.abs(ref)), 1e-300)
+                worst = max(worst, float(np.max(np.abs(got - ref)) / scale))
+    prob.free()
+    torch.cuda.empty_cache()
+    return worst
+
+
+def test_small_config_sampled_points():
+    p = inputs.CONFIGS["small"]
+    dev = _full_scale_points("small", 0, 6, [0, 1, 2, p.n_A // 2, p.n_A - 2, p.n_A - 1])
+    assert dev <= TOL
+
+
+@pytest.mark.slow
+def test_paper_config_sampled_points():
+    p = inputs.CONFIGS["paper"]
+    dev = _full_scale_points("paper", 0, 4, [0, 1, 2, 2431, p.n_A - 2, p.n_A - 1])
+    assert dev <= TOL

@@ -1,0 +1,167 @@
+"""Pin the CPU oracle (oracle/sse_oracle.py) to the reference's golden outputs.
+
+The fixtures in tests/golden were produced by running the reference
+``negflow`` (tests/golden/make_golden.py); these tests need no GPU.
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import sse_oracle as orc
+from tests.golden_cases import criterion5_instances, digest, kat_scalar, load_case, stream_case_names
+
+CASES = stream_case_names()
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.fixture(scope="module", params=CASES)
+def case(request):
+    c = load_case(request.param)
+    assert c.inputs_ok, f"{c.name}: regenerated inputs differ from the fixture digest"
+    return c
+
+
+def test_golden_inputs_and_nmap(case):
+    p = case.p
+    assert np.array_equal(orc.build_neighbor_map(p.n_A, p.n_B), case.idx)
+
+
+def test_preprocess_matches_reference_bitwise(case):
+    dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    assert digest(dc_l, dc_g) == case.meta["dc_sha256"]
+    if "dc_l" in case.arrays:
+        assert np.array_equal(dc_l, case.arrays["dc_l"])
+
+
+def test_sigma_reference_restatement(case):
+    dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    out_l, out_g = orc.sigma_reference(
+        case.g_l, case.g_g, dc_l, dc_g, case.dh, case.idx, case.offsets, case.weights
+    )
+    ref_l, ref_g = case.arrays["sigma_l"], case.arrays["sigma_g"]
+    assert orc.parity_dev(out_l, out_g, ref_l, ref_g) <= 1e-14
+
+
+def test_batched_fused_restatement(case):
+    dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    out_l, out_g = orc.sigma_batched_fused(
+        case.g_l, case.g_g, dc_l, dc_g, case.dh, case.idx, case.offsets, case.weights
+    )
+    if "bf_l" in case.arrays:
+        assert orc.parity_dev(out_l, out_g, case.arrays["bf_l"], case.arrays["bf_g"]) <= 1e-14
+    assert orc.parity_dev(out_l, out_g, case.arrays["sigma_l"], case.arrays["sigma_g"]) <= 1e-12
+
+
+def test_reassociated_algebra_matches_reference(case):
+    """G@(sum_i dH_i Xi_i) == sum_i (G@dH_i)@Xi_i: the kernel's algebra, pinned."""
+    dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    out_l = orc.sigma_reassociated(case.g_l, dc_l, case.dh, case.idx, case.offsets, case.weights)
+    out_g = orc.sigma_reassociated(case.g_g, dc_g, case.dh, case.idx, case.offsets, case.weights)
+    assert orc.parity_dev(out_l, out_g, case.arrays["sigma_l"], case.arrays["sigma_g"]) <= 1e-13
+
+
+def test_loop_oracle_small(case):
+    p = case.p
+    if p.n_kz * p.n_E * p.n_A * p.n_B * p.n_qz * p.n_w > 5000:
+        pytest.skip("loop oracle is for small shapes")
+    dc_l, _ = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    out = orc.sigma_loop(case.g_l, dc_l, case.dh, case.idx, case.offsets, case.weights, p.n_qz)
+    assert rel(out, case.arrays["sigma_l"]) <= 1e-12
+
+
+def test_pi_restatement(case):
+    if "pi_l" not in case.arrays:
+        pytest.skip("no Pi fixture for this case")
+    ew = case.meta["energy_weight"]
+    ch_l, ch_g = orc.pi_chains(case.g_l, case.g_g, case.dh, case.idx, case.offsets, ew, case.p.n_qz)
+    pi_l, pi_g = orc.pi_from_chains(ch_l, ch_g)
+    assert orc.parity_dev(pi_l, pi_g, case.arrays["pi_l"], case.arrays["pi_g"]) <= 1e-13
+
+
+def test_kat_scalar():
+    g_l, g_g, dc_l, dc_g, dh, idx, off, wt, ref_l, ref_g = kat_scalar()
+    out_l, out_g = orc.sigma_reference(g_l, g_g, dc_l, dc_g, dh, idx, off, wt)
+    assert np.array_equal(out_l, ref_l) and np.array_equal(out_g, ref_g)
+    # the hand-evaluated scalar of test_sse.py:175-197
+    for a in range(2):
+        b = int(idx[a, 0])
+        expected = 1j * 0.37 * sum(
+            g_l[0, 0, b, 0, 0] * dh[a, 0, i, 0, 0] * dh[a, 0, j, 0, 0] * dc_l[0, 0, a, 0, i, j]
+            for i in range(3)
+            for j in range(3)
+        )
+        assert abs(out_l[0, 0, a, 0, 0] - expected) <= 1e-13 * abs(expected)
+
+
+def test_criterion5_fifty_instances():
+    worst = 0.0
+    for p, grid, nmap, g_l, g_g, d_l, d_g, dh, ref_l, ref_g in criterion5_instances():
+        off = np.array(grid.offsets)
+        wt = np.array(grid.weights)
+        dc_l, dc_g = orc.preprocess_D(d_l, d_g, nmap.idx)
+        for fn in (orc.sigma_reference, orc.sigma_batched_fused):
+            out_l, out_g = fn(g_l, g_g, dc_l, dc_g, dh, nmap.idx, off, wt)
+            worst = max(worst, orc.parity_dev(out_l, out_g, ref_l, ref_g))
+    assert worst <= 1e-10
+
+
+def test_shifted_grid_semantics():
+    """test_sse.py:101-112."""
+    arr = np.arange(12, dtype=complex).reshape(3, 4)[..., None]
+    out = orc.shifted_grid(arr, 1, 1)
+    for k in range(3):
+        for e in range(4):
+            expected = arr[(k - 1) % 3, e - 1] if e - 1 >= 0 else 0
+            assert out[k, e] == expected
+    assert np.all(orc.shifted_grid(arr, 0, 4) == 0)
+    assert np.all(orc.shifted_grid(arr, 0, -4) == 0)
+    assert orc.shifted_grid(arr, -1, -1)[0, 0] == arr[1, 1]
+
+
+def test_neighbor_map_examples():
+    assert orc.build_neighbor_map(8, 4)[0].tolist() == [1, 1, 2, 2]
+    assert orc.build_neighbor_map(4, 1)[:, 0].tolist() == [1, 0, 3, 2]
+    with pytest.raises(ValueError):
+        orc.build_neighbor_map(3, 3)
+    with pytest.raises(ValueError):
+        orc.build_neighbor_map(5, 1)
+
+
+def test_preprocess_missing_neighbor_slot():
+    """test_sse.py:151-162."""
+    idx = np.array([[1], [0], [1]], dtype=np.int64)
+    d = np.ones((1, 1, 3, 2, 3, 3), complex)
+    with pytest.raises(ValueError, match="missing neighbor slot"):
+        orc.preprocess_D(d, d, idx)
+    with pytest.raises(ValueError, match="missing neighbor slot"):
+        orc.preprocess_D(
+            np.ones((1, 1, 3, 1, 3, 3), complex),
+            np.ones((1, 1, 3, 1, 3, 3), complex),
+            np.array([[1, 2], [0, 2], [0, 1]], dtype=np.int64),
+        )
+
+
+def test_sigma_tallies_match_reference_counter_sites():
+    # counts observed from the reference for the SURVEY tiny config:
+    # REFERENCE sigma.dhg = 113,246,208 and BATCHED_FUSED sigma.dhg = 9,437,184
+    t_ref = orc.sigma_tallies("reference", 3, 3, 32, 4, 64, 4, 4)
+    t_bf = orc.sigma_tallies("batched-fused", 3, 3, 32, 4, 64, 4, 4)
+    assert t_ref["sigma.dhg"] == 113_246_208
+    assert t_bf["sigma.dhg"] == 9_437_184
+    assert t_ref["sigma.accumulate"] == t_bf["sigma.accumulate"] == 113_246_208
+
+
+def test_reduction_order_permutation():
+    """test_sse.py:239-250: ascending (q,w,s) vs shuffled agree to 1e-12."""
+    c = load_case("test_tiny_s3")
+    dc_l, dc_g = orc.preprocess_D(c.d_l, c.d_g, c.idx)
+    base = orc.sigma_reference(c.g_l, c.g_g, dc_l, dc_g, c.dh, c.idx, c.offsets, c.weights)
+    order = list(itertools.product(range(c.p.n_qz), range(c.p.n_w), range(c.p.n_B)))
+    np.random.default_rng(0).shuffle(order)
+    out = orc.sigma_reference(c.g_l, c.g_g, dc_l, dc_g, c.dh, c.idx, c.offsets, c.weights, qws_order=order)
+    assert orc.parity_dev(out[0], out[1], base[0], base[1]) <= 1e-12
