@@ -175,11 +175,20 @@ def _dptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
 def _stream_ptr(stream):
+    """cudaStream_t of a torch stream (default: torch's current stream).
+
+    torch's default stream has handle 0, which libsse would read as "use the
+    library's own stream"; map it to cudaStreamLegacy so our kernels stay
+    ordered with torch's work and events.
+    """
     import torch
 
     s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    return ctypes.c_void_p(s.cuda_stream or _CUDA_STREAM_LEGACY)
 
 
 def _device_ctx(t):
