@@ -14,6 +14,8 @@
 // algebra; results agree with the reference to rounding (tests/).
 #include "sse_kernels.cuh"
 
+#include <cstdlib>
+
 namespace sse {
 
 // --------------------------------------------------------------------------
@@ -242,6 +244,141 @@ sigma_dmma_kernel(SigmaArgs p) {
 }
 
 // --------------------------------------------------------------------------
+// K3 (pipelined): same contraction and accumulation order as sigma_dmma_kernel,
+// restructured for latency hiding with one 8-warp CTA per SM:
+//  * the (q, s, w) loop is flattened and register double-buffered: the A
+//    (shifted G rows, 3 tiles) and B (M fragments) operands of iteration
+//    it+1 are loaded while the 54 DMMAs of iteration it run;
+//  * DMMAs are issued k-step-outer over the warp's 3 tiles x 3 n-tiles, so 9
+//    independent accumulator chains separate dependent DMMAs;
+//  * the E < off skip is warp-uniform (no branches between the tiles).
+// --------------------------------------------------------------------------
+template <int NO>
+struct OperandStage {
+  double2 a[kRowTiles][frag_geom(NO).kh];
+  double2 b[frag_geom(NO).fv];
+  int off;
+};
+
+template <int NO>
+__global__ void __launch_bounds__(kSigmaWarps * 32, 1)
+sigma_dmma_pipe_kernel(SigmaArgs p) {
+  constexpr FragGeom FG = frag_geom(NO);
+  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
+  const int pol = blockIdx.y;
+  int bx = blockIdx.x;
+  const int rc = bx % p.ctas_per_ak;
+  bx /= p.ctas_per_ak;
+  const int k = bx % p.nkz;
+  const int la = bx / p.nkz;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rbase = rc * kRowsPerCta + warp * (kRowTiles * 8);
+  const int pcol = lane & 3;
+  const double2* __restrict__ G = p.G[pol];
+  const double2* __restrict__ Mf = p.M[pol];
+  const int* __restrict__ offs = p.off;
+
+  int e_row[kRowTiles];
+  bool v_row[kRowTiles];
+  long long r_off[kRowTiles];  // row offset within a (k', b) slab: E * g_se + m * NO + pcol
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t) {
+    const int row = rbase + t * 8 + (lane >> 2);
+    v_row[t] = row < p.rows;
+    e_row[t] = row / NO;
+    r_off[t] = (long long)e_row[t] * p.g_se + (row - e_row[t] * NO) * NO + pcol;
+  }
+  // warp-uniform bounds of the warp's rows
+  const int warp_rows = min(kRowTiles * 8, p.rows - rbase);
+  const int warp_emax = warp_rows > 0 ? (rbase + warp_rows - 1) / NO : -1;
+
+  double acc[kRowTiles][NT][2];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+
+  // load cursor over the flattened (q, s, w) iterations
+  int lq = 0, ls = 0, lw = 0;
+  long long slab = 0;           // (k', b) slab offset of the cursor's (q, s)
+  const double2* mfq = nullptr;  // M fragments of the cursor's (q, s), lane-offset
+  auto setup_qs = [&]() {
+    int kp = (k - lq) % p.nkz;
+    if (kp < 0) kp += p.nkz;
+    const int lb = __ldg(p.nbr + la * p.nb + ls);
+    slab = lb * p.g_sa + kp * p.g_sk;
+    mfq = Mf + ((long long)((la * p.nb + ls) * p.nqz + lq) * p.nw) * (FV * 32) + lane;
+  };
+  auto load = [&](OperandStage<NO>& st) {
+    const int off = __ldg(offs + lw);
+    st.off = off;
+#pragma unroll
+    for (int j = 0; j < FV; ++j) st.b[j] = __ldg(mfq + (lw * FV + j) * 32);
+    const long long shift = slab - (long long)off * p.g_se;
+#pragma unroll
+    for (int t = 0; t < kRowTiles; ++t) {
+      const bool ok = v_row[t] && e_row[t] >= off;
+#pragma unroll
+      for (int kk = 0; kk < KH; ++kk) {
+        st.a[t][kk] = make_double2(0.0, 0.0);
+        if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO)) st.a[t][kk] = __ldg(G + shift + r_off[t] + 4 * kk);
+      }
+    }
+    if (++lw == p.nw) {
+      lw = 0;
+      if (++ls == p.nb) {
+        ls = 0;
+        ++lq;
+      }
+      if (lq < p.nqz) setup_qs();
+    }
+  };
+  auto compute = [&](const OperandStage<NO>& st) {
+    if (warp_emax < st.off) return;  // every row of the warp has E < off: no term
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+#pragma unroll
+      for (int t = 0; t < kRowTiles; ++t) {
+        const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int f = kk * NT + nt;
+          const double b = (f & 1) ? st.b[f >> 1].y : st.b[f >> 1].x;
+          dmma884(acc[t][nt], a, b);
+        }
+      }
+    }
+  };
+
+  const int n_it = p.nqz * p.nb * p.nw;
+  OperandStage<NO> s0, s1;
+  setup_qs();
+  load(s0);
+  for (int it = 0; it < n_it; it += 2) {
+    if (it + 1 < n_it) load(s1);
+    compute(s0);
+    if (it + 1 >= n_it) break;
+    if (it + 2 < n_it) load(s0);
+    compute(s1);
+  }
+
+  // epilogue: lane holds (Re, Im) of C[row][n = 4 nt + (lane & 3)]; Sigma = i C
+  double2* __restrict__ S = p.S[pol];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t) {
+    if (!v_row[t]) continue;
+    const int row = rbase + t * 8 + (lane >> 2);
+    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
+                   (long long)e_row[t] * p.s_se + (row - e_row[t] * NO) * NO;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int n = 4 * nt + (lane & 3);
+      if (n < NO) dst[n] = make_double2(-acc[t][nt][1], acc[t][nt][0]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // K3g: generic Sigma with DFMA (any No).  One thread per output element
 // (k, E, atom, m, n); compact operator M[q,w][p][n]; same (q, s, w) order.
 // --------------------------------------------------------------------------
@@ -390,10 +527,24 @@ cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Sigma kernel selection (env SSE_SIGMA_KERNEL): 1 = register-pipelined
+// (default), 0 = simple.
+static int sigma_kernel_choice() {
+  static int choice = -1;
+  if (choice < 0) {
+    const char* env = getenv("SSE_SIGMA_KERNEL");
+    choice = env ? atoi(env) : 1;
+  }
+  return choice;
+}
+
 template <int NO>
 static void launch_dmma(const SigmaArgs& a, int chunk_atoms, cudaStream_t st) {
   dim3 grid((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
-  sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
+  if (sigma_kernel_choice() == 1)
+    sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
+  else
+    sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
 }
 
 cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {

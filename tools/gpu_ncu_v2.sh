@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 300 python tools/profile_sigma.py > gpurun_out/prof_plain.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sigma_dmma -s 1 -c 1 -o gpurun_out/sigma_v2 -f python tools/profile_sigma.py > gpurun_out/ncu_v2.log 2>&1
+echo "rc=$?"; tail -2 gpurun_out/ncu_v2.log
