@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -213,8 +214,13 @@ int validate_slab(const sse_dims* d, const sse_slab* s, const char* what) {
   return SSE_OK;
 }
 
-// Operator chunk: bound the per-polarity operator buffer to ~1 GiB.
+// Operator chunk: bound the per-polarity operator buffer to ~1 GiB
+// (SSE_OP_CHUNK_ATOMS overrides, for experiments).
 int64_t op_chunk_atoms(const sse_dims* d) {
+  if (const char* env = getenv("SSE_OP_CHUNK_ATOMS")) {
+    const long long v = atoll(env);
+    if (v > 0) return v;
+  }
   const size_t per_atom = sse::operator_bytes((int)d->norb, (int)d->nb, (int)d->nqz, (int)d->nw, 1);
   return std::max<int64_t>(1, (int64_t)((1ull << 30) / std::max<size_t>(per_atom, 1)));
 }

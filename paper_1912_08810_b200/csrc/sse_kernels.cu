@@ -379,233 +379,6 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
 }
 
 // --------------------------------------------------------------------------
-// K3 (TMA): the pipelined kernel with its operands staged through a
-// warp-private shared-memory ring filled by bulk-async copies (TMA,
-// cp.async.bulk -> SASS UBLKCP) and tracked by mbarriers:
-//  * per (q, s, w) stage, lane 0 of each warp issues one bulk copy of the
-//    M fragments (FV*512 bytes, contiguous) and one per energy block of the
-//    shifted G rows the warp needs (No*No*16 bytes each, E - off >= 0 only),
-//    n_stages - 1 stages ahead of the consumer;
-//  * consumers wait on the stage's mbarrier, read their fragments with
-//    16-byte LDS into the register double buffer, and run the 54 DMMAs;
-//  * no CTA-wide barrier: each warp's ring is private, so one warp's L2/DRAM
-//    latency never stalls another warp.
-// --------------------------------------------------------------------------
-template <int NO>
-struct TmaGeom {
-  static constexpr int kWarpRows = kRowTiles * 8;
-  static constexpr int kMaxBlk = (kWarpRows % NO == 0) ? kWarpRows / NO : (kWarpRows + NO - 1) / NO + 1;
-  static constexpr int kBVec = frag_geom(NO).fv * 32;   // double2 per stage (M fragments)
-  static constexpr int kAVec = kMaxBlk * NO * NO;       // double2 per stage (G blocks)
-  static constexpr int kStageVec = kBVec + kAVec;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      " .reg .pred P1;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int NO>
-__global__ void __launch_bounds__(kSigmaWarps * 32, 1)
-sigma_dmma_tma_kernel(SigmaArgs p, int n_stages) {
-  constexpr FragGeom FG = frag_geom(NO);
-  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
-  using TG = TmaGeom<NO>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int pol = blockIdx.y;
-  int bx = blockIdx.x;
-  const int rc = bx % p.ctas_per_ak;
-  bx /= p.ctas_per_ak;
-  const int k = bx % p.nkz;
-  const int la = bx / p.nkz;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rbase = rc * kRowsPerCta + warp * TG::kWarpRows;
-  const int pcol = lane & 3;
-  const double2* __restrict__ G = p.G[pol];
-  const double2* __restrict__ Mf = p.M[pol];
-  const int* __restrict__ offs = p.off;
-
-  double2* ring = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * n_stages * TG::kStageVec;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double2*>(smem_raw) +
-                                               (size_t)kSigmaWarps * n_stages * TG::kStageVec) +
-                   warp * n_stages;
-
-  const int warp_rows = min(TG::kWarpRows, p.rows - rbase);
-  const int warp_emax = warp_rows > 0 ? (rbase + warp_rows - 1) / NO : -1;
-  const int e0 = rbase / NO;                  // first energy block of the warp's rows
-  const int nblk = warp_rows > 0 ? warp_emax - e0 + 1 : 0;
-
-  int e_row[kRowTiles], a_idx[kRowTiles];
-  bool v_row[kRowTiles];
-#pragma unroll
-  for (int t = 0; t < kRowTiles; ++t) {
-    const int row = rbase + t * 8 + (lane >> 2);
-    v_row[t] = row < p.rows;
-    e_row[t] = row / NO;
-    a_idx[t] = TG::kBVec + (e_row[t] - e0) * NO * NO + (row - e_row[t] * NO) * NO + pcol;
-  }
-
-  double acc[kRowTiles][NT][2];
-#pragma unroll
-  for (int t = 0; t < kRowTiles; ++t)
-#pragma unroll
-    for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
-
-  if (lane == 0) {
-    for (int s = 0; s < n_stages; ++s) mbar_init(bars + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-
-  // producer cursor (all lanes track it; lane 0 issues)
-  int iq = 0, is = 0, iw = 0, i_it = 0;
-  long long islab = 0;
-  const double2* imf = nullptr;
-  auto qs_base = [&]() {
-    int kp = (k - iq) % p.nkz;
-    if (kp < 0) kp += p.nkz;
-    const int lb = __ldg(p.nbr + la * p.nb + is);
-    islab = lb * p.g_sa + kp * p.g_sk;
-    imf = Mf + ((long long)((la * p.nb + is) * p.nqz + iq) * p.nw) * TG::kBVec;
-  };
-  const int n_it = p.nqz * p.nb * p.nw;
-  auto issue = [&]() {
-    const int stage = i_it % n_stages;
-    const int off = __ldg(offs + iw);
-    if (lane == 0) {
-      uint64_t* bar = bars + stage;
-      double2* sb = ring + stage * TG::kStageVec;
-      if (warp_emax < off || nblk == 0) {
-        mbar_arrive(bar);  // nothing to compute for this warp: empty phase
-      } else {
-        const int efirst = max(e0, off);
-        const uint32_t bytes = (TG::kBVec + (e0 + nblk - efirst) * NO * NO) * 16;
-        // WAR on the ring slot: its previous contents were read by LDS whose
-        // results the warp's DMMAs (mma.sync, all lanes) already consumed.
-        mbar_arrive_expect_tx(bar, bytes);
-        bulk_g2s(sb, imf + iw * TG::kBVec, TG::kBVec * 16, bar);
-        for (int e = efirst; e < e0 + nblk; ++e)
-          bulk_g2s(sb + TG::kBVec + (e - e0) * NO * NO, G + islab + (long long)(e - off) * p.g_se,
-                   NO * NO * 16, bar);
-      }
-    }
-    ++i_it;
-    if (++iw == p.nw) {
-      iw = 0;
-      if (++is == p.nb) {
-        is = 0;
-        ++iq;
-      }
-      if (iq < p.nqz) qs_base();
-    }
-  };
-
-  // consumer: stage `it` -> registers
-  int cw = 0;
-  auto lds = [&](OperandStage<NO>& st, int it) {
-    const int off = __ldg(offs + cw);
-    if (++cw == p.nw) cw = 0;
-    st.off = off;
-    if (warp_emax < off || nblk == 0) return;
-    const int stage = it % n_stages;
-    mbar_wait(bars + stage, (uint32_t)((it / n_stages) & 1));
-    const double2* sb = ring + stage * TG::kStageVec;
-#pragma unroll
-    for (int j = 0; j < FV; ++j) st.b[j] = sb[j * 32 + lane];
-#pragma unroll
-    for (int t = 0; t < kRowTiles; ++t) {
-      const bool ok = v_row[t] && e_row[t] >= off;
-#pragma unroll
-      for (int kk = 0; kk < KH; ++kk) {
-        st.a[t][kk] = make_double2(0.0, 0.0);
-        if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO)) st.a[t][kk] = sb[a_idx[t] + 4 * kk];
-      }
-    }
-  };
-  auto compute = [&](const OperandStage<NO>& st) {
-    if (warp_emax < st.off || nblk == 0) return;
-#pragma unroll
-    for (int kk = 0; kk < KSTEPS; ++kk) {
-#pragma unroll
-      for (int t = 0; t < kRowTiles; ++t) {
-        const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int f = kk * NT + nt;
-          const double b = (f & 1) ? st.b[f >> 1].y : st.b[f >> 1].x;
-          dmma884(acc[t][nt], a, b);
-        }
-      }
-    }
-  };
-
-  qs_base();
-  for (int i = 0; i < n_stages && i < n_it; ++i) issue();
-  OperandStage<NO> s0, s1;
-  lds(s0, 0);
-  for (int it = 0; it < n_it; it += 2) {
-    if (it + 1 < n_it) lds(s1, it + 1);
-    compute(s0);
-    __syncwarp();
-    if (i_it < n_it) issue();  // refills stage it % n_stages (its data is in s0)
-    if (it + 1 >= n_it) break;
-    if (it + 2 < n_it) lds(s0, it + 2);
-    compute(s1);
-    __syncwarp();
-    if (i_it < n_it) issue();
-  }
-
-  double2* __restrict__ S = p.S[pol];
-#pragma unroll
-  for (int t = 0; t < kRowTiles; ++t) {
-    if (!v_row[t]) continue;
-    const int row = rbase + t * 8 + (lane >> 2);
-    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
-                   (long long)e_row[t] * p.s_se + (row - e_row[t] * NO) * NO;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int n = 4 * nt + (lane & 3);
-      if (n < NO) dst[n] = make_double2(-acc[t][nt][1], acc[t][nt][0]);
-    }
-  }
-}
-
-template <int NO>
-static int tma_stages() {
-  const size_t stage = (size_t)TmaGeom<NO>::kStageVec * 16 * kSigmaWarps + 8 * kSigmaWarps;
-  const size_t budget = 225 * 1024;
-  int s = (int)(budget / stage);
-  return s > 4 ? 4 : s;
-}
-
-// --------------------------------------------------------------------------
 // K3g: generic Sigma with DFMA (any No).  One thread per output element
 // (k, E, atom, m, n); compact operator M[q,w][p][n]; same (q, s, w) order.
 // --------------------------------------------------------------------------
@@ -754,31 +527,21 @@ cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Sigma kernel selection (env SSE_SIGMA_KERNEL): 1 = register-pipelined
-// (default), 0 = simple.
+// Sigma kernel selection (env SSE_SIGMA_KERNEL, read per launch): 1 =
+// register-pipelined (default), 0 = simple.  Both accumulate every output in
+// the same (q, s, w, k-step) order, so they agree bitwise (tested).
 static int sigma_kernel_choice() {
-  static int choice = -1;
-  if (choice < 0) {
-    const char* env = getenv("SSE_SIGMA_KERNEL");
-    choice = env ? atoi(env) : 1;
-  }
-  return choice;
+  const char* env = getenv("SSE_SIGMA_KERNEL");
+  return env ? atoi(env) : 1;
 }
 
 template <int NO>
 static void launch_dmma(const SigmaArgs& a, int chunk_atoms, cudaStream_t st) {
   dim3 grid((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
-  const int choice = sigma_kernel_choice();
-  const int stages = tma_stages<NO>();
-  if (choice == 2 && stages >= 2) {
-    const size_t smem = (size_t)kSigmaWarps * stages * (TmaGeom<NO>::kStageVec * 16 + 8);
-    cudaFuncSetAttribute(sigma_dmma_tma_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sigma_dmma_tma_kernel<NO><<<grid, kSigmaWarps * 32, smem, st>>>(a, stages);
-  } else if (choice == 0) {
+  if (sigma_kernel_choice() == 0)
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  } else {
+  else
     sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  }
 }
 
 cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {

@@ -115,6 +115,19 @@ def test_deterministic_bitwise():
     assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
 
 
+def test_simple_and_pipelined_kernels_bitwise(monkeypatch):
+    """Both K3 kernels accumulate in the same (q, s, w, k-step) order."""
+    c = load_case("orb10_s6")
+    args = (GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx), _grid(c))
+    monkeypatch.setenv("SSE_SIGMA_KERNEL", "1")
+    a = sse_sigma(SseVariant.BATCHED_FUSED, *args)
+    monkeypatch.setenv("SSE_SIGMA_KERNEL", "0")
+    b = sse_sigma(SseVariant.BATCHED_FUSED, *args)
+    assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+    dev = orc.parity_dev(b.lesser, b.greater, c.arrays["sigma_l"], c.arrays["sigma_g"])
+    assert dev <= TOL
+
+
 def test_layout_transformed_equals_grid_major_bitwise():
     """K1 round trip is lossless and the atom-major accumulation has the same order."""
     c = load_case("orb12_s5")
