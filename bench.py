@@ -395,7 +395,7 @@ def run_gpu(args, p, grid, idx) -> None:
             "tflops": total_flops / (step_ms * 1e-3) / 1e12,
             "tflops_per_gpu": total_flops / (step_ms * 1e-3) / 1e12 / world,
             "roofline": {
-                "bound": "tensor", "kernel": "sigma_dmma_kernel<12> (K3)",
+                "bound": "tensor", "kernel": "sigma_dmma_pipe_kernel<12> (K3)",
                 "achieved": k3_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": k3_tflops / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
