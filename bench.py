@@ -36,6 +36,16 @@ FP64_PEAK_TFLOPS = 36.85  # measured DMMA.8x8x4 sustained, profiles/r01_fp64_pea
 FP64_PEAK_SOURCE = "measured DMMA m8n8k4 sustained on this pool's B200 (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry"
 
 
+def k3_kernel_name() -> str:
+    """The K3 variant libsse launches for the bench workload (SSE_SIGMA_KERNEL, default 3)."""
+    return {
+        "0": "sigma_dmma_kernel<12> (K3 simple)",
+        "1": "sigma_dmma_pipe_kernel<12> (K3 register-pipelined)",
+        "2": "sigma_dmma_slide_kernel<12,8,dbuf> (K3 TMA sliding window, 8 warps)",
+    }.get(os.environ.get("SSE_SIGMA_KERNEL", "3"),
+          "sigma_dmma_slide_kernel<12,12> (K3 TMA sliding window, 12 warps)")
+
+
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -395,7 +405,7 @@ def run_gpu(args, p, grid, idx) -> None:
             "tflops": total_flops / (step_ms * 1e-3) / 1e12,
             "tflops_per_gpu": total_flops / (step_ms * 1e-3) / 1e12 / world,
             "roofline": {
-                "bound": "tensor", "kernel": "sigma_dmma_pipe_kernel<12> (K3)",
+                "bound": "tensor", "kernel": k3_kernel_name(),
                 "achieved": k3_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": k3_tflops / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),

@@ -328,6 +328,9 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   sa.s_sk = ss.sk;
   sa.s_se = ss.se;
   sa.npol = npol;
+  sa.off_slide = 1;
+  for (int64_t w = 1; w < d->nw; ++w)
+    if (off[w] < off[w - 1] || off[w] > off[w - 1] + 1) sa.off_slide = 0;
   CHECK(profiled(ds, st, SSE_PROF_SIGMA, alg_flops(d, off, n, npol),
                  [&] { return sse::launch_sigma(sa, (int)n, st); }));
   if (launches) *launches += 2;

@@ -379,6 +379,296 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
 }
 
 // --------------------------------------------------------------------------
+// K3 (TMA, sliding window): the pipelined kernel fed from shared memory by a
+// single CTA-level producer (lane 0 of warp 0) issuing bulk-async copies
+// (cp.async.bulk -> SASS UBLKCP), with full/empty mbarriers per stage:
+//  * M fragments: one FV*512-byte copy per (q, s, w) stage into a ring of
+//    kSlideStages slots, shared by all 8 warps (8x less L2 traffic than
+//    per-warp loads);
+//  * G rows: within a (q, s) segment the CTA's window of source energies
+//    [E_lo - off_w, E_hi - off_w] slides down by one block per stage (the
+//    offsets are non-decreasing with steps <= 1, true of default_grid), so
+//    only the newly entering energy block is copied; blocks live in a FIFO
+//    ring of R slots (FIFO index = segment base + (segment top - energy)).
+// Consumers wait on the stage's full barrier, read fragments with LDS into the
+// register double buffer, run the 54 DMMAs and arrive on the empty barrier.
+// Accumulation order is identical to the other K3 kernels (bitwise equal).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared (TMA engine), completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kSlideStages = 12;
+constexpr int kSlideLookahead = 6;
+constexpr int kMaxSlideNw = 1024;
+
+template <int NO, int NW>
+struct SlideGeom {
+  static constexpr int kRows = NW * kRowTiles * 8;              // output rows per CTA
+  static constexpr int kTE = (kRows + NO - 1) / NO + 1;         // max energy blocks per window
+  static constexpr int kNeed = 2 * kTE + kSlideStages;          // live FIFO span bound
+  static constexpr int kRing = kNeed <= 32 ? 32 : (kNeed <= 64 ? 64 : 128);
+  static constexpr int kBVec = frag_geom(NO).fv * 32;            // double2 per M stage
+  static constexpr size_t kSmem = (size_t)kSlideStages * kBVec * 16 + (size_t)kRing * NO * NO * 16 +
+                                  2 * kSlideStages * 8 + kMaxSlideNw * 4;
+  static constexpr bool kFits = kSmem <= 225 * 1024;
+};
+
+template <int NO, int NW, bool DBUF>
+__global__ void __launch_bounds__(NW * 32, 1)
+sigma_dmma_slide_kernel(SigmaArgs p) {
+  constexpr FragGeom FG = frag_geom(NO);
+  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
+  using SG = SlideGeom<NO, NW>;
+  constexpr int R = SG::kRing, SB = kSlideStages, BVEC = SG::kBVec, BLK = NO * NO;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring_b = reinterpret_cast<double2*>(smem_raw);
+  double2* ring_a = ring_b + SB * BVEC;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring_a + R * BLK);
+  uint64_t* empty = full + SB;
+
+  const int pol = blockIdx.y;
+  int bx = blockIdx.x;
+  const int rc = bx % p.ctas_per_ak;
+  bx /= p.ctas_per_ak;
+  const int k = bx % p.nkz;
+  const int la = bx / p.nkz;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cta_r0 = rc * SG::kRows;
+  const int rbase = cta_r0 + warp * (kRowTiles * 8);
+  const int pcol = lane & 3;
+  const double2* __restrict__ G = p.G[pol];
+  const double2* __restrict__ Mf = p.M[pol];
+  const int* __restrict__ offs = p.off;
+  // stage t is produced by lane 0 of warp t % NW (round-robin), kSlideLookahead
+  // stages ahead of the consumers; every warp steps the producer state machine.
+
+  // CTA energy range (rows [cta_r0, cta_r0 + kRowsPerCta) clipped to the matrix)
+  const int e_lo = cta_r0 / NO;
+  const int e_hi = (min(cta_r0 + SG::kRows, p.rows) - 1) / NO;
+
+  int e_row[kRowTiles], m_off[kRowTiles];
+  bool v_row[kRowTiles];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t) {
+    const int row = rbase + t * 8 + (lane >> 2);
+    v_row[t] = row < p.rows;
+    e_row[t] = row / NO;
+    m_off[t] = (row - e_row[t] * NO) * NO + pcol;
+  }
+  const int warp_rows = min(kRowTiles * 8, p.rows - rbase);
+  const int warp_emax = warp_rows > 0 ? (rbase + warp_rows - 1) / NO : -1;
+
+  double acc[kRowTiles][NT][2];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+
+  int* s_off = reinterpret_cast<int*>(empty + SB);  // frequency offsets (p.nw <= kMaxSlideNw)
+  for (int w = threadIdx.x; w < p.nw; w += blockDim.x) s_off[w] = offs[w];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int n_it = p.nqz * p.nb * p.nw;
+
+  // Segment state machine, run identically by the producer and the consumers:
+  // seg_base = FIFO index of the segment top block, top0 = its energy,
+  // low = lowest energy of the segment loaded so far, next = next FIFO index.
+  struct Seg {
+    int q, s, w, it;
+    int seg_base, top0, low, next;
+    long long slab;
+    const double2* mf;
+  };
+  auto seg_begin = [&](Seg& g) {
+    int kp = (k - g.q) % p.nkz;
+    if (kp < 0) kp += p.nkz;
+    const int lb = __ldg(p.nbr + la * p.nb + g.s);
+    g.slab = lb * p.g_sa + kp * p.g_sk;
+    g.mf = Mf + ((long long)((la * p.nb + g.s) * p.nqz + g.q) * p.nw) * BVEC;
+    g.seg_base = g.next;
+    g.top0 = e_hi - s_off[0];
+    g.low = g.top0 + 1;
+  };
+  // Advance to the next stage; returns this stage's window bottom (clipped).
+  auto seg_step = [&](Seg& g, int off) {
+    const int lo = max(0, e_lo - off);
+    const int top = e_hi - off;
+    int new_lo = g.low;
+    if (top >= 0 && lo < g.low) new_lo = lo;
+    return new_lo;
+  };
+  auto seg_next = [&](Seg& g) {
+    ++g.it;
+    if (++g.w == p.nw) {
+      g.w = 0;
+      if (++g.s == p.nb) {
+        g.s = 0;
+        ++g.q;
+      }
+      g.next = (g.low <= g.top0) ? g.seg_base + (g.top0 - g.low) + 1 : g.seg_base;
+      if (g.q < p.nqz) seg_begin(g);
+    }
+  };
+
+  Seg prod{0, 0, 0, 0, 0, 0, 0, 0, 0, nullptr};
+  Seg cons{0, 0, 0, 0, 0, 0, 0, 0, 0, nullptr};
+  seg_begin(prod);
+  seg_begin(cons);
+
+  auto produce = [&](bool mine) {  // all lanes step the state; lane 0 of the owner issues
+    const int t = prod.it;
+    const int slot = t % SB;
+    const int off = s_off[prod.w];
+    const int new_lo = seg_step(prod, off);
+    if (mine && lane == 0) {
+      if (t >= SB) mbar_wait(empty + slot, (uint32_t)(((t - SB) / SB) & 1));
+      const int n_new = prod.low - new_lo;
+      mbar_arrive_expect_tx(full + slot, (uint32_t)(BVEC + n_new * BLK) * 16);
+      bulk_g2s(ring_b + slot * BVEC, prod.mf + prod.w * BVEC, BVEC * 16, full + slot);
+      for (int e = prod.low - 1; e >= new_lo; --e) {
+        const int f = (prod.seg_base + prod.top0 - e) & (R - 1);
+        bulk_g2s(ring_a + f * BLK, G + prod.slab + (long long)e * p.g_se, BLK * 16, full + slot);
+      }
+    }
+    prod.low = new_lo;
+    seg_next(prod);
+  };
+
+  // consumer: stage -> registers (waits on the stage's full barrier)
+  auto lds = [&](OperandStage<NO>& st) {
+    const int t = cons.it;
+    const int slot = t % SB;
+    const int off = s_off[cons.w];
+    st.off = off;
+    cons.low = seg_step(cons, off);
+    const int seg_base = cons.seg_base, top0 = cons.top0;
+    mbar_wait(full + slot, (uint32_t)((t / SB) & 1));
+    if (warp_emax >= off) {
+      const double2* sb = ring_b + slot * BVEC;
+#pragma unroll
+      for (int j = 0; j < FV; ++j) st.b[j] = sb[j * 32 + lane];
+#pragma unroll
+      for (int tt = 0; tt < kRowTiles; ++tt) {
+        const int e = e_row[tt] - off;
+        const bool ok = v_row[tt] && e >= 0;
+        const double2* src = ring_a + ((seg_base + top0 - e) & (R - 1)) * BLK + m_off[tt];
+#pragma unroll
+        for (int kk = 0; kk < KH; ++kk) {
+          st.a[tt][kk] = make_double2(0.0, 0.0);
+          if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO)) st.a[tt][kk] = src[4 * kk];
+        }
+      }
+    }
+    seg_next(cons);
+  };
+  // k-steps [k0, k1) of one stage's DMMAs (the stage is split around the
+  // blocking full-barrier wait of the next stage so the wait overlaps math)
+  auto compute_part = [&](const OperandStage<NO>& st, int k0, int k1) {
+    if (warp_emax < st.off) return;
+#pragma unroll
+    for (int kk = 0; kk < KSTEPS; ++kk) {
+      if (kk < k0 || kk >= k1) continue;
+#pragma unroll
+      for (int t = 0; t < kRowTiles; ++t) {
+        const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int f = kk * NT + nt;
+          const double b = (f & 1) ? st.b[f >> 1].y : st.b[f >> 1].x;
+          dmma884(acc[t][nt], a, b);
+        }
+      }
+    }
+  };
+  auto release = [&](int t) {  // the warp is done with stage t's shared memory
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + (t % SB));
+  };
+
+  constexpr int L = kSlideLookahead;
+  for (int i = 0; i < L && i < n_it; ++i) produce(i % NW == warp);
+  constexpr int KSPLIT = KSTEPS / 2;
+  if (DBUF) {
+    // register double buffer: stage it+1 is read from shared memory between
+    // the two halves of stage it's DMMAs
+    OperandStage<NO> s0, s1;
+    lds(s0);
+    for (int it = 0; it < n_it; it += 2) {
+      if (it + L < n_it) produce((it + L) % NW == warp);
+      compute_part(s0, 0, KSPLIT);
+      if (it + 1 < n_it) lds(s1);
+      compute_part(s0, KSPLIT, KSTEPS);
+      release(it);
+      if (it + 1 >= n_it) break;
+      if (it + 1 + L < n_it) produce((it + 1 + L) % NW == warp);
+      compute_part(s1, 0, KSPLIT);
+      if (it + 2 < n_it) lds(s0);
+      compute_part(s1, KSPLIT, KSTEPS);
+      release(it + 1);
+    }
+  } else {
+    // single buffer: the LDS latency is hidden by the other warps of the SMSP
+    OperandStage<NO> s0;
+    for (int it = 0; it < n_it; ++it) {
+      if (it + L < n_it) produce((it + L) % NW == warp);
+      lds(s0);
+      compute_part(s0, 0, KSTEPS);
+      release(it);
+    }
+  }
+
+  double2* __restrict__ S = p.S[pol];
+#pragma unroll
+  for (int t = 0; t < kRowTiles; ++t) {
+    if (!v_row[t]) continue;
+    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
+                   (long long)e_row[t] * p.s_se + m_off[t] - pcol;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int n = 4 * nt + (lane & 3);
+      if (n < NO) dst[n] = make_double2(-acc[t][nt][1], acc[t][nt][0]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // K3g: generic Sigma with DFMA (any No).  One thread per output element
 // (k, E, atom, m, n); compact operator M[q,w][p][n]; same (q, s, w) order.
 // --------------------------------------------------------------------------
@@ -527,27 +817,56 @@ cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Sigma kernel selection (env SSE_SIGMA_KERNEL, read per launch): 1 =
-// register-pipelined (default), 0 = simple.  Both accumulate every output in
-// the same (q, s, w, k-step) order, so they agree bitwise (tested).
+// Sigma kernel selection (env SSE_SIGMA_KERNEL, read per launch):
+//   3 = TMA sliding-window, 12 warps (default when the offsets slide),
+//   2 = TMA sliding-window, 8 warps with a register double buffer,
+//   1 = register-pipelined (default otherwise), 0 = simple.
+// All accumulate every output in the same (q, s, w, k-step) order, so they
+// agree bitwise (tested).
 static int sigma_kernel_choice() {
   const char* env = getenv("SSE_SIGMA_KERNEL");
-  return env ? atoi(env) : 1;
+  return env ? atoi(env) : 3;
 }
 
 template <int NO>
-static void launch_dmma(const SigmaArgs& a, int chunk_atoms, cudaStream_t st) {
-  dim3 grid((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
-  if (sigma_kernel_choice() == 0)
+static void launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
+  SigmaArgs a = a0;
+  const int choice = sigma_kernel_choice();
+  auto grid_for_rows = [&](int rows_per_cta) {
+    a.ctas_per_ak = (a.rows + rows_per_cta - 1) / rows_per_cta;
+    return dim3((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
+  };
+  if (choice == 0) {
+    const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  else
+  } else if ((choice == 2 || choice == 3) && a.off_slide && a.nw <= kMaxSlideNw) {
+    if (choice == 2 && SlideGeom<NO, 8>::kFits) {
+      const dim3 grid = grid_for_rows(SlideGeom<NO, 8>::kRows);
+      const size_t smem = SlideGeom<NO, 8>::kSmem;
+      cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      sigma_dmma_slide_kernel<NO, 8, true><<<grid, 8 * 32, smem, st>>>(a);
+      return;
+    }
+    if (choice == 3 && SlideGeom<NO, 12>::kFits) {
+      const dim3 grid = grid_for_rows(SlideGeom<NO, 12>::kRows);
+      const size_t smem = SlideGeom<NO, 12>::kSmem;
+      cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      sigma_dmma_slide_kernel<NO, 12, false><<<grid, 12 * 32, smem, st>>>(a);
+      return;
+    }
+    const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
+  } else {
+    const dim3 grid = grid_for_rows(kRowsPerCta);
+    sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
+  }
 }
 
 cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
   SigmaArgs a = a0;
   if (a.no <= kMaxDmmaOrb) {
-    a.ctas_per_ak = (a.rows + kRowsPerCta - 1) / kRowsPerCta;
     switch (a.no) {
       case 1: launch_dmma<1>(a, chunk_atoms, st); break;
       case 2: launch_dmma<2>(a, chunk_atoms, st); break;

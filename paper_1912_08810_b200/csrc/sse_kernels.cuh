@@ -57,6 +57,7 @@ struct SigmaArgs {
   long long g_sa, g_sk, g_se;  // G slab strides in complex elements
   long long s_sa, s_sk, s_se;  // Sigma slab strides in complex elements
   int npol;               // polarities to process (1 or 2)
+  int off_slide;          // 1: offsets non-decreasing with steps <= 1 (sliding-window K3 eligible)
 };
 
 cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st);

@@ -115,16 +115,20 @@ def test_deterministic_bitwise():
     assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
 
 
-def test_simple_and_pipelined_kernels_bitwise(monkeypatch):
-    """Both K3 kernels accumulate in the same (q, s, w, k-step) order."""
-    c = load_case("orb10_s6")
+@pytest.mark.parametrize("name", ["orb10_s6", "orb12_s5", "cli_small_s2", "general_grid_s8"])
+def test_all_sigma_kernels_bitwise(monkeypatch, name):
+    """Every K3 kernel (simple, pipelined, TMA sliding-window x2) accumulates in the
+    same (q, s, w, k-step) order: outputs are bitwise equal (the general grid's
+    non-sliding offsets route the TMA choices to the pipelined kernel)."""
+    c = load_case(name)
     args = (GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx), _grid(c))
-    monkeypatch.setenv("SSE_SIGMA_KERNEL", "1")
-    a = sse_sigma(SseVariant.BATCHED_FUSED, *args)
-    monkeypatch.setenv("SSE_SIGMA_KERNEL", "0")
-    b = sse_sigma(SseVariant.BATCHED_FUSED, *args)
-    assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
-    dev = orc.parity_dev(b.lesser, b.greater, c.arrays["sigma_l"], c.arrays["sigma_g"])
+    outs = []
+    for choice in ("0", "1", "2", "3"):
+        monkeypatch.setenv("SSE_SIGMA_KERNEL", choice)
+        outs.append(sse_sigma(SseVariant.BATCHED_FUSED, *args))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
+    dev = orc.parity_dev(outs[0].lesser, outs[0].greater, c.arrays["sigma_l"], c.arrays["sigma_g"])
     assert dev <= TOL
 
 
