@@ -507,78 +507,44 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 
   const int n_it = p.nqz * p.nb * p.nw;
 
-  // Segment state machine, run identically by the producer and the consumers:
-  // seg_base = FIFO index of the segment top block, top0 = its energy,
-  // low = lowest energy of the segment loaded so far, next = next FIFO index.
-  struct Seg {
-    int q, s, w, it;
-    int seg_base, top0, low, next;
-    long long slab;
-    const double2* mf;
-  };
-  auto seg_begin = [&](Seg& g) {
-    int kp = (k - g.q) % p.nkz;
+  // Window bookkeeping in closed form.  Segment sg = (q, s) covers stages
+  // [sg*nw, (sg+1)*nw); its window at stage w is [max(0, e_lo - off_w),
+  // e_hi - off_w].  With non-decreasing offsets (steps <= 1) the window bottom
+  // L(w) = max(0, e_lo - off_w) never rises, so stage w loads exactly the
+  // blocks [L(w), L(w-1) - 1] (L(-1) = top0 + 1, top0 = e_hi - off_0) and a
+  // segment loads seg_blocks blocks.  Energy e of segment sg sits at FIFO
+  // index sg * seg_blocks + (top0 - e).
+  const int top0 = e_hi - s_off[0];
+  const bool seg_empty = top0 < 0;
+  const int seg_blocks = seg_empty ? 0 : top0 + 1 - max(0, e_lo - s_off[p.nw - 1]);
+  auto win_low = [&](int w) { return w < 0 ? top0 + 1 : max(0, e_lo - s_off[w]); };
+
+  auto produce = [&](int t) {  // lane 0 of the owning warp
+    const int slot = t % SB;
+    const int sg = t / p.nw, w = t - sg * p.nw;
+    const int q = sg / p.nb, s = sg - q * p.nb;
+    int kp = (k - q) % p.nkz;
     if (kp < 0) kp += p.nkz;
-    const int lb = __ldg(p.nbr + la * p.nb + g.s);
-    g.slab = lb * p.g_sa + kp * p.g_sk;
-    g.mf = Mf + ((long long)((la * p.nb + g.s) * p.nqz + g.q) * p.nw) * BVEC;
-    g.seg_base = g.next;
-    g.top0 = e_hi - s_off[0];
-    g.low = g.top0 + 1;
-  };
-  // Advance to the next stage; returns this stage's window bottom (clipped).
-  auto seg_step = [&](Seg& g, int off) {
-    const int lo = max(0, e_lo - off);
-    const int top = e_hi - off;
-    int new_lo = g.low;
-    if (top >= 0 && lo < g.low) new_lo = lo;
-    return new_lo;
-  };
-  auto seg_next = [&](Seg& g) {
-    ++g.it;
-    if (++g.w == p.nw) {
-      g.w = 0;
-      if (++g.s == p.nb) {
-        g.s = 0;
-        ++g.q;
-      }
-      g.next = (g.low <= g.top0) ? g.seg_base + (g.top0 - g.low) + 1 : g.seg_base;
-      if (g.q < p.nqz) seg_begin(g);
+    const long long slab = __ldg(p.nbr + la * p.nb + s) * p.g_sa + kp * p.g_sk;
+    const double2* mf = Mf + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw + w) * BVEC;
+    const int hi = seg_empty ? 0 : win_low(w - 1), lo = seg_empty ? 0 : win_low(w);
+    if (t >= SB) mbar_wait(empty + slot, (uint32_t)(((t - SB) / SB) & 1));
+    mbar_arrive_expect_tx(full + slot, (uint32_t)(BVEC + (hi - lo) * BLK) * 16);
+    bulk_g2s(ring_b + slot * BVEC, mf, BVEC * 16, full + slot);
+    for (int e = hi - 1; e >= lo; --e) {
+      const int f = (sg * seg_blocks + top0 - e) & (R - 1);
+      bulk_g2s(ring_a + f * BLK, G + slab + (long long)e * p.g_se, BLK * 16, full + slot);
     }
   };
 
-  Seg prod{0, 0, 0, 0, 0, 0, 0, 0, 0, nullptr};
-  Seg cons{0, 0, 0, 0, 0, 0, 0, 0, 0, nullptr};
-  seg_begin(prod);
-  seg_begin(cons);
-
-  auto produce = [&](bool mine) {  // all lanes step the state; lane 0 of the owner issues
-    const int t = prod.it;
-    const int slot = t % SB;
-    const int off = s_off[prod.w];
-    const int new_lo = seg_step(prod, off);
-    if (mine && lane == 0) {
-      if (t >= SB) mbar_wait(empty + slot, (uint32_t)(((t - SB) / SB) & 1));
-      const int n_new = prod.low - new_lo;
-      mbar_arrive_expect_tx(full + slot, (uint32_t)(BVEC + n_new * BLK) * 16);
-      bulk_g2s(ring_b + slot * BVEC, prod.mf + prod.w * BVEC, BVEC * 16, full + slot);
-      for (int e = prod.low - 1; e >= new_lo; --e) {
-        const int f = (prod.seg_base + prod.top0 - e) & (R - 1);
-        bulk_g2s(ring_a + f * BLK, G + prod.slab + (long long)e * p.g_se, BLK * 16, full + slot);
-      }
-    }
-    prod.low = new_lo;
-    seg_next(prod);
-  };
-
-  // consumer: stage -> registers (waits on the stage's full barrier)
+  // consumer cursor
+  int c_it = 0, c_sg = 0, c_w = 0;
   auto lds = [&](OperandStage<NO>& st) {
-    const int t = cons.it;
+    const int t = c_it;
     const int slot = t % SB;
-    const int off = s_off[cons.w];
+    const int off = s_off[c_w];
     st.off = off;
-    cons.low = seg_step(cons, off);
-    const int seg_base = cons.seg_base, top0 = cons.top0;
+    const int fbase = c_sg * seg_blocks + top0 + off;  // FIFO index of row energy E: fbase - E
     mbar_wait(full + slot, (uint32_t)((t / SB) & 1));
     if (warp_emax >= off) {
       const double2* sb = ring_b + slot * BVEC;
@@ -586,9 +552,8 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
       for (int j = 0; j < FV; ++j) st.b[j] = sb[j * 32 + lane];
 #pragma unroll
       for (int tt = 0; tt < kRowTiles; ++tt) {
-        const int e = e_row[tt] - off;
-        const bool ok = v_row[tt] && e >= 0;
-        const double2* src = ring_a + ((seg_base + top0 - e) & (R - 1)) * BLK + m_off[tt];
+        const bool ok = v_row[tt] && e_row[tt] >= off;
+        const double2* src = ring_a + ((fbase - e_row[tt]) & (R - 1)) * BLK + m_off[tt];
 #pragma unroll
         for (int kk = 0; kk < KH; ++kk) {
           st.a[tt][kk] = make_double2(0.0, 0.0);
@@ -596,7 +561,11 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
         }
       }
     }
-    seg_next(cons);
+    ++c_it;
+    if (++c_w == p.nw) {
+      c_w = 0;
+      ++c_sg;
+    }
   };
   // k-steps [k0, k1) of one stage's DMMAs (the stage is split around the
   // blocking full-barrier wait of the next stage so the wait overlaps math)
@@ -623,7 +592,8 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   };
 
   constexpr int L = kSlideLookahead;
-  for (int i = 0; i < L && i < n_it; ++i) produce(i % NW == warp);
+  if (lane == 0)
+    for (int i = warp; i < L && i < n_it; i += NW) produce(i);
   constexpr int KSPLIT = KSTEPS / 2;
   if (DBUF) {
     // register double buffer: stage it+1 is read from shared memory between
@@ -631,13 +601,13 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     OperandStage<NO> s0, s1;
     lds(s0);
     for (int it = 0; it < n_it; it += 2) {
-      if (it + L < n_it) produce((it + L) % NW == warp);
+      if (lane == 0 && it + L < n_it && (it + L) % NW == warp) produce(it + L);
       compute_part(s0, 0, KSPLIT);
       if (it + 1 < n_it) lds(s1);
       compute_part(s0, KSPLIT, KSTEPS);
       release(it);
       if (it + 1 >= n_it) break;
-      if (it + 1 + L < n_it) produce((it + 1 + L) % NW == warp);
+      if (lane == 0 && it + 1 + L < n_it && (it + 1 + L) % NW == warp) produce(it + 1 + L);
       compute_part(s1, 0, KSPLIT);
       if (it + 2 < n_it) lds(s0);
       compute_part(s1, KSPLIT, KSTEPS);
@@ -647,7 +617,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     // single buffer: the LDS latency is hidden by the other warps of the SMSP
     OperandStage<NO> s0;
     for (int it = 0; it < n_it; ++it) {
-      if (it + L < n_it) produce((it + L) % NW == warp);
+      if (lane == 0 && it + L < n_it && (it + L) % NW == warp) produce(it + L);
       lds(s0);
       compute_part(s0, 0, KSTEPS);
       release(it);
