@@ -41,9 +41,8 @@ def k3_kernel_name() -> str:
     return {
         "0": "sigma_dmma_kernel<12> (K3 simple)",
         "1": "sigma_dmma_pipe_kernel<12> (K3 register-pipelined)",
-        "2": "sigma_dmma_slide_kernel<12,8,dbuf> (K3 TMA sliding window, 8 warps)",
     }.get(os.environ.get("SSE_SIGMA_KERNEL", "3"),
-          "sigma_dmma_slide_kernel<12,12> (K3 TMA sliding window, 12 warps)")
+          "sigma_dmma_slide_kernel<12,12,3> (K3 TMA sliding window, 12 warps x 3 row tiles)")
 
 
 def env_rank():

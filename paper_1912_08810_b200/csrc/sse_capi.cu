@@ -329,6 +329,7 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   sa.s_se = ss.se;
   sa.npol = npol;
   sa.off_slide = 1;
+  sa.lookahead = getenv("SSE_SLIDE_LOOKAHEAD") ? atoi(getenv("SSE_SLIDE_LOOKAHEAD")) : 0;
   for (int64_t w = 1; w < d->nw; ++w)
     if (off[w] < off[w - 1] || off[w] > off[w - 1] + 1) sa.off_slide = 0;
   CHECK(profiled(ds, st, SSE_PROF_SIGMA, alg_flops(d, off, n, npol),

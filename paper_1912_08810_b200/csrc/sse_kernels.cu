@@ -253,12 +253,14 @@ sigma_dmma_kernel(SigmaArgs p) {
 //    independent accumulator chains separate dependent DMMAs;
 //  * the E < off skip is warp-uniform (no branches between the tiles).
 // --------------------------------------------------------------------------
-template <int NO>
-struct OperandStage {
-  double2 a[kRowTiles][frag_geom(NO).kh];
+template <int NO, int MT>
+struct OperandStageT {
+  double2 a[MT][frag_geom(NO).kh];
   double2 b[frag_geom(NO).fv];
   int off;
 };
+template <int NO>
+using OperandStage = OperandStageT<NO, kRowTiles>;
 
 template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32, 1)
@@ -379,19 +381,20 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
 }
 
 // --------------------------------------------------------------------------
-// K3 (TMA, sliding window): the pipelined kernel fed from shared memory by a
-// single CTA-level producer (lane 0 of warp 0) issuing bulk-async copies
-// (cp.async.bulk -> SASS UBLKCP), with full/empty mbarriers per stage:
+// K3 (TMA, sliding window) — production kernel: the DMMA contraction fed
+// from shared memory by bulk-async copies (cp.async.bulk -> SASS UBLKCP)
+// with full/empty mbarriers per stage; 12 warps x 3 row tiles (288 rows), one
+// CTA per SM, 160 registers (3 warps per SMSP keep the DMMA pipe fed).
 //  * M fragments: one FV*512-byte copy per (q, s, w) stage into a ring of
-//    kSlideStages slots, shared by all 8 warps (8x less L2 traffic than
-//    per-warp loads);
+//    kSlideStages slots, shared by all warps;
 //  * G rows: within a (q, s) segment the CTA's window of source energies
-//    [E_lo - off_w, E_hi - off_w] slides down by one block per stage (the
-//    offsets are non-decreasing with steps <= 1, true of default_grid), so
-//    only the newly entering energy block is copied; blocks live in a FIFO
-//    ring of R slots (FIFO index = segment base + (segment top - energy)).
-// Consumers wait on the stage's full barrier, read fragments with LDS into the
-// register double buffer, run the 54 DMMAs and arrive on the empty barrier.
+//    [E_lo - off_w, E_hi - off_w] slides down by one block per stage (offsets
+//    non-decreasing with steps <= 1, as default_grid's are), so only the
+//    entering energy block is copied; blocks live in a FIFO ring of R slots;
+//  * stage t is produced by lane 0 of warp t % NW, kSlideLookahead stages
+//    ahead (round-robin spreads the producer work over the warps);
+//  * consumers wait on the stage's full barrier, read fragments with LDS,
+//    run the DMMAs and arrive on the stage's empty barrier.
 // Accumulation order is identical to the other K3 kernels (bitwise equal).
 // --------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -431,9 +434,9 @@ constexpr int kSlideStages = 12;
 constexpr int kSlideLookahead = 6;
 constexpr int kMaxSlideNw = 1024;
 
-template <int NO, int NW>
+template <int NO, int NW, int MT>
 struct SlideGeom {
-  static constexpr int kRows = NW * kRowTiles * 8;              // output rows per CTA
+  static constexpr int kRows = NW * MT * 8;              // output rows per CTA
   static constexpr int kTE = (kRows + NO - 1) / NO + 1;         // max energy blocks per window
   static constexpr int kNeed = 2 * kTE + kSlideStages;          // live FIFO span bound
   static constexpr int kRing = kNeed <= 32 ? 32 : (kNeed <= 64 ? 64 : 128);
@@ -443,12 +446,12 @@ struct SlideGeom {
   static constexpr bool kFits = kSmem <= 225 * 1024;
 };
 
-template <int NO, int NW, bool DBUF>
+template <int NO, int NW, int MT>
 __global__ void __launch_bounds__(NW * 32, 1)
 sigma_dmma_slide_kernel(SigmaArgs p) {
   constexpr FragGeom FG = frag_geom(NO);
   constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
-  using SG = SlideGeom<NO, NW>;
+  using SG = SlideGeom<NO, NW, MT>;
   constexpr int R = SG::kRing, SB = kSlideStages, BVEC = SG::kBVec, BLK = NO * NO;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* ring_b = reinterpret_cast<double2*>(smem_raw);
@@ -464,7 +467,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   const int la = bx / p.nkz;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cta_r0 = rc * SG::kRows;
-  const int rbase = cta_r0 + warp * (kRowTiles * 8);
+  const int rbase = cta_r0 + warp * (MT * 8);
   const int pcol = lane & 3;
   const double2* __restrict__ G = p.G[pol];
   const double2* __restrict__ Mf = p.M[pol];
@@ -476,21 +479,21 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   const int e_lo = cta_r0 / NO;
   const int e_hi = (min(cta_r0 + SG::kRows, p.rows) - 1) / NO;
 
-  int e_row[kRowTiles], m_off[kRowTiles];
-  bool v_row[kRowTiles];
+  int e_row[MT], m_off[MT];
+  bool v_row[MT];
 #pragma unroll
-  for (int t = 0; t < kRowTiles; ++t) {
+  for (int t = 0; t < MT; ++t) {
     const int row = rbase + t * 8 + (lane >> 2);
     v_row[t] = row < p.rows;
     e_row[t] = row / NO;
     m_off[t] = (row - e_row[t] * NO) * NO + pcol;
   }
-  const int warp_rows = min(kRowTiles * 8, p.rows - rbase);
+  const int warp_rows = min(MT * 8, p.rows - rbase);
   const int warp_emax = warp_rows > 0 ? (rbase + warp_rows - 1) / NO : -1;
 
-  double acc[kRowTiles][NT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int t = 0; t < kRowTiles; ++t)
+  for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
@@ -539,7 +542,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 
   // consumer cursor
   int c_it = 0, c_sg = 0, c_w = 0;
-  auto lds = [&](OperandStage<NO>& st) {
+  auto lds = [&](OperandStageT<NO, MT>& st) {
     const int t = c_it;
     const int slot = t % SB;
     const int off = s_off[c_w];
@@ -551,7 +554,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 #pragma unroll
       for (int j = 0; j < FV; ++j) st.b[j] = sb[j * 32 + lane];
 #pragma unroll
-      for (int tt = 0; tt < kRowTiles; ++tt) {
+      for (int tt = 0; tt < MT; ++tt) {
         const bool ok = v_row[tt] && e_row[tt] >= off;
         const double2* src = ring_a + ((fbase - e_row[tt]) & (R - 1)) * BLK + m_off[tt];
 #pragma unroll
@@ -567,15 +570,14 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
       ++c_sg;
     }
   };
-  // k-steps [k0, k1) of one stage's DMMAs (the stage is split around the
-  // blocking full-barrier wait of the next stage so the wait overlaps math)
-  auto compute_part = [&](const OperandStage<NO>& st, int k0, int k1) {
+  // k-steps [k0, k1) of one stage's DMMAs
+  auto compute_part = [&](const OperandStageT<NO, MT>& st, int k0, int k1) {
     if (warp_emax < st.off) return;
 #pragma unroll
     for (int kk = 0; kk < KSTEPS; ++kk) {
       if (kk < k0 || kk >= k1) continue;
 #pragma unroll
-      for (int t = 0; t < kRowTiles; ++t) {
+      for (int t = 0; t < MT; ++t) {
         const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -591,31 +593,12 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     if (lane == 0) mbar_arrive(empty + (t % SB));
   };
 
-  constexpr int L = kSlideLookahead;
+  const int L = p.lookahead > 0 ? min(p.lookahead, SB - 1) : kSlideLookahead;
   if (lane == 0)
     for (int i = warp; i < L && i < n_it; i += NW) produce(i);
-  constexpr int KSPLIT = KSTEPS / 2;
-  if (DBUF) {
-    // register double buffer: stage it+1 is read from shared memory between
-    // the two halves of stage it's DMMAs
-    OperandStage<NO> s0, s1;
-    lds(s0);
-    for (int it = 0; it < n_it; it += 2) {
-      if (lane == 0 && it + L < n_it && (it + L) % NW == warp) produce(it + L);
-      compute_part(s0, 0, KSPLIT);
-      if (it + 1 < n_it) lds(s1);
-      compute_part(s0, KSPLIT, KSTEPS);
-      release(it);
-      if (it + 1 >= n_it) break;
-      if (lane == 0 && it + 1 + L < n_it && (it + 1 + L) % NW == warp) produce(it + 1 + L);
-      compute_part(s1, 0, KSPLIT);
-      if (it + 2 < n_it) lds(s0);
-      compute_part(s1, KSPLIT, KSTEPS);
-      release(it + 1);
-    }
-  } else {
+  {
     // single buffer: the LDS latency is hidden by the other warps of the SMSP
-    OperandStage<NO> s0;
+    OperandStageT<NO, MT> s0;
     for (int it = 0; it < n_it; ++it) {
       if (lane == 0 && it + L < n_it && (it + L) % NW == warp) produce(it + L);
       lds(s0);
@@ -626,7 +609,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 
   double2* __restrict__ S = p.S[pol];
 #pragma unroll
-  for (int t = 0; t < kRowTiles; ++t) {
+  for (int t = 0; t < MT; ++t) {
     if (!v_row[t]) continue;
     double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
                    (long long)e_row[t] * p.s_se + m_off[t] - pcol;
@@ -788,9 +771,9 @@ cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
 }
 
 // Sigma kernel selection (env SSE_SIGMA_KERNEL, read per launch):
-//   3 = TMA sliding-window, 12 warps (default when the offsets slide),
-//   2 = TMA sliding-window, 8 warps with a register double buffer,
-//   1 = register-pipelined (default otherwise), 0 = simple.
+//   3 = TMA sliding-window, 12 warps x 3 row tiles (default when the offsets
+//       slide, i.e. non-decreasing with steps <= 1, as default_grid's do),
+//   1 = register-pipelined (used otherwise), 0 = simple.
 // All accumulate every output in the same (q, s, w, k-step) order, so they
 // agree bitwise (tested).
 static int sigma_kernel_choice() {
@@ -809,21 +792,13 @@ static void launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
   if (choice == 0) {
     const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  } else if ((choice == 2 || choice == 3) && a.off_slide && a.nw <= kMaxSlideNw) {
-    if (choice == 2 && SlideGeom<NO, 8>::kFits) {
-      const dim3 grid = grid_for_rows(SlideGeom<NO, 8>::kRows);
-      const size_t smem = SlideGeom<NO, 8>::kSmem;
-      cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  } else if (choice == 3 && a.off_slide && a.nw <= kMaxSlideNw) {
+    if (SlideGeom<NO, 12, 3>::kFits) {
+      const dim3 grid = grid_for_rows(SlideGeom<NO, 12, 3>::kRows);
+      const size_t smem = SlideGeom<NO, 12, 3>::kSmem;
+      cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
-      sigma_dmma_slide_kernel<NO, 8, true><<<grid, 8 * 32, smem, st>>>(a);
-      return;
-    }
-    if (choice == 3 && SlideGeom<NO, 12>::kFits) {
-      const dim3 grid = grid_for_rows(SlideGeom<NO, 12>::kRows);
-      const size_t smem = SlideGeom<NO, 12>::kSmem;
-      cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      sigma_dmma_slide_kernel<NO, 12, false><<<grid, 12 * 32, smem, st>>>(a);
+      sigma_dmma_slide_kernel<NO, 12, 3><<<grid, 12 * 32, smem, st>>>(a);
       return;
     }
     const dim3 grid = grid_for_rows(kRowsPerCta);

@@ -58,6 +58,7 @@ struct SigmaArgs {
   long long s_sa, s_sk, s_se;  // Sigma slab strides in complex elements
   int npol;               // polarities to process (1 or 2)
   int off_slide;          // 1: offsets non-decreasing with steps <= 1 (sliding-window K3 eligible)
+  int lookahead;          // sliding-window K3 producer lookahead (0 = default)
 };
 
 cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st);

@@ -52,7 +52,7 @@ def test_library_is_sm100a_only():
 @pytest.mark.parametrize("kernel, dmma", [
     ("_ZN3sse22sigma_dmma_pipe_kernelILi12EEEvNS_9SigmaArgsE", 108),  # production K3 (2 stages x 54)
     ("_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", 54),        # simple K3
-    ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELb0EEEvNS_9SigmaArgsE", 54),  # TMA sliding-window K3
+    ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELi3EEEvNS_9SigmaArgsE", 54),  # TMA sliding-window K3
 ])
 def test_fp64_tensor_core_sass_present(kernel, dmma):
     """The Sigma kernels issue DMMA.8x8x4 (FP64 tensor cores), not a CPU/DFMA fallback."""
