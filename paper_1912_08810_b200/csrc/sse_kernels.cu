@@ -792,7 +792,11 @@ static void launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
   if (choice == 0) {
     const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  } else if (choice == 3 && a.off_slide && a.nw <= kMaxSlideNw) {
+  } else if (choice == 3 && a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw) {
+    // nw >= kSlideStages: the kSlideStages stages in flight span at most one
+    // (q, s) segment boundary, so at most 2 * kTE + kSlideStages FIFO blocks
+    // are live (SlideGeom::kNeed <= kRing); shorter segments use the
+    // register-pipelined kernel.
     if (SlideGeom<NO, 12, 3>::kFits) {
       const dim3 grid = grid_for_rows(SlideGeom<NO, 12, 3>::kRows);
       const size_t smem = SlideGeom<NO, 12, 3>::kSmem;

@@ -132,6 +132,33 @@ def test_all_sigma_kernels_bitwise(monkeypatch, name):
     assert dev <= TOL
 
 
+@pytest.mark.parametrize("n_e, n_w, n_o, n_a", [
+    (24, 6, 12, 10),    # the smoke shape: 6 offsets < 12 ring stages (pipelined fallback)
+    (48, 12, 12, 6),    # sliding-window kernel, one CTA tile, segments of exactly 12 stages
+    (64, 20, 12, 5),    # sliding-window kernel, two CTA tiles, window clipped at E = 0
+    (40, 13, 10, 6),    # No = 10 (padded DMMA embedding; ring too large: pipelined kernel)
+    (31, 16, 4, 7),     # No = 4, ragged last tile
+])
+def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a):
+    """Shapes that exercise the K3 ring/window logic, checked against the oracle
+    (pinned to the reference by tests/test_oracle.py) for every kernel choice."""
+    p = SimParams(n_kz=3, n_qz=2, n_E=n_e, n_w=n_w, n_A=n_a, n_B=4, n_orb=n_o)
+    g_l, g_g, d_l, d_g, dh = inputs.stream_instance(11, p, dh_scale=0.05)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    dc = CombinedD(*orc.preprocess_D(d_l, d_g, nmap.idx))
+    off, wt = np.array(grid.offsets), np.array(grid.weights)
+    ref_l, ref_g = orc.sigma_batched_fused(g_l, g_g, dc.lesser, dc.greater, dh, nmap.idx, off, wt)
+    outs = []
+    for choice in ("0", "1", "3"):
+        monkeypatch.setenv("SSE_SIGMA_KERNEL", choice)
+        out = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(g_l, g_g), dc, dh, nmap, grid)
+        assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
+        outs.append(out)
+    for o in outs[1:]:
+        assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
+
+
 def test_layout_transformed_equals_grid_major_bitwise():
     """K1 round trip is lossless and the atom-major accumulation has the same order."""
     c = load_case("orb12_s5")
