@@ -17,16 +17,29 @@ from paper_1912_08810_b200.problem import ShardProblem
 
 
 class DeviceProblem(ShardProblem):
+    """Rank `rank` of a `world`-way atom sharding, on device `rank`, halo filled locally."""
+
     def __init__(self, name, seed=0, world=1, rank=0):
-        super().__init__(inputs.CONFIGS[name], rank=rank, world=world, seed=seed)
+        super().__init__(inputs.CONFIGS[name], rank=rank, world=world, device=rank, seed=seed)
+
+    def launch(self):
+        with self.torch.cuda.device(self.device):
+            self.fill(owned_g_only=False)
+            self.step()
 
     def run(self):
-        self.fill(owned_g_only=False)
-        self.step()
-        self.torch.cuda.synchronize()
+        self.launch()
+        self.torch.cuda.synchronize(self.device)
 
-    def sigma_block(self, pol, k, e, a):
-        return super().sigma_block(pol, k, e, a)
+
+def run_sharded(name, world, seed=0):
+    """All shards of a config, one per GPU, launched concurrently."""
+    shards = [DeviceProblem(name, seed, world, r) for r in range(world)]
+    for sh in shards:
+        sh.launch()
+    for sh in shards:
+        sh.torch.cuda.synchronize(sh.device)
+    return shards
 
 
 def host_point(prob: ShardProblem, pol: int, k: int, e: int, a: int) -> np.ndarray:

@@ -345,3 +345,40 @@ def test_paper_config_sampled_points():
     p = inputs.CONFIGS["paper"]
     dev = _full_scale_points("paper", 0, 4, [0, 1, 2, 2431, p.n_A - 2, p.n_A - 1])
     assert dev <= TOL
+
+
+def _sharded_points(name, world, atoms_per_shard=3, points=3, seed=0):
+    torch = _torch()
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"{name} needs {world} GPUs for its memory footprint")
+    from tests.scale_helpers import host_point, run_sharded
+
+    shards = run_sharded(name, world, seed)
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for sh in shards:
+        p = sh.p
+        atoms = {sh.lo, sh.hi - 1, *rng.integers(sh.lo, sh.hi, atoms_per_shard - 2).tolist()}
+        for a in sorted(atoms):
+            for e in sorted({p.n_E - 1, *rng.integers(0, p.n_E, points).tolist()}):
+                k = int(rng.integers(0, p.n_kz))
+                for pol in (0, 1):
+                    got = sh.sigma_block(pol, k, e, a)
+                    ref = host_point(sh, pol, k, e, a)
+                    worst = max(worst, float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)))
+    for sh in shards:
+        sh.free()
+    torch.cuda.empty_cache()
+    return worst
+
+
+@pytest.mark.slow
+def test_kheavy_config_sampled_points_two_gpus():
+    """Nkz = Nqz = 7 (k - q wrap over 7 momenta), 221.5 GB: atom-sharded over 2 B200."""
+    assert _sharded_points("kheavy", 2) <= TOL
+
+
+@pytest.mark.slow
+def test_large_config_sampled_points_four_gpus():
+    """NA = 10,240, NE = 1,220, Nkz = Nqz = 5, 575.7 GB: atom-sharded over 4 B200."""
+    assert _sharded_points("large", 4) <= TOL
