@@ -129,6 +129,29 @@ int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
                      double* Sig_l, double* Sig_g, void* stream,
                      sse_timing* t);
 
+/* Phonon self-energy Pi^{<>} (drop-in for negflow.sse.sse_pi, sse.py:409-428;
+ * chains sse.py:332-390, slots sse.py:393-406):
+ *   chain[q,w,a,s,i,j] = w_E sum_{k,E: E+off_w<NE} tr(dH[a,s,i] G1[(k+q)%Nkz, E+off_w, a]
+ *                                                   dH[a,s,j] G2[k,E,f(a,s)]),
+ *   greater: (G1,G2) = (G>,G<), lesser: (G<,G>);
+ *   Pi[q,w,a,0] = -i sum_s chain, Pi[q,w,a,1+s] = +i chain;  Pi [Nqz, Nw, NA, NB+1, 3, 3].
+ * d->nqz is the reference's n_qz argument; off: frequency offsets; energy_weight: w_E;
+ * mask: optional uint8 [Nkz, NE] point mask (sse.py:362-364: G2 zeroed where 0), NULL = all.
+ * Host call: atoms [atom_lo, atom_hi) are computed (atom_range), Pi rows of the
+ * other atoms are left untouched (the caller zero-fills, as the reference's are 0). */
+int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double* G_g,
+                const double* dH, const int64_t* nmap, const int64_t* off,
+                double energy_weight, const unsigned char* mask, int64_t atom_lo,
+                int64_t atom_hi, double* Pi_l, double* Pi_g, sse_timing* t);
+/* Device-resident Pi of an owned atom range: g = slab with the owned atoms and
+ * all their neighbours; dH [out.natoms, NB, 3, No, No]; nmap HOST [out.natoms, NB]
+ * (global ids); Pi_* device [Nqz, Nw, out.natoms, NB+1, 3, 3]. */
+int sse_pi_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
+                  const double* G_l, const double* G_g, const double* dH,
+                  const int64_t* nmap, const int64_t* off, double energy_weight,
+                  const unsigned char* mask, double* Pi_l, double* Pi_g, void* stream,
+                  sse_timing* t);
+
 /* Layout transform K1 (to_atom_major / to_grid_major, sse.py:48-55):
  * [Nkz, NE, NA, blk] <-> [NA, Nkz, NE, blk], blk = block_doubles doubles.
  * to_atom_major = 1: grid -> atom major; 0: atom -> grid major.  Device ptrs. */
@@ -172,7 +195,10 @@ int sse_fill_synthetic(sse_ctx* ctx, uint64_t seed, uint32_t tensor_id,
 #define SSE_PROF_SIGMA 1      /* K3 fused Sigma (DMMA) */
 #define SSE_PROF_LAYOUT 2     /* K1 layout transform */
 #define SSE_PROF_PREPROCESS 3 /* preprocess_D */
-#define SSE_PROF_KINDS 4
+#define SSE_PROF_PI_BUILD 4   /* K5 Pi operand build */
+#define SSE_PROF_PI 5         /* K6 Pi chains (DMMA) */
+#define SSE_PROF_PI_ASSEMBLE 6 /* K7 Pi slot assembly */
+#define SSE_PROF_KINDS 7
 typedef struct sse_profile {
   double ms[SSE_PROF_KINDS];
   double flops[SSE_PROF_KINDS];

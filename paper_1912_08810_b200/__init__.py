@@ -17,7 +17,7 @@ from .types import (
     build_neighbor_map,
     default_grid,
 )
-from .sse import alg_flops, sigma_tallies, sse_sigma
+from .sse import alg_flops, pi_tallies, sigma_tallies, sse_pi, sse_sigma
 
 __version__ = "0.1.0"
 
@@ -33,6 +33,8 @@ __all__ = [
     "alg_flops",
     "build_neighbor_map",
     "default_grid",
+    "pi_tallies",
     "sigma_tallies",
+    "sse_pi",
     "sse_sigma",
 ]

@@ -25,6 +25,8 @@ EXPORTED = (
     "sse_sigma_c128",
     "sse_sigma_c128_slab",
     "sse_sigma_device",
+    "sse_pi_c128",
+    "sse_pi_device",
     "sse_layout_transform",
     "sse_preprocess_D",
     "sse_fill_synthetic",
@@ -32,7 +34,7 @@ EXPORTED = (
     "sse_profile_end",
 )
 
-PROF_KINDS = ("operator", "sigma", "layout", "preprocess")
+PROF_KINDS = ("operator", "sigma", "layout", "preprocess", "pi_build", "pi", "pi_assemble")
 
 
 class SseDims(ctypes.Structure):
@@ -68,9 +70,9 @@ class SseTiming(ctypes.Structure):
 
 class SseProfile(ctypes.Structure):
     _fields_ = [
-        ("ms", ctypes.c_double * 4),
-        ("flops", ctypes.c_double * 4),
-        ("launches", ctypes.c_int64 * 4),
+        ("ms", ctypes.c_double * 7),
+        ("flops", ctypes.c_double * 7),
+        ("launches", ctypes.c_int64 * 7),
     ]
 
     def as_dict(self) -> dict:
@@ -110,6 +112,8 @@ def load() -> ctypes.CDLL:
         lib.sse_version.restype = i32
         lib.sse_sigma_c128.argtypes = [_P, pdims, i32] + [_P] * 7 + [_P, _P, _P, ptim]
         lib.sse_sigma_c128_slab.argtypes = [_P, pdims, i32, pslab, pslab] + [_P] * 7 + [_P, _P, _P, ptim]
+        lib.sse_pi_c128.argtypes = [_P, pdims, _P, _P, _P, _P, _P, dbl, _P, i64, i64, _P, _P, ptim]
+        lib.sse_pi_device.argtypes = [_P, pdims, pslab, pslab, _P, _P, _P, _P, _P, dbl, _P, _P, _P, _P, ptim]
         lib.sse_profile_begin.argtypes = [_P]
         lib.sse_profile_end.argtypes = [_P, ctypes.POINTER(SseProfile)]
         lib.sse_sigma_device.argtypes = [_P, pdims, pslab, pslab] + [_P] * 6 + [_P, _P, _P, _P, _P, ptim]

@@ -20,10 +20,14 @@ from __future__ import annotations
 
 import importlib
 
+from .sse import sse_pi as _b200_sse_pi
 from .sse import sse_sigma as _b200_sse_sigma
 
 _TARGETS = ("negflow.sse", "negflow.distsim", "negflow.cli", "negflow")
-_saved: dict[str, object] = {}
+# sse_pi is bound by name in negflow.sse (self_consistent_loop sse.py:534,
+# count_sse_phase sse.py:450), negflow.cli (cli.py:223) and the package root.
+_PI_TARGETS = ("negflow.sse", "negflow.cli", "negflow")
+_saved: dict[tuple[str, str], object] = {}
 
 
 def make_drop_in(self_energy_cls, **kwargs):
@@ -37,18 +41,38 @@ def make_drop_in(self_energy_cls, **kwargs):
     return sse_sigma
 
 
-def patch_reference(**kwargs) -> None:
-    """Rebind every reference lookup of ``sse_sigma`` to the B200 path."""
+def make_pi_drop_in(self_energy_cls, **kwargs):
+    """sse_pi with the reference signature returning ``self_energy_cls``."""
+
+    def sse_pi(g, dh, nmap, grid, n_qz, counter=None, hoist_invariant=True, point_mask=None, atom_range=None):
+        out = _b200_sse_pi(g, dh, nmap, grid, n_qz, counter=counter, hoist_invariant=hoist_invariant,
+                           point_mask=point_mask, atom_range=atom_range, **kwargs)
+        return self_energy_cls(lesser=out.lesser, greater=out.greater)
+
+    sse_pi.__doc__ = "B200 drop-in for negflow.sse.sse_pi (sse.py:409-428)."
+    return sse_pi
+
+
+def _bind(name: str, attr: str, fn) -> None:
+    mod = importlib.import_module(name)
+    if (name, attr) not in _saved:
+        _saved[(name, attr)] = getattr(mod, attr)
+    setattr(mod, attr, fn)
+
+
+def patch_reference(pi: bool = True, **kwargs) -> None:
+    """Rebind every reference lookup of ``sse_sigma`` (and ``sse_pi``) to the B200 path."""
     gf = importlib.import_module("negflow.gf")
     drop_in = make_drop_in(gf.SelfEnergyTensor, **kwargs)
     for name in _TARGETS:
-        mod = importlib.import_module(name)
-        if name not in _saved:
-            _saved[name] = getattr(mod, "sse_sigma")
-        setattr(mod, "sse_sigma", drop_in)
+        _bind(name, "sse_sigma", drop_in)
+    if pi:
+        pi_drop_in = make_pi_drop_in(gf.SelfEnergyTensor, **kwargs)
+        for name in _PI_TARGETS:
+            _bind(name, "sse_pi", pi_drop_in)
 
 
 def unpatch_reference() -> None:
-    for name, fn in list(_saved.items()):
-        setattr(importlib.import_module(name), "sse_sigma", fn)
-        del _saved[name]
+    for (name, attr), fn in list(_saved.items()):
+        setattr(importlib.import_module(name), attr, fn)
+        del _saved[(name, attr)]

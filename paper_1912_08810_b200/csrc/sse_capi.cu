@@ -94,6 +94,8 @@ struct DevState {
   cudaStream_t stream = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev[6] = {};
   DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev;
+  DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2];
+  std::vector<unsigned char> pi_mask_host;
   // host copies of the small tables last uploaded (skip re-uploads: a pageable
   // upload would otherwise serialise the host with the stream on every call)
   std::vector<int> nbr_host, off_host, pp_nbr_host, pp_rev_host;
@@ -171,7 +173,8 @@ int init_dev(DevState& d, int device) {
 void destroy_dev(DevState& d) {
   cudaSetDevice(d.device);
   for (DevBuf* b : {&d.g[0], &d.g[1], &d.s[0], &d.s[1], &d.dc[0], &d.dc[1], &d.dh, &d.op[0],
-                    &d.op[1], &d.nbr, &d.off, &d.wt, &d.tmp_g, &d.tmp_s, &d.pp_nbr, &d.pp_rev})
+                    &d.op[1], &d.nbr, &d.off, &d.wt, &d.tmp_g, &d.tmp_s, &d.pp_nbr, &d.pp_rev,
+                    &d.pi_vt[0], &d.pi_vt[1], &d.pi_part, &d.pi_mask, &d.pi_out[0], &d.pi_out[1]})
     b->release();
   for (auto& e : d.ev)
     if (e) cudaEventDestroy(e);
@@ -213,6 +216,8 @@ int validate_slab(const sse_dims* d, const sse_slab* s, const char* what) {
                 (long long)(s->atom0 + s->natoms), (long long)d->na);
   return SSE_OK;
 }
+
+constexpr int64_t kPiEnergiesPerChunk = 96;
 
 // Operator chunk: bound the per-polarity operator buffer to ~1 GiB
 // (SSE_OP_CHUNK_ATOMS overrides, for experiments).
@@ -265,10 +270,12 @@ int prepare_tables(DevState& ds, const sse_dims* d, const sse_slab& g, const sse
     }
   std::vector<int> offs(d->nw);
   for (int64_t w = 0; w < d->nw; ++w) offs[w] = (int)off[w];
-  std::vector<double> wts(wt, wt + d->nw);
   CHECK(upload_cached(ds.nbr, ds.nbr_host, nbr, st));
   CHECK(upload_cached(ds.off, ds.off_host, offs, st));
-  CHECK(upload_cached(ds.wt, ds.wt_host, wts, st));
+  if (wt) {
+    std::vector<double> wts(wt, wt + d->nw);
+    CHECK(upload_cached(ds.wt, ds.wt_host, wts, st));
+  }
   return SSE_OK;
 }
 
@@ -346,6 +353,100 @@ int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const ss
   for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk)
     CHECK(run_chunk(ds, d, g, out, p, off, a0, std::min<int64_t>(chunk, out.natoms - a0), st, npol,
                     launches));
+  return SSE_OK;
+}
+
+// Phonon self-energy Pi (sse_pi, sse.py:409-428) for the owned atoms of `out`:
+// K5 operand build (VT) -> K6 DMMA chains (partials per E-chunk) -> K7 assembly,
+// in atom chunks bounded by a ~16 GiB VT scratch.  Pi_* are device
+// [Nqz, Nw, out.natoms, NB+1, 3, 3]; mask: host [Nkz*NE] or NULL.
+int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
+                 const double2* G_l, const double2* G_g, const double2* dH, const int64_t* nmap,
+                 const int64_t* off, double energy_weight, const unsigned char* mask, double2* Pi_l,
+                 double2* Pi_g, cudaStream_t st, int* launches) {
+  CHECK(prepare_tables(ds, d, g, out, nmap, off, nullptr, st));
+  const unsigned char* mask_dev = nullptr;
+  if (mask) {
+    std::vector<unsigned char> m(mask, mask + d->nkz * d->ne);
+    CHECK(upload_cached(ds.pi_mask, ds.pi_mask_host, m, st));
+    mask_dev = ds.pi_mask.as<unsigned char>();
+  }
+  const int no = (int)d->norb, no2 = no * no, nb = (int)d->nb, ncol = nb * 9;
+  const size_t vt_atom = (size_t)d->nkz * d->ne * no2 * ncol * 16;  // per chain polarity
+  int64_t chunk = std::max<int64_t>(1, (int64_t)((8ull << 30) / std::max<size_t>(vt_atom, 1)));
+  chunk = std::min<int64_t>(chunk, out.natoms);
+  const int nqz = (int)d->nqz, nw = (int)d->nw;
+  // E-chunks of a fixed size (independent of the atom partition, so Pi is
+  // bitwise identical for any chunking / device count)
+  const int e_per = (int)std::min<int64_t>(d->ne, kPiEnergiesPerChunk);
+  const int echunks = (int)((d->ne + e_per - 1) / e_per);
+  const int m_tiles = (nw + 7) / 8, n_tiles = (2 * ncol + 7) / 8;
+  const int warp_groups = ((m_tiles + 2) / 3) * ((n_tiles + 2) / 3);
+  CHECK(ds.pi_vt[0].ensure(vt_atom * chunk));
+  CHECK(ds.pi_vt[1].ensure(vt_atom * chunk));
+  CHECK(ds.pi_part.ensure((size_t)chunk * 2 * nqz * echunks * nw * ncol * 16));
+  const SlabStrides gs = strides_of(d, g);
+  for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk) {
+    const int n = (int)std::min<int64_t>(chunk, out.natoms - a0);
+    sse::PiBuildArgs ba{};
+    ba.G[0] = G_l;
+    ba.G[1] = G_g;
+    ba.dH = dH;
+    ba.nbr = ds.nbr.as<int>() + a0 * nb;
+    ba.mask = mask_dev;
+    ba.VT[0] = ds.pi_vt[0].as<double2>();
+    ba.VT[1] = ds.pi_vt[1].as<double2>();
+    ba.nkz = (int)d->nkz;
+    ba.ne = (int)d->ne;
+    ba.nb = nb;
+    ba.no = no;
+    ba.atom_begin = (int)a0;
+    ba.chunk_atoms = n;
+    ba.g_sa = gs.sa;
+    ba.g_sk = gs.sk;
+    ba.g_se = gs.se;
+    CHECK(profiled(ds, st, SSE_PROF_PI_BUILD, 0.0, [&] { return sse::launch_pi_build(ba, st); }));
+    sse::PiArgs pa{};
+    pa.G[0] = G_l;
+    pa.G[1] = G_g;
+    pa.VT[0] = ba.VT[0];
+    pa.VT[1] = ba.VT[1];
+    pa.partial = ds.pi_part.as<double2>();
+    pa.off = ds.off.as<int>();
+    pa.nkz = (int)d->nkz;
+    pa.nqz = nqz;
+    pa.ne = (int)d->ne;
+    pa.nw = nw;
+    pa.nb = nb;
+    pa.no = no;
+    pa.ncol = ncol;
+    pa.echunks = echunks;
+    pa.e_per_chunk = e_per;
+    pa.warp_groups = warp_groups;
+    pa.energy_weight = energy_weight;
+    pa.g_sa = gs.sa;
+    pa.g_sk = gs.sk;
+    pa.g_se = gs.se;
+    pa.g_atom_of_chunk0 = out.atom0 + a0 - g.atom0;
+    double flops = 0;  // 8 per complex MAC, both chain polarities, valid (E + off < NE) terms
+    for (int64_t w = 0; w < d->nw; ++w) flops += (double)std::max<int64_t>(0, d->ne - off[w]);
+    flops *= 16.0 * n * nqz * d->nkz * no2 * ncol;
+    CHECK(profiled(ds, st, SSE_PROF_PI, flops, [&] { return sse::launch_pi(pa, n, st); }));
+    sse::PiAssembleArgs aa{};
+    aa.partial = pa.partial;
+    aa.Pi[0] = Pi_l;
+    aa.Pi[1] = Pi_g;
+    aa.nqz = nqz;
+    aa.nw = nw;
+    aa.nb = nb;
+    aa.ncol = ncol;
+    aa.echunks = echunks;
+    aa.atom_begin = (int)a0;
+    aa.chunk_atoms = n;
+    aa.out_natoms = (int)out.natoms;
+    CHECK(profiled(ds, st, SSE_PROF_PI_ASSEMBLE, 0.0, [&] { return sse::launch_pi_assemble(aa, st); }));
+    if (launches) *launches += 3;
+  }
   return SSE_OK;
 }
 
@@ -664,6 +765,126 @@ int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const s
     CU(cudaEventSynchronize(ds.ev[1]));
     t->sigma_ms = t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
     t->kernel_launches = launches;
+  }
+  return SSE_OK;
+}
+
+int sse_pi_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
+                  const double* G_l, const double* G_g, const double* dH, const int64_t* nmap,
+                  const int64_t* off, double energy_weight, const unsigned char* mask, double* Pi_l,
+                  double* Pi_g, void* stream, sse_timing* t) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
+  CHECK(validate_dims(d));
+  if (!off) return fail(SSE_EINVAL, "frequency map is NULL");
+  for (int64_t w = 0; w < d->nw; ++w)
+    if (off[w] < 0 || off[w] >= d->ne)
+      return fail(SSE_EINVAL, "frequency offset %lld (index %lld) outside [0, %lld)", (long long)off[w],
+                  (long long)w, (long long)d->ne);
+  if (!std::isfinite(energy_weight)) return fail(SSE_EINVAL, "energy weight is not finite");
+  CHECK(validate_slab(d, g, "G"));
+  CHECK(validate_slab(d, out, "output"));
+  if (!G_l || !G_g || !dH || !nmap || !Pi_l || !Pi_g) return fail(SSE_EINVAL, "NULL tensor pointer");
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->n_devices = 1;
+    CU(cudaEventRecord(ds.ev[0], st));
+  }
+  int launches = 0;
+  CHECK(pi_on_device(ds, d, *g, *out, (const double2*)G_l, (const double2*)G_g, (const double2*)dH, nmap,
+                     off, energy_weight, mask, (double2*)Pi_l, (double2*)Pi_g, st, &launches));
+  if (t) {
+    CU(cudaEventRecord(ds.ev[1], st));
+    CU(cudaEventSynchronize(ds.ev[1]));
+    t->sigma_ms = t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
+    t->kernel_launches = launches;
+  }
+  return SSE_OK;
+}
+
+int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double* G_g, const double* dH,
+                const int64_t* nmap, const int64_t* off, double energy_weight, const unsigned char* mask,
+                int64_t atom_lo, int64_t atom_hi, double* Pi_l, double* Pi_g, sse_timing* t) {
+  if (!ctx) return fail(SSE_EINVAL, "context is NULL");
+  CHECK(validate_dims(d));
+  if (atom_lo < 0 || atom_hi > d->na || atom_lo > atom_hi) return fail(SSE_EINVAL, "invalid atom range");
+  if (!G_l || !G_g || !dH || !nmap || !Pi_l || !Pi_g || !off) return fail(SSE_EINVAL, "NULL tensor pointer");
+  if (t) std::memset(t, 0, sizeof(*t));
+  if (atom_lo == atom_hi) return SSE_OK;
+  const int nd = (int)ctx->devs.size();
+  const int64_t span = atom_hi - atom_lo, per = (span + nd - 1) / nd;
+  const size_t blk = (size_t)d->norb * d->norb * 16, rows = (size_t)(d->nkz * d->ne);
+  const size_t dh_atom = (size_t)d->nb * 3 * blk;
+  const size_t pi_row = (size_t)(d->nb + 1) * 9 * 16, pi_rows = (size_t)(d->nqz * d->nw);
+  auto on_device = [&](DevState& ds, int64_t lo, int64_t hi, sse_timing* tt) -> int {
+    const int64_t on = hi - lo;
+    if (on <= 0) return SSE_OK;
+    CU(cudaSetDevice(ds.device));
+    int64_t glo = lo, ghi = hi;
+    for (int64_t i = lo * d->nb; i < hi * d->nb; ++i) {
+      if (nmap[i] < 0 || nmap[i] >= d->na)
+        return fail(SSE_EINVAL, "neighbor index %lld outside [0, %lld)", (long long)nmap[i], (long long)d->na);
+      glo = std::min(glo, nmap[i]);
+      ghi = std::max(ghi, nmap[i] + 1);
+    }
+    const int64_t gn = ghi - glo;
+    cudaStream_t st = ds.stream;
+    for (int p = 0; p < 2; ++p) {
+      CHECK(ds.g[p].ensure(rows * gn * blk));
+      CHECK(ds.pi_out[p].ensure(pi_rows * on * pi_row));
+    }
+    CHECK(ds.dh.ensure(on * dh_atom));
+    CU(cudaEventRecord(ds.ev[0], st));
+    const char* Gh[2] = {(const char*)G_l, (const char*)G_g};
+    for (int p = 0; p < 2; ++p)
+      CU(cudaMemcpy2DAsync(ds.g[p].ptr, gn * blk, Gh[p] + glo * blk, d->na * blk, gn * blk, rows,
+                           cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(ds.dh.ptr, (const char*)dH + lo * dh_atom, on * dh_atom, cudaMemcpyHostToDevice, st));
+    int launches = 0;
+    const sse_slab gs{glo, gn, 0, 0}, os{lo, on, 0, 0};
+    CHECK(pi_on_device(ds, d, gs, os, ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dh.as<double2>(),
+                       nmap + lo * d->nb, off, energy_weight, mask, ds.pi_out[0].as<double2>(),
+                       ds.pi_out[1].as<double2>(), st, &launches));
+    double* Ph[2] = {Pi_l, Pi_g};
+    for (int p = 0; p < 2; ++p)
+      CU(cudaMemcpy2DAsync((char*)Ph[p] + lo * pi_row, d->na * pi_row, ds.pi_out[p].ptr, on * pi_row,
+                           on * pi_row, pi_rows, cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(ds.ev[1], st));
+    CU(cudaEventSynchronize(ds.ev[1]));
+    if (tt) {
+      tt->total_ms = std::max(tt->total_ms, (double)elapsed(ds.ev[0], ds.ev[1]));
+      tt->h2d_bytes += 2 * rows * gn * blk + on * dh_atom;
+      tt->d2h_bytes += 2 * pi_rows * on * pi_row;
+      tt->kernel_launches += launches;
+    }
+    return SSE_OK;
+  };
+  if (nd == 1) return on_device(ctx->devs[0], atom_lo, atom_hi, t);
+  std::vector<int> rcs(nd, SSE_OK);
+  std::vector<sse_timing> ts(nd);
+  std::vector<std::string> errs(nd);
+  std::vector<std::thread> th;
+  for (int i = 0; i < nd; ++i)
+    th.emplace_back([&, i] {
+      std::memset(&ts[i], 0, sizeof(sse_timing));
+      const int64_t lo = atom_lo + std::min<int64_t>(i * per, span), hi = atom_lo + std::min<int64_t>((i + 1) * per, span);
+      rcs[i] = on_device(ctx->devs[i], lo, hi, &ts[i]);
+      if (rcs[i] != SSE_OK) errs[i] = g_last_error;
+    });
+  for (auto& x : th) x.join();
+  for (int i = 0; i < nd; ++i) {
+    if (rcs[i] != SSE_OK) {
+      g_last_error = errs[i];
+      return rcs[i];
+    }
+    if (t) {
+      t->total_ms = std::max(t->total_ms, ts[i].total_ms);
+      t->h2d_bytes += ts[i].h2d_bytes;
+      t->d2h_bytes += ts[i].d2h_bytes;
+      t->kernel_launches += ts[i].kernel_launches;
+    }
   }
   return SSE_OK;
 }

@@ -622,6 +622,248 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 }
 
 // --------------------------------------------------------------------------
+// K5: Pi operand build.  One CTA per (chunk atom, k, group of energies):
+// dH[a] staged in shared memory; per energy U_{s,j} = dH[a,s,j] @ G2_s and
+// VT[(n,p)][(s,i,j)] = (U_{s,j} @ dH[a,s,i])[p][n] (for both chain
+// polarities: chain pol 0 (lesser) uses G2 = G>, pol 1 (greater) G2 = G<).
+// --------------------------------------------------------------------------
+constexpr int kPiBuildEnergies = 4;
+
+__global__ void pi_build_kernel(PiBuildArgs p) {
+  extern __shared__ double2 smem[];
+  const int no = p.no, no2 = no * no, nb = p.nb, ncol = nb * 9;
+  double2* s_dh = smem;                   // [NB][3][no2]
+  double2* s_g2 = s_dh + nb * 3 * no2;    // [NB][no2]
+  double2* s_u = s_g2 + nb * no2;         // [NB][3][no2]
+  const int n_eg = (p.ne + kPiBuildEnergies - 1) / kPiBuildEnergies;
+  int bx = blockIdx.x;
+  const int eg = bx % n_eg;
+  bx /= n_eg;
+  const int k = bx % p.nkz;
+  const int la = bx / p.nkz;
+  const int a_out = p.atom_begin + la;
+  for (int x = threadIdx.x; x < nb * 3 * no2; x += blockDim.x)
+    s_dh[x] = p.dH[(long long)a_out * nb * 3 * no2 + x];
+  for (int pol = 0; pol < 2; ++pol) {
+    const double2* G2 = p.G[1 - pol];
+    for (int e = eg * kPiBuildEnergies; e < min(p.ne, (eg + 1) * kPiBuildEnergies); ++e) {
+      const bool masked = p.mask && !p.mask[k * p.ne + e];
+      __syncthreads();
+      for (int x = threadIdx.x; x < nb * no2; x += blockDim.x) {
+        const int s = x / no2, r = x % no2;
+        const int lb = p.nbr[la * nb + s];
+        s_g2[x] = G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e * p.g_se + r];
+      }
+      __syncthreads();
+      for (int x = threadIdx.x; x < nb * 3 * no2; x += blockDim.x) {  // U_{s,j} = dH_{s,j} @ G2_s
+        const int sj = x / no2, r = x % no2, pr = r / no, n = r % no, s = sj / 3;
+        double re = 0.0, im = 0.0;
+        for (int t = 0; t < no; ++t) {
+          const double2 u = s_dh[sj * no2 + pr * no + t];
+          const double2 v = s_g2[s * no2 + t * no + n];
+          re = fma(u.x, v.x, re);
+          re = fma(-u.y, v.y, re);
+          im = fma(u.x, v.y, im);
+          im = fma(u.y, v.x, im);
+        }
+        s_u[x] = make_double2(re, im);
+      }
+      __syncthreads();
+      double2* out = p.VT[pol] + (((long long)la * p.nkz + k) * p.ne + e) * no2 * ncol;
+      for (int x = threadIdx.x; x < no2 * ncol; x += blockDim.x) {  // x = (n*no + pp)*ncol + c
+        const int c = x % ncol, kap = x / ncol, n = kap / no, pp = kap % no;
+        const int s = c / 9, i = (c / 3) % 3, j = c % 3;
+        double re = 0.0, im = 0.0;
+        if (!masked) {
+          const double2* u = s_u + (s * 3 + j) * no2 + pp * no;   // U_{s,j}[pp][:]
+          const double2* d = s_dh + (s * 3 + i) * no2 + n;         // dH_{s,i}[:][n]
+          for (int t = 0; t < no; ++t) {
+            const double2 uu = u[t], dd = d[t * no];
+            re = fma(uu.x, dd.x, re);
+            re = fma(-uu.y, dd.y, re);
+            im = fma(uu.x, dd.y, im);
+            im = fma(uu.y, dd.x, im);
+          }
+        }
+        out[x] = make_double2(re, im);  // VT[(n,pp)][c] = V_c[pp][n]
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K6: Pi chains on FP64 tensor cores.  CTA = (chunk atom, chain polarity, q,
+// E-chunk); 9 warps, warp w covers a 3x3 block of 8x8 tiles of the
+// [Nw x 2*ncol] real-embedded chain block (rows = frequencies w, columns =
+// (Re, Im) of (s, i, j)); K = (k, E, n, p): A = G1[(k+q)%Nkz, E+off_w, a]
+// (zero when E+off_w >= NE), B = VT[k][E] (real embedding built on the fly
+// from the complex operand).  Register double buffer over the flattened
+// (k, E, kappa-pair) loop.
+// --------------------------------------------------------------------------
+constexpr int kPiWarps = 9;
+
+__global__ void __launch_bounds__(kPiWarps * 32)
+pi_dmma_kernel(PiArgs p, int chunk_atoms) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bx = blockIdx.x;
+  const int ec = bx % p.echunks;
+  bx /= p.echunks;
+  const int q = bx % p.nqz;
+  bx /= p.nqz;
+  const int pol = bx % 2;
+  const int la = bx / 2;
+  const int wg = blockIdx.y * kPiWarps + warp;
+  if (wg >= p.warp_groups) return;
+  const int no2 = p.no * p.no;
+  const int khp = (no2 + 3) / 4;                 // kappa pairs (k-step pairs)
+  const int n_ntile = (2 * p.ncol + 7) / 8;
+  const int gn = (n_ntile + 2) / 3;
+  const int mg = wg / gn, ng = wg % gn;
+  const int pcol = lane & 3;
+
+  const double2* __restrict__ G1 = p.G[pol];
+  const double2* __restrict__ VT = p.VT[pol] + (long long)la * p.nkz * p.ne * no2 * p.ncol;
+  const long long g_atom = (p.g_atom_of_chunk0 + la) * p.g_sa;
+
+  // per-lane rows (frequencies) of the warp's 3 m-tiles, and columns of its 3 n-tiles
+  int off_t[3];
+  bool row_ok[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int w = (mg * 3 + t) * 8 + (lane >> 2);
+    row_ok[t] = w < p.nw;
+    off_t[t] = row_ok[t] ? __ldg(p.off + w) : 0;
+  }
+  int col_c[3];
+  bool col_ok[3], part_im[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int nc = (ng * 3 + u) * 8 + (lane >> 2);
+    col_c[u] = nc >> 1;
+    part_im[u] = nc & 1;
+    col_ok[u] = col_c[u] < p.ncol;
+  }
+  // smallest offset of the warp's rows (for the warp-uniform skip E + off >= NE)
+  int off_min = 1 << 30;
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+    if (row_ok[t]) off_min = min(off_min, off_t[t]);
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
+
+  double acc[3][3][2];
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+#pragma unroll
+    for (int u = 0; u < 3; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+
+  const int e_lo = ec * p.e_per_chunk, e_hi = min(p.ne, e_lo + p.e_per_chunk);
+  // flattened loop over (k, E in [e_lo, min(e_hi, NE - off_min)), kappa pair)
+  const int e_end = min(e_hi, p.ne - off_min);
+  const int ne_c = max(0, e_end - e_lo);
+  const long long n_it = (long long)p.nkz * ne_c * khp;
+
+  struct Ops {
+    double2 a[3];
+    double2 b[3];
+  };
+  auto load = [&](Ops& o, long long it) {
+    const int kq = (int)(it % khp);
+    const long long ke = it / khp;
+    const int e = e_lo + (int)(ke % ne_c);
+    const int k = (int)(ke / ne_c);
+    int kp = (k + q) % p.nkz;
+    const int kap = kq * 4 + pcol;
+    const bool kap_ok = kap < no2;
+    const double2* arow = G1 + g_atom + (long long)kp * p.g_sk + kap;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      o.a[t] = make_double2(0.0, 0.0);
+      if (row_ok[t] && kap_ok && e + off_t[t] < p.ne) o.a[t] = __ldg(arow + (long long)(e + off_t[t]) * p.g_se);
+    }
+    const double2* brow = VT + (((long long)k * p.ne + e) * no2 + kap) * p.ncol;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      o.b[u] = make_double2(0.0, 0.0);
+      if (col_ok[u] && kap_ok) o.b[u] = __ldg(brow + col_c[u]);
+    }
+  };
+  auto compute = [&](const Ops& o) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const double a = h == 0 ? o.a[t].x : o.a[t].y;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          // B'[re-row][2c] = Re V, [re-row][2c+1] = Im V, [im-row][2c] = -Im V, [im-row][2c+1] = Re V
+          const double b = h == 0 ? (part_im[u] ? o.b[u].y : o.b[u].x) : (part_im[u] ? o.b[u].x : -o.b[u].y);
+          dmma884(acc[t][u], a, b);
+        }
+      }
+  };
+  Ops o0, o1;
+  if (n_it > 0) load(o0, 0);
+  for (long long it = 0; it < n_it; it += 2) {
+    if (it + 1 < n_it) load(o1, it + 1);
+    compute(o0);
+    if (it + 1 >= n_it) break;
+    if (it + 2 < n_it) load(o0, it + 2);
+    compute(o1);
+  }
+
+  // partial chains (w_E-scaled) of this E-chunk: lane holds (Re, Im) of
+  // C[row w][col c = 4 ntile + (lane & 3)]
+  double2* part = p.partial + ((((long long)la * 2 + pol) * p.nqz + q) * p.echunks + ec) * p.nw * p.ncol;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int w = (mg * 3 + t) * 8 + (lane >> 2);
+    if (w >= p.nw) continue;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int c = (ng * 3 + u) * 4 + (lane & 3);
+      if (c < p.ncol)
+        part[(long long)w * p.ncol + c] = make_double2(p.energy_weight * acc[t][u][0], p.energy_weight * acc[t][u][1]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K7: Pi assembly (sse.py:393-406): chain = sum of the E-chunk partials in
+// order; Pi[q,w,a,1+s] = i chain_s, Pi[q,w,a,0] = -i sum_s chain_s.
+// --------------------------------------------------------------------------
+__global__ void pi_assemble_kernel(PiAssembleArgs p) {
+  const long long total = (long long)p.chunk_atoms * 2 * p.nqz * p.nw * 9;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const int ij = (int)(x % 9);
+    long long r = x / 9;
+    const int w = (int)(r % p.nw);
+    r /= p.nw;
+    const int q = (int)(r % p.nqz);
+    r /= p.nqz;
+    const int pol = (int)(r % 2);
+    const int la = (int)(r / 2);
+    const double2* part = p.partial + (((long long)la * 2 + pol) * p.nqz + q) * p.echunks * p.nw * p.ncol;
+    double2* out = p.Pi[pol] + (((long long)q * p.nw + w) * p.out_natoms + p.atom_begin + la) * (p.nb + 1) * 9;
+    double sre = 0.0, sim = 0.0;
+    for (int s = 0; s < p.nb; ++s) {
+      const int c = s * 9 + ij;
+      double cre = 0.0, cim = 0.0;
+      for (int ec = 0; ec < p.echunks; ++ec) {
+        const double2 v = part[((long long)ec * p.nw + w) * p.ncol + c];
+        cre += v.x;
+        cim += v.y;
+      }
+      out[(1 + s) * 9 + ij] = make_double2(-cim, cre);  // +i chain
+      sre += cre;
+      sim += cim;
+    }
+    out[ij] = make_double2(sim, -sre);  // -i sum_s chain
+  }
+}
+
+// --------------------------------------------------------------------------
 // K3g: generic Sigma with DFMA (any No).  One thread per output element
 // (k, E, atom, m, n); compact operator M[q,w][p][n]; same (q, s, w) order.
 // --------------------------------------------------------------------------
@@ -840,6 +1082,29 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
     dim3 grid(grid_for(total, 256), a.npol);
     sigma_generic_kernel<<<grid, 256, 0, st>>>(a, chunk_atoms);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)7 * a.nb * a.no * a.no * sizeof(double2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(pi_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPiBuildEnergies - 1) / kPiBuildEnergies);
+  pi_build_kernel<<<(unsigned)blocks, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
+  dim3 grid((unsigned)((long long)chunk_atoms * 2 * a.nqz * a.echunks), (a.warp_groups + kPiWarps - 1) / kPiWarps);
+  pi_dmma_kernel<<<grid, kPiWarps * 32, 0, st>>>(a, chunk_atoms);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pi_assemble(const PiAssembleArgs& a, cudaStream_t st) {
+  const long long total = (long long)a.chunk_atoms * 2 * a.nqz * a.nw * 9;
+  pi_assemble_kernel<<<grid_for(total, 256), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

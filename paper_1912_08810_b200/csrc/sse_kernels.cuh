@@ -61,6 +61,49 @@ struct SigmaArgs {
   int lookahead;          // sliding-window K3 producer lookahead (0 = default)
 };
 
+// Phonon self-energy Pi (sse.py:332-428), chains in the V form
+//   chain[q,w,a,s,i,j] = w_E sum_{k,E} sum_{n,p} G1[(k+q)%Nkz, E+off_w, a][n,p] * V[p,n],
+//   V = dH[a,s,j] @ G2[k,E,f(a,s)] @ dH[a,s,i]      (trace cyclicity of
+//   tr(dH_i G1' dH_j G2), sse.py:365-389); greater chain: G1 = G>, G2 = G<;
+//   lesser chain: G1 = G<, G2 = G> (sse.py:369).
+// K5 pi_build: VT[k][E][(n,p)][(s,i,j)] = V_{s,ij}[p][n] for a chunk of atoms.
+// K6 pi_dmma:  per (atom, chain polarity, q, E-chunk) the [Nw x NB*9] chain
+//              block on FP64 tensor cores (rows = frequencies, K = (E, n, p)),
+//              partial sums per E-chunk to a scratch.
+// K7 pi_assemble: sum the E-chunks in order, Pi[q,w,a,1+s] = i w_E chain,
+//              Pi[q,w,a,0] = -i sum_s w_E chain (sse.py:393-406).
+struct PiBuildArgs {
+  const double2* G[2];        // G slab per polarity (layout by strides)
+  const double2* dH;          // [out atoms][NB][3][No][No]
+  const int* nbr;             // [chunk][NB] G-slab index of f(a,s)
+  const unsigned char* mask;  // [Nkz][NE] point mask or nullptr (sse.py:362-364)
+  double2* VT[2];             // out per CHAIN polarity: [chunk][Nkz][NE][No*No][NB*9]
+  int nkz, ne, nb, no;
+  int atom_begin, chunk_atoms;  // chunk within the output slab (dH rows, nbr rows)
+  long long g_sa, g_sk, g_se;
+};
+struct PiArgs {
+  const double2* G[2];      // G slab per polarity
+  const double2* VT[2];     // per chain polarity, from K5
+  double2* partial;         // [chunk][2][Nqz][echunks][Nw][ncol] (w_E-scaled chains)
+  const int* off;           // [Nw]
+  int nkz, nqz, ne, nw, nb, no, ncol;
+  int echunks, e_per_chunk;
+  int warp_groups;          // ceil(m-tiles/3) * ceil(n-tiles/3)
+  double energy_weight;
+  long long g_sa, g_sk, g_se;
+  long long g_atom_of_chunk0;  // G-slab index of the chunk's first output atom
+};
+struct PiAssembleArgs {
+  const double2* partial;
+  double2* Pi[2];           // [Nqz][Nw][out_natoms][NB+1][3][3] per polarity
+  int nqz, nw, nb, ncol, echunks;
+  int atom_begin, chunk_atoms, out_natoms;
+};
+cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st);
+cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st);
+cudaError_t launch_pi_assemble(const PiAssembleArgs& a, cudaStream_t st);
+
 cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st);
 cudaError_t launch_sigma(const SigmaArgs& a, int chunk_atoms, cudaStream_t st);
 cudaError_t launch_layout_transform(long long nkz, long long ne, long long na, long long blk_vec,

@@ -32,6 +32,9 @@ Array = np.ndarray
 
 __all__ = [
     "sse_sigma",
+    "sse_pi",
+    "pi_tallies",
+    "pi_device",
     "sigma_tallies",
     "sigma_device",
     "layout_transform",
@@ -160,6 +163,84 @@ def sse_sigma(
     return SelfEnergyTensor(lesser=out_l, greater=out_g)
 
 
+def pi_tallies(hoist_invariant: bool, n_kz, n_qz, n_e, n_w, n_atoms, n_b, n_o) -> dict[str, int]:
+    """Complex MAC tallies of the reference Pi kernel (sse.py:353-386), both chains."""
+    per = 2 * n_atoms * n_b * n_kz * n_e * 3 * n_o**3
+    return {"pi.m2": per * (1 if hoist_invariant else n_qz * n_w), "pi.m1": per * n_qz * n_w}
+
+
+def sse_pi(
+    g,
+    dh: Array,
+    nmap,
+    grid,
+    n_qz: int,
+    counter: FlopCounter | None = None,
+    hoist_invariant: bool = True,
+    point_mask: Array | None = None,
+    atom_range: tuple[int, int] | None = None,
+    *,
+    n_gpus: int | None = None,
+    timing: dict | None = None,
+):
+    """Phonon self-energy Pi^{<>} (drop-in for sse.py:409-428) on FP64 tensor cores.
+
+    Same arguments and conventions as the reference: ``point_mask`` restricts
+    the (k, E) reduction and ``atom_range`` the produced atoms (distsim);
+    ``hoist_invariant`` only changes the ``counter`` tallies (the reference's
+    two arrangements are value-identical, test_sse.py:313-318).  Returns the
+    slot-layout tensor [Nqz, Nw, NA, NB+1, 3, 3] (slot 0 = -i sum_s chain,
+    slots 1.. = +i chain, sse.py:393-406).
+    """
+    if g.kind != "electron":
+        raise ValueError("sse_pi expects the electron Green's tensor")
+    g_l, g_g = g.lesser, g.greater
+    n_kz, n_e, n_a, n_o, _ = g_l.shape
+    n_b = nmap.n_B
+    n_w = grid.n_w
+    a_lo, a_hi = atom_range if atom_range is not None else (0, n_a)
+    mask = None
+    if point_mask is not None:
+        mask = np.asarray(point_mask, dtype=bool)
+        if mask.shape != (n_kz, n_e):
+            raise ValueError(f"point mask must have shape ({n_kz}, {n_e})")
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    if n_a != nmap.n_A:
+        raise ValueError(f"electron tensor has {n_a} atoms but the neighbor map has {nmap.n_A}")
+    dh = np.asarray(dh)
+    if dh.shape != (n_a, n_b, 3, n_o, n_o):
+        raise ValueError(f"dH must have shape {(n_a, n_b, 3, n_o, n_o)}, got {dh.shape}")
+    if not 0 <= a_lo <= a_hi <= n_a:
+        raise ValueError(f"atom range {atom_range} outside [0, {n_a}]")
+    if counter is not None:
+        for stage, n in pi_tallies(hoist_invariant, n_kz, n_qz, n_e, n_w, a_hi - a_lo, n_b, n_o).items():
+            counter.stages[stage] = counter.stages.get(stage, 0) + n
+    shape = (n_qz, n_w, n_a, n_b + 1, 3, 3)
+    out_l = np.zeros(shape, dtype=np.complex128)
+    out_g = np.zeros(shape, dtype=np.complex128)
+    from .types import SelfEnergyTensor as _SE
+
+    if out_l.size == 0 or g_l.size == 0 or a_hi == a_lo or n_w == 0:
+        return _SE(lesser=out_l, greater=out_g)
+    idx = np.ascontiguousarray(nmap.idx, dtype=np.int64)
+    if idx.size and (idx.min() < 0 or idx.max() >= n_a):
+        raise ValueError(f"neighbor map entries must lie in [0, {n_a})")
+    offsets = np.array([int(o) for o in grid.offsets], dtype=np.int64)
+    arrays = [_f64(g_l), _f64(g_g), _f64(dh)]
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    tim = _lib.SseTiming()
+    ctx = _lib.context(n_gpus=n_gpus or _default_gpus())
+    rc = _lib.load().sse_pi_c128(
+        ctx.handle, ctypes.byref(dims), *[_ptr(a) for a in arrays], _ptr(idx), _ptr(offsets),
+        float(grid.energy_weight), _ptr(mask) if mask is not None else None, int(a_lo), int(a_hi),
+        _ptr(out_l), _ptr(out_g), ctypes.byref(tim),
+    )
+    _lib.check(rc)
+    if timing is not None:
+        timing.update(tim.as_dict())
+    return _SE(lesser=out_l, greater=out_g)
+
+
 # ---------------------------------------------------------------------------
 # device-resident API (torch CUDA tensors, complex128)
 # ---------------------------------------------------------------------------
@@ -251,6 +332,34 @@ def sigma_device(
     )
     _lib.check(rc)
     return tim.as_dict() if sync_timing else None
+
+
+def pi_device(
+    g_l, g_g, dh, nmap_rows: Array, offsets, energy_weight: float, pi_l, pi_g, *, n_a: int, n_qz: int,
+    g_atom0: int = 0, out_atom0: int = 0, atom_major: bool = False, point_mask=None, stream=None,
+) -> None:
+    """Pi of an owned atom range, all tensors on one GPU (see sse_pi_device in include/sse.h).
+
+    g_*: slab with the owned atoms and their neighbours ([Nkz, NE, gA, No, No]
+    or atom-major); dh [oA, NB, 3, No, No]; pi_* [Nqz, Nw, oA, NB+1, 3, 3].
+    """
+    if atom_major:
+        g_atoms, n_kz, n_e, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
+    else:
+        n_kz, n_e, g_atoms, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
+    o_atoms, n_b = dh.shape[0], dh.shape[1]
+    idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    mask = None if point_mask is None else np.ascontiguousarray(point_mask, dtype=np.uint8)
+    dims = _lib.SseDims(n_kz, n_qz, n_e, len(offs), n_a, n_b, n_o)
+    gs = _lib.SseSlab(g_atom0, g_atoms, int(atom_major), 0)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, int(atom_major), 0)
+    rc = _lib.load().sse_pi_device(
+        _device_ctx(g_l).handle, ctypes.byref(dims), ctypes.byref(gs), ctypes.byref(os_), _dptr(g_l), _dptr(g_g),
+        _dptr(dh), _ptr(idx), _ptr(offs), float(energy_weight), _ptr(mask) if mask is not None else None,
+        _dptr(pi_l), _dptr(pi_g), _stream_ptr(stream), None,
+    )
+    _lib.check(rc)
 
 
 def layout_transform(src, dst, to_atom_major: bool, stream=None) -> None:

@@ -1,0 +1,170 @@
+"""Parity of the CUDA phonon self-energy Pi (K5-K7, through the C ABI).
+
+Reference: negflow.sse.sse_pi (sse.py:409-428), chains sse.py:332-390, slot
+assembly sse.py:393-406.  Golden outputs come from the reference itself
+(tests/golden/make_golden.py); larger shapes and the mask/atom-range options
+are checked against the oracle (pinned to those goldens by tests/test_oracle.py).
+Tolerance: the reference metric <= 1e-10.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import sse_oracle as orc
+from paper_1912_08810_b200 import inputs
+from paper_1912_08810_b200.sse import pi_tallies, sse_pi
+from paper_1912_08810_b200.types import (
+    EnergyGrid,
+    FlopCounter,
+    GreensTensor,
+    NeighborMap,
+    SimParams,
+    build_neighbor_map,
+    default_grid,
+)
+from tests.golden_cases import load_case
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+PI_CASES = ["test_tiny_s3", "test_tiny_s4", "cli_tiny_s1", "cli_small_s2", "general_grid_s8"]
+
+
+def _grid(case):
+    n_e = case.p.n_E
+    return EnergyGrid(
+        values=tuple(np.linspace(-1, 1, n_e)) if n_e > 1 else (0.0,),
+        frequency_map=tuple(zip(case.offsets.tolist(), case.weights.tolist())),
+        energy_weight=case.meta["energy_weight"],
+    )
+
+
+@pytest.mark.parametrize("name", PI_CASES)
+def test_pi_golden_parity(name):
+    c = load_case(name)
+    assert c.inputs_ok
+    counter = FlopCounter()
+    out = sse_pi(GreensTensor(c.g_l, c.g_g), c.dh, NeighborMap(c.idx), _grid(c), c.p.n_qz, counter=counter)
+    dev = orc.parity_dev(out.lesser, out.greater, c.arrays["pi_l"], c.arrays["pi_g"])
+    assert dev <= TOL, (name, dev)
+    p = c.p
+    assert counter.stages == pi_tallies(True, p.n_kz, p.n_qz, p.n_E, p.n_w, p.n_A, p.n_B, p.n_orb)
+
+
+def test_pi_zero_electron_input():
+    """test_sse.py:275-281."""
+    c = load_case("test_tiny_s3")
+    zero = GreensTensor(np.zeros_like(c.g_l), np.zeros_like(c.g_g))
+    out = sse_pi(zero, c.dh, NeighborMap(c.idx), _grid(c), c.p.n_qz)
+    assert np.all(out.lesser == 0) and np.all(out.greater == 0)
+
+
+def test_pi_single_point_signs():
+    """test_sse.py:284-302: one (k, E) point, slot 0 = -i chain, slot 1 = +i chain."""
+    p = SimParams(n_kz=1, n_qz=1, n_E=1, n_w=1, n_A=2, n_B=1, n_orb=1)
+    nmap = build_neighbor_map(2, 1)
+    w_e = 0.21
+    grid = EnergyGrid(values=(0.0,), frequency_map=((0, 1.0),), energy_weight=w_e)
+    rng = np.random.default_rng(10)
+    z = lambda s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
+    g = GreensTensor(z(p.electron_shape), z(p.electron_shape))
+    dh = z((2, 1, 3, 1, 1))
+    out = sse_pi(g, dh, nmap, grid, 1)
+    for a in range(2):
+        b = int(nmap.idx[a, 0])
+        chain = np.array([[w_e * dh[a, 0, i, 0, 0] * g.greater[0, 0, a, 0, 0] * dh[a, 0, j, 0, 0]
+                           * g.lesser[0, 0, b, 0, 0] for j in range(3)] for i in range(3)])
+        assert np.allclose(out.greater[0, 0, a, 0], -1j * chain, atol=1e-14)
+        assert np.allclose(out.greater[0, 0, a, 1], +1j * chain, atol=1e-14)
+
+
+def test_pi_hoisting_is_value_neutral():
+    """test_sse.py:313-318; only the counter tallies differ (sse.py:353-386)."""
+    c = load_case("cli_tiny_s1")
+    args = (GreensTensor(c.g_l, c.g_g), c.dh, NeighborMap(c.idx), _grid(c), c.p.n_qz)
+    c1, c2 = FlopCounter(), FlopCounter()
+    a = sse_pi(*args, counter=c1, hoist_invariant=True)
+    b = sse_pi(*args, counter=c2, hoist_invariant=False)
+    assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+    assert c1.stages["pi.m1"] == c2.stages["pi.m1"]
+    assert c2.stages["pi.m2"] == c1.stages["pi.m2"] * c.p.n_qz * c.p.n_w
+
+
+@pytest.mark.parametrize("n_kz, n_qz, n_e, n_w, n_a, n_b, n_o", [
+    (3, 3, 30, 10, 6, 4, 12),   # the No of the paper configs
+    (2, 2, 17, 5, 5, 4, 10),    # No = 10 (small config), 5 atoms (odd) with NB even
+    (4, 3, 9, 3, 4, 1, 5),      # NB = 1 (XOR partner slot), Nqz < Nkz
+    (1, 1, 12, 11, 3, 2, 4),    # Nw close to NE (most E + off >= NE terms dropped)
+])
+def test_pi_shapes_against_oracle(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o):
+    p = SimParams(n_kz=n_kz, n_qz=n_qz, n_E=n_e, n_w=n_w, n_A=n_a, n_B=n_b, n_orb=n_o)
+    g_l, g_g, _, _, dh = inputs.stream_instance(5, p, dh_scale=0.05)
+    nmap = build_neighbor_map(n_a, n_b)
+    grid = default_grid(p)
+    out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
+    ch_l, ch_g = orc.pi_chains(g_l, g_g, dh, nmap.idx, np.array(grid.offsets), grid.energy_weight, n_qz)
+    ref_l, ref_g = orc.pi_from_chains(ch_l, ch_g)
+    assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL
+
+
+def test_pi_point_mask_and_atom_range():
+    """The distributed schemes' options (sse.py:339-364): a (k, E) mask and an atom range."""
+    p = SimParams(n_kz=2, n_qz=2, n_E=11, n_w=3, n_A=8, n_B=2, n_orb=3)
+    g_l, g_g, _, _, dh = inputs.stream_instance(6, p)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    mask = np.zeros((p.n_kz, p.n_E), dtype=bool)
+    mask[:, 3:8] = True
+    mask[1, 0] = True
+    out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, p.n_qz, point_mask=mask, atom_range=(2, 6))
+    ch_l, ch_g = orc.pi_chains(g_l, g_g, dh, nmap.idx, np.array(grid.offsets), grid.energy_weight, p.n_qz,
+                               point_mask=mask, atom_range=(2, 6))
+    ref_l, ref_g = orc.pi_from_chains(ch_l, ch_g)
+    assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL
+    assert np.all(out.lesser[:, :, :2] == 0) and np.all(out.greater[:, :, 6:] == 0)
+    with pytest.raises(ValueError, match="point mask must have shape"):
+        sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, p.n_qz, point_mask=mask[:, :5])
+
+
+def test_pi_rejects_phonon_tensor():
+    c = load_case("test_tiny_s3")
+    with pytest.raises(ValueError, match="expects the electron Green's tensor"):
+        sse_pi(GreensTensor(c.d_l, c.d_g), c.dh, NeighborMap(c.idx), _grid(c), c.p.n_qz)
+
+
+def test_pi_multi_gpu_bitwise():
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    c = load_case("cli_small_s2")
+    args = (GreensTensor(c.g_l, c.g_g), c.dh, NeighborMap(c.idx), _grid(c), c.p.n_qz)
+    a = sse_pi(*args, n_gpus=1)
+    b = sse_pi(*args, n_gpus=2)
+    assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+
+
+def test_pi_device_api_slab_bitwise():
+    """Owned-range shard with halo (atom-major) equals the host call bitwise."""
+    import torch
+
+    from paper_1912_08810_b200 import sse as dev
+
+    p = SimParams(n_kz=3, n_qz=3, n_E=20, n_w=6, n_A=10, n_B=4, n_orb=12)
+    g_l, g_g, _, _, dh = inputs.stream_instance(8, p, dh_scale=0.05)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    full = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, p.n_qz)
+    lo, hi = 3, 7
+    glo, ghi = int(nmap.idx[lo:hi].min()), int(nmap.idx[lo:hi].max()) + 1
+    glo, ghi = min(glo, lo), max(ghi, hi)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    gl = cu(np.moveaxis(g_l[:, :, glo:ghi], 2, 0))
+    gg = cu(np.moveaxis(g_g[:, :, glo:ghi], 2, 0))
+    shape = (p.n_qz, p.n_w, hi - lo, p.n_B + 1, 3, 3)
+    pl = torch.zeros(shape, dtype=torch.complex128, device="cuda")
+    pg = torch.zeros_like(pl)
+    dev.pi_device(gl, gg, cu(dh[lo:hi]), nmap.idx[lo:hi], grid.offsets, grid.energy_weight, pl, pg,
+                  n_a=p.n_A, n_qz=p.n_qz, g_atom0=glo, out_atom0=lo, atom_major=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(pl.cpu().numpy(), full.lesser[:, :, lo:hi])
+    assert np.array_equal(pg.cpu().numpy(), full.greater[:, :, lo:hi])
