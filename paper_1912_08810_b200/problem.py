@@ -70,6 +70,7 @@ class ShardProblem:
         self.dc = [t.empty((p.n_qz, p.n_w, self.n_owned, p.n_B, 3, 3), **c128) for _ in range(2)]
         self.dh = t.empty((self.n_owned, p.n_B, 3, p.n_orb, p.n_orb), **c128)
         self.sig = [t.zeros((self.n_owned, p.n_kz, p.n_E, p.n_orb, p.n_orb), **c128) for _ in range(2)]
+        self.pi_out = None
         self.tensors_allocated = True
 
     def fill(self, owned_g_only: bool) -> None:
@@ -103,12 +104,26 @@ class ShardProblem:
             out_atom0=self.lo, atom_major=True, stream=stream,
         )
 
-    def step(self, exchange=None, stream=None) -> None:
-        """One SSE evaluation: halo exchange (if any) + preprocess_D + Sigma."""
+    def pi(self, stream=None) -> None:
+        """Phonon self-energy Pi of the owned atoms (sse.py:409-428), [Nqz, Nw, oA, NB+1, 3, 3]."""
+        t, p = self.torch, self.p
+        if self.pi_out is None:
+            shape = (p.n_qz, p.n_w, self.n_owned, p.n_B + 1, 3, 3)
+            self.pi_out = [t.zeros(shape, dtype=t.complex128, device=self.device) for _ in range(2)]
+        dev.pi_device(
+            self.g[0], self.g[1], self.dh, self.idx[self.lo:self.hi], self.offsets, self.grid.energy_weight,
+            self.pi_out[0], self.pi_out[1], n_a=p.n_A, n_qz=p.n_qz, g_atom0=self.glo, out_atom0=self.lo,
+            atom_major=True, stream=stream,
+        )
+
+    def step(self, exchange=None, stream=None, with_pi: bool = False) -> None:
+        """One SSE evaluation: halo exchange (if any) + preprocess_D + Sigma (+ Pi)."""
         if exchange is not None:
             exchange(self)
         self.preprocess(stream)
         self.sigma(stream)
+        if with_pi:
+            self.pi(stream)
 
     def sigma_block(self, pol: int, k: int, e: int, a: int) -> np.ndarray:
         """Sigma[k, e, a] of an owned atom (copied to the host)."""
@@ -119,7 +134,7 @@ class ShardProblem:
         return dev.alg_flops(p.n_kz, p.n_qz, p.n_E, self.n_owned, p.n_B, p.n_orb, self.offsets)
 
     def free(self) -> None:
-        for name in ("g", "d", "dc", "dh", "sig"):
+        for name in ("g", "d", "dc", "dh", "sig", "pi_out"):
             if hasattr(self, name):
                 delattr(self, name)
         self.tensors_allocated = False
