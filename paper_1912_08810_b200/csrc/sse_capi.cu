@@ -373,8 +373,10 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
   }
   const int no = (int)d->norb, no2 = no * no, nb = (int)d->nb, ncol = nb * 9;
   const size_t vt_atom = (size_t)d->nkz * d->ne * no2 * ncol * 16;  // per chain polarity
-  int64_t chunk = std::max<int64_t>(1, (int64_t)((8ull << 30) / std::max<size_t>(vt_atom, 1)));
+  int64_t chunk = std::max<int64_t>(1, (int64_t)((12ull << 30) / std::max<size_t>(vt_atom, 1)));
   chunk = std::min<int64_t>(chunk, out.natoms);
+  const int64_t n_chunks = (out.natoms + chunk - 1) / chunk;
+  chunk = (out.natoms + n_chunks - 1) / n_chunks;  // balanced chunks (no tiny tail launch)
   const int nqz = (int)d->nqz, nw = (int)d->nw;
   // E-chunks of a fixed size (independent of the atom partition, so Pi is
   // bitwise identical for any chunking / device count)

@@ -703,7 +703,7 @@ __global__ void pi_build_kernel(PiBuildArgs p) {
 constexpr int kPiWarps = 9;
 
 __global__ void __launch_bounds__(kPiWarps * 32)
-pi_dmma_kernel(PiArgs p, int chunk_atoms) {
+pi_dmma_direct_kernel(PiArgs p, int chunk_atoms) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx = blockIdx.x;
   const int ec = bx % p.echunks;
@@ -824,6 +824,209 @@ pi_dmma_kernel(PiArgs p, int chunk_atoms) {
       const int c = (ng * 3 + u) * 4 + (lane & 3);
       if (c < p.ncol)
         part[(long long)w * p.ncol + c] = make_double2(p.energy_weight * acc[t][u][0], p.energy_weight * acc[t][u][1]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K6 (TMA): the production Pi kernel.  CTA = (chunk atom, chain polarity,
+// q-block of up to kPiQB momenta, E-chunk); 9 warps, warp = (m-group,
+// n-group) owning 3 x 3 tiles of the chain block for each q of the block.
+// The B operand VT[k][E] (No^2 x ncol complex, contiguous) is staged per
+// (k, E) step by the TMA engine into a 2-slot shared-memory ring (full/empty
+// mbarriers, producer rotated over the warps), read with 16-byte LDS and
+// turned into the real-embedded fragments with selects; A = G1 rows through
+// L1/L2 with a register double buffer over kappa pairs.  Each VT stage feeds
+// all q of the block (one HBM read of VT per (atom, polarity, q-block)).
+// --------------------------------------------------------------------------
+constexpr int kPiQB = 2;
+
+// -x by flipping the sign bit with an integer instruction (the compiler would
+// otherwise emit DADD on the FP64 pipe, which the DMMAs need)
+__device__ __forceinline__ double neg_sign_bit(double x) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  asm volatile("xor.b32 %0, %0, 0x80000000;" : "+r"(hi));
+  double r;
+  asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+constexpr int kPiStages = 2;
+
+__global__ void __launch_bounds__(kPiWarps * 32, 1)
+pi_dmma_kernel(PiArgs p, int chunk_atoms) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int no2 = p.no * p.no, ncol = p.ncol;
+  const int stage_vec = no2 * ncol;
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPiStages * stage_vec);
+  uint64_t* empty = full + kPiStages;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int qblocks = (p.nqz + kPiQB - 1) / kPiQB;
+  int bx = blockIdx.x;
+  const int ec = bx % p.echunks;
+  bx /= p.echunks;
+  const int qb = bx % qblocks;
+  bx /= qblocks;
+  const int pol = bx % 2;
+  const int la = bx / 2;
+  const int q0 = qb * kPiQB, nq = min(kPiQB, p.nqz - q0);
+  const int wg = blockIdx.y * kPiWarps + warp;
+  const bool active = wg < p.warp_groups;  // idle warps still take part in the barriers
+  const int khp = (no2 + 3) / 4;
+  const int n_ntile = (2 * ncol + 7) / 8;
+  const int gn = (n_ntile + 2) / 3;
+  const int mg = active ? wg / gn : 0, ng = active ? wg % gn : 0;
+  const int pcol = lane & 3;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPiStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kPiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const double2* __restrict__ G1 = p.G[pol];
+  const double2* __restrict__ VT = p.VT[pol] + (long long)la * p.nkz * p.ne * stage_vec;
+  const long long g_atom = (p.g_atom_of_chunk0 + la) * p.g_sa;
+
+  int off_t[3];
+  bool row_ok[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int w = (mg * 3 + t) * 8 + (lane >> 2);
+    row_ok[t] = active && w < p.nw;
+    off_t[t] = row_ok[t] ? __ldg(p.off + w) : 0;
+  }
+  int col_c[3];
+  bool col_ok[3], part_im[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int nc = (ng * 3 + u) * 8 + (lane >> 2);
+    col_c[u] = nc >> 1;
+    part_im[u] = nc & 1;
+    col_ok[u] = active && col_c[u] < ncol;
+  }
+  int off_min = 1 << 30;
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+    if (row_ok[t]) off_min = min(off_min, off_t[t]);
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
+
+  double acc[kPiQB][3][3][2];
+#pragma unroll
+  for (int qq = 0; qq < kPiQB; ++qq)
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) acc[qq][t][u][0] = acc[qq][t][u][1] = 0.0;
+
+  const int e_lo = ec * p.e_per_chunk, e_hi = min(p.ne, e_lo + p.e_per_chunk);
+  const int ne_c = e_hi - e_lo;
+  const int n_st = p.nkz * ne_c;  // (k, E) stages
+  const long long n_it = (long long)n_st * khp;
+
+  auto produce = [&](int st) {  // lane 0 of warp st % kPiWarps
+    const int slot = st % kPiStages;
+    if (st >= kPiStages) mbar_wait(empty + slot, (uint32_t)(((st - kPiStages) / kPiStages) & 1));
+    const int k = st / ne_c, e = e_lo + st % ne_c;
+    mbar_arrive_expect_tx(full + slot, (uint32_t)stage_vec * 16);
+    bulk_g2s(ring + slot * stage_vec, VT + ((long long)k * p.ne + e) * stage_vec, (uint32_t)stage_vec * 16,
+             full + slot);
+  };
+  struct OpsA {
+    double2 a[kPiQB][3];
+  };
+  auto load_a = [&](OpsA& o, long long it) {
+    const int kq = (int)(it % khp);
+    const int st = (int)(it / khp);
+    const int k = st / ne_c, e = e_lo + st % ne_c;
+    const int kap = kq * 4 + pcol;
+    const bool kap_ok = kap < no2;
+#pragma unroll
+    for (int qq = 0; qq < kPiQB; ++qq) {
+      const int kp = (k + q0 + qq) % p.nkz;
+      const double2* arow = G1 + g_atom + (long long)kp * p.g_sk + kap;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        o.a[qq][t] = make_double2(0.0, 0.0);
+        if (qq < nq && row_ok[t] && kap_ok && e + off_t[t] < p.ne)
+          o.a[qq][t] = __ldg(arow + (long long)(e + off_t[t]) * p.g_se);
+      }
+    }
+  };
+  auto step = [&](const OpsA& o, long long it) {
+    const int kq = (int)(it % khp);
+    const int st = (int)(it / khp);
+    const int e = e_lo + st % ne_c;
+    if (kq == 0) {
+      if (lane == 0 && st + 1 < n_st && (st + 1) % kPiWarps == warp) produce(st + 1);
+      mbar_wait(full + st % kPiStages, (uint32_t)((st / kPiStages) & 1));
+    }
+    if (active && e + off_min < p.ne) {
+      const int kap = kq * 4 + pcol;
+      const double2* sb = ring + (st % kPiStages) * stage_vec + (long long)kap * ncol;
+      // real-embedded B fragments of the two k-steps of this kappa pair:
+      // re-row: (Re V, Im V) by column parity, im-row: (-Im V, Re V); the
+      // negation flips the sign bit on the integer pipe (no FP64-pipe op)
+      double b_re[3], b_im[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const double2 v = (col_ok[u] && kap < no2) ? sb[col_c[u]] : make_double2(0.0, 0.0);
+        const double neg_im = neg_sign_bit(v.y);
+        b_re[u] = part_im[u] ? v.y : v.x;
+        b_im[u] = part_im[u] ? v.x : neg_im;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int qq = 0; qq < kPiQB; ++qq) {
+          if (qq >= nq) continue;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const double a = h == 0 ? o.a[qq][t].x : o.a[qq][t].y;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) dmma884(acc[qq][t][u], a, h == 0 ? b_re[u] : b_im[u]);
+          }
+        }
+    }
+    if (kq == khp - 1) {  // done with this stage's shared memory
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st % kPiStages);
+    }
+  };
+
+  if (threadIdx.x == 0 && n_st > 0) produce(0);
+  OpsA o0, o1;
+  if (n_it > 0) load_a(o0, 0);
+  for (long long it = 0; it < n_it; it += 2) {
+    if (it + 1 < n_it) load_a(o1, it + 1);
+    step(o0, it);
+    if (it + 1 >= n_it) break;
+    if (it + 2 < n_it) load_a(o0, it + 2);
+    step(o1, it + 1);
+  }
+
+  if (!active) return;
+#pragma unroll
+  for (int qq = 0; qq < kPiQB; ++qq) {
+    if (qq >= nq) continue;
+    double2* part =
+        p.partial + ((((long long)la * 2 + pol) * p.nqz + q0 + qq) * p.echunks + ec) * p.nw * ncol;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int w = (mg * 3 + t) * 8 + (lane >> 2);
+      if (w >= p.nw) continue;
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int c = (ng * 3 + u) * 4 + (lane & 3);
+        if (c < ncol)
+          part[(long long)w * ncol + c] =
+              make_double2(p.energy_weight * acc[qq][t][u][0], p.energy_weight * acc[qq][t][u][1]);
+      }
     }
   }
 }
@@ -1097,8 +1300,21 @@ cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
-  dim3 grid((unsigned)((long long)chunk_atoms * 2 * a.nqz * a.echunks), (a.warp_groups + kPiWarps - 1) / kPiWarps);
-  pi_dmma_kernel<<<grid, kPiWarps * 32, 0, st>>>(a, chunk_atoms);
+  const size_t stage_bytes = (size_t)a.no * a.no * a.ncol * 16;
+  const size_t smem = kPiStages * stage_bytes + 2 * kPiStages * 8;
+  const char* env = getenv("SSE_PI_KERNEL");
+  const bool direct = (env && env[0] == '0') || smem > 220 * 1024;
+  const unsigned gy = (unsigned)((a.warp_groups + kPiWarps - 1) / kPiWarps);
+  if (direct) {
+    dim3 grid((unsigned)((long long)chunk_atoms * 2 * a.nqz * a.echunks), gy);
+    pi_dmma_direct_kernel<<<grid, kPiWarps * 32, 0, st>>>(a, chunk_atoms);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(pi_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int qblocks = (a.nqz + kPiQB - 1) / kPiQB;
+    dim3 grid((unsigned)((long long)chunk_atoms * 2 * qblocks * a.echunks), gy);
+    pi_dmma_kernel<<<grid, kPiWarps * 32, smem, st>>>(a, chunk_atoms);
+  }
   return cudaGetLastError();
 }
 
