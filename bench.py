@@ -369,6 +369,34 @@ def run_gpu(args, p, grid, idx) -> None:
                     worst = max(worst, float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)))
         check = worst
 
+    # Pi (the other half of the SSE phase, sse.py:534) on the same resident G
+    pi_info = None
+    if args.pi_steps > 0:
+        prob.pi()
+        torch.cuda.synchronize()
+        barrier(world)
+        with Profile(device=local_rank) as pprof:
+            start.record(stream)
+            for _ in range(args.pi_steps):
+                prob.pi()
+            end.record(stream)
+            torch.cuda.synchronize()
+        pi_ms = allreduce_max(start.elapsed_time(end) / args.pi_steps, world)
+        k6 = pprof.result["pi"]
+        k6_tflops = allreduce_sum(k6["flops"] / (k6["ms"] * 1e-3) / 1e12 if k6["ms"] > 0 else 0.0, world) / world
+        terms = sum(max(0, p.n_E - int(o)) for o in grid.offsets)
+        pi_flops = 16 * p.n_A * p.n_B * p.n_qz * p.n_kz * 9 * p.n_orb**2 * terms
+        pi_info = {
+            "s_per_eval": pi_ms / 1e3, "steps": args.pi_steps, "tflops": pi_flops / (pi_ms * 1e-3) / 1e12,
+            "flops_alg": pi_flops,
+            "roofline": {"bound": "tensor", "kernel": "pi_dmma_kernel (K6, TMA-staged V operand)",
+                         "achieved": k6_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": k6_tflops / FP64_PEAK_TFLOPS},
+            "kernels": {k: pprof.result[k] for k in ("pi_build", "pi", "pi_assemble")},
+            "note": "phonon self-energy Pi (sse_pi) per Born iteration, V form: chain = w_E sum <G1(E+off)^T, "
+                    "dH_j G2 dH_i>; not part of `value` (north_star's path is Sigma)",
+        }
+
     prob.free()
     del prob
     torch.cuda.synchronize()
@@ -420,6 +448,8 @@ def run_gpu(args, p, grid, idx) -> None:
                             "bytes_per_step": sdist.halo_bytes(plan, p.n_kz * p.n_E * p.n_orb**2 * 16)}
         if check is not None:
             line["parity_check_max_rel_dev"] = check
+        if pi_info is not None:
+            line["pi"] = pi_info
         if e2e is not None:
             line["e2e"] = e2e
         if cpu is not None:
@@ -444,6 +474,7 @@ def main():
     ap.add_argument("--cpu-pairs", type=int, default=2, help="pairs timed for cpu_baseline (0 = skip)")
     ap.add_argument("--ref-pairs", type=int, default=1, help="pairs per step of --impl reference")
     ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--pi-steps", type=int, default=1, help="timed Pi evaluations after Sigma (0 = skip)")
     args = ap.parse_args()
 
     from paper_1912_08810_b200.inputs import config

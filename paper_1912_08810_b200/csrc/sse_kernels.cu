@@ -627,65 +627,85 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 // VT[(n,p)][(s,i,j)] = (U_{s,j} @ dH[a,s,i])[p][n] (for both chain
 // polarities: chain pol 0 (lesser) uses G2 = G>, pol 1 (greater) G2 = G<).
 // --------------------------------------------------------------------------
-constexpr int kPiBuildEnergies = 4;
+constexpr int kPiBuildEnergies = 8;   // energies per CTA (looped in groups that fit the block)
+constexpr int kPiBuildThreads = 288;
+constexpr int kPiMaxNo = 16;
 
-__global__ void pi_build_kernel(PiBuildArgs p) {
+// Thread (s, j, pp) of an energy keeps the row U_{s,j}[pp][:] = (dH_{s,j} @ G2_s)[pp][:]
+// in registers and emits VT[(n,pp)][(s,i,j)] = (U_{s,j} @ dH_{s,i})[pp][n] for
+// all i, n; dH and G2 are read from shared memory (warp-broadcast rows).
+__global__ void __launch_bounds__(kPiBuildThreads)
+pi_build_kernel(PiBuildArgs p) {
   extern __shared__ double2 smem[];
   const int no = p.no, no2 = no * no, nb = p.nb, ncol = nb * 9;
-  double2* s_dh = smem;                   // [NB][3][no2]
-  double2* s_g2 = s_dh + nb * 3 * no2;    // [NB][no2]
-  double2* s_u = s_g2 + nb * no2;         // [NB][3][no2]
-  const int n_eg = (p.ne + kPiBuildEnergies - 1) / kPiBuildEnergies;
+  const int tpe = nb * 3 * no;                       // threads per energy
+  const int epg = tpe >= kPiBuildThreads ? 1 : kPiBuildThreads / tpe;  // energies per pass
+  double2* s_dh = smem;                              // [NB][3][no2]
+  double2* s_g2 = s_dh + nb * 3 * no2;               // [epg][NB][no2]
+  const int n_eb = (p.ne + kPiBuildEnergies - 1) / kPiBuildEnergies;
   int bx = blockIdx.x;
-  const int eg = bx % n_eg;
-  bx /= n_eg;
+  const int eb = bx % n_eb;
+  bx /= n_eb;
   const int k = bx % p.nkz;
   const int la = bx / p.nkz;
   const int a_out = p.atom_begin + la;
   for (int x = threadIdx.x; x < nb * 3 * no2; x += blockDim.x)
     s_dh[x] = p.dH[(long long)a_out * nb * 3 * no2 + x];
+  const int e_begin = eb * kPiBuildEnergies, e_end = min(p.ne, e_begin + kPiBuildEnergies);
   for (int pol = 0; pol < 2; ++pol) {
     const double2* G2 = p.G[1 - pol];
-    for (int e = eg * kPiBuildEnergies; e < min(p.ne, (eg + 1) * kPiBuildEnergies); ++e) {
+    for (int e0 = e_begin; e0 < e_end; e0 += epg) {
+      __syncthreads();
+      for (int x = threadIdx.x; x < epg * nb * no2; x += blockDim.x) {
+        const int sl = x / (nb * no2), y = x % (nb * no2), ss = y / no2, rr = y % no2;
+        const int e = e0 + sl;
+        if (e < e_end) {
+          const int lb = p.nbr[la * nb + ss];
+          s_g2[x] = G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e * p.g_se + rr];
+        }
+      }
+      __syncthreads();
+      for (int x = threadIdx.x; x < epg * tpe; x += blockDim.x) {
+      const int slot = x / tpe, r = x % tpe;
+      const int s = r / (3 * no), j = (r / no) % 3, pp = r % no;
+      const int e = e0 + slot;
+      if (e >= e_end) continue;
       const bool masked = p.mask && !p.mask[k * p.ne + e];
-      __syncthreads();
-      for (int x = threadIdx.x; x < nb * no2; x += blockDim.x) {
-        const int s = x / no2, r = x % no2;
-        const int lb = p.nbr[la * nb + s];
-        s_g2[x] = G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e * p.g_se + r];
-      }
-      __syncthreads();
-      for (int x = threadIdx.x; x < nb * 3 * no2; x += blockDim.x) {  // U_{s,j} = dH_{s,j} @ G2_s
-        const int sj = x / no2, r = x % no2, pr = r / no, n = r % no, s = sj / 3;
+      double2 u[kPiMaxNo];
+      const double2* g2 = s_g2 + (slot * nb + s) * no2;
+      const double2* dj = s_dh + (s * 3 + j) * no2 + pp * no;  // dH_{s,j}[pp][:]
+#pragma unroll
+      for (int t = 0; t < kPiMaxNo; ++t) {
         double re = 0.0, im = 0.0;
-        for (int t = 0; t < no; ++t) {
-          const double2 u = s_dh[sj * no2 + pr * no + t];
-          const double2 v = s_g2[s * no2 + t * no + n];
-          re = fma(u.x, v.x, re);
-          re = fma(-u.y, v.y, re);
-          im = fma(u.x, v.y, im);
-          im = fma(u.y, v.x, im);
-        }
-        s_u[x] = make_double2(re, im);
-      }
-      __syncthreads();
-      double2* out = p.VT[pol] + (((long long)la * p.nkz + k) * p.ne + e) * no2 * ncol;
-      for (int x = threadIdx.x; x < no2 * ncol; x += blockDim.x) {  // x = (n*no + pp)*ncol + c
-        const int c = x % ncol, kap = x / ncol, n = kap / no, pp = kap % no;
-        const int s = c / 9, i = (c / 3) % 3, j = c % 3;
-        double re = 0.0, im = 0.0;
-        if (!masked) {
-          const double2* u = s_u + (s * 3 + j) * no2 + pp * no;   // U_{s,j}[pp][:]
-          const double2* d = s_dh + (s * 3 + i) * no2 + n;         // dH_{s,i}[:][n]
-          for (int t = 0; t < no; ++t) {
-            const double2 uu = u[t], dd = d[t * no];
-            re = fma(uu.x, dd.x, re);
-            re = fma(-uu.y, dd.y, re);
-            im = fma(uu.x, dd.y, im);
-            im = fma(uu.y, dd.x, im);
+        if (t < no)
+          for (int rr = 0; rr < no; ++rr) {
+            const double2 a = dj[rr], b = g2[rr * no + t];
+            re = fma(a.x, b.x, re);
+            re = fma(-a.y, b.y, re);
+            im = fma(a.x, b.y, im);
+            im = fma(a.y, b.x, im);
           }
+        u[t] = make_double2(re, im);
+      }
+      double2* out = p.VT[pol] + (((long long)la * p.nkz + k) * p.ne + e) * no2 * ncol;
+      for (int i = 0; i < 3; ++i) {
+        const double2* di = s_dh + (s * 3 + i) * no2;  // dH_{s,i}
+        const int c = s * 9 + i * 3 + j;
+        for (int n = 0; n < no; ++n) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int t = 0; t < kPiMaxNo; ++t) {
+            if (t < no) {
+              const double2 b = di[t * no + n];
+              re = fma(u[t].x, b.x, re);
+              re = fma(-u[t].y, b.y, re);
+              im = fma(u[t].x, b.y, im);
+              im = fma(u[t].y, b.x, im);
+            }
+          }
+          out[(long long)(n * no + pp) * ncol + c] = masked ? make_double2(0.0, 0.0) : make_double2(re, im);
         }
-        out[x] = make_double2(re, im);  // VT[(n,pp)][c] = V_c[pp][n]
+      }
       }
     }
   }
@@ -1289,13 +1309,16 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
 }
 
 cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)7 * a.nb * a.no * a.no * sizeof(double2);
+  if (a.no > kPiMaxNo) return cudaErrorInvalidValue;
+  const int tpe = a.nb * 3 * a.no;
+  const int epg = tpe >= kPiBuildThreads ? 1 : kPiBuildThreads / tpe;
+  const size_t smem = (size_t)(3 + epg) * a.nb * a.no * a.no * sizeof(double2);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(pi_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPiBuildEnergies - 1) / kPiBuildEnergies);
-  pi_build_kernel<<<(unsigned)blocks, 256, smem, st>>>(a);
+  pi_build_kernel<<<(unsigned)blocks, kPiBuildThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
