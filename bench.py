@@ -397,6 +397,51 @@ def run_gpu(args, p, grid, idx) -> None:
                     "dH_j G2 dH_i>; not part of `value` (north_star's path is Sigma)",
         }
 
+    # the step as it follows a distributed GF phase: G arrives in the GF
+    # (k, E)-point layout, one NCCL all-to-all builds the atom slabs (halo included),
+    # Sigma returns to the point owners with a second all-to-all
+    gf_info = None
+    if args.gf_layout_steps > 0 and world > 1:
+        import torch.distributed as dist
+
+        # the GF phase's layout of the same G: rank r holds every atom of its (k, E) points;
+        # built from the owned atoms with the return collective itself
+        g_pts = [sdist.atom_slab_to_points(prob.g[pol][prob.lo - prob.glo:prob.hi - prob.glo], idx, p.n_kz, p.n_E)
+                 for pol in range(2)]
+        def digest(ts):  # bit-pattern checksum (int64 wrap-around sum): equal inputs <=> equal digests
+            return [int(torch.view_as_real(t).view(torch.int64).sum()) for t in ts]
+
+        want = digest(prob.g)
+
+        def gf_step():
+            for pol in range(2):
+                prob.g[pol].copy_(sdist.points_to_atom_slab(g_pts[pol], idx, p.n_kz, p.n_E))
+            prob.preprocess()
+            prob.sigma()
+            return [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
+
+        gf_step()
+        torch.cuda.synchronize()
+        same = float(digest(prob.g) == want)
+        same = -allreduce_max(-same, world)  # min over ranks
+        barrier(world)
+        start.record(stream)
+        for _ in range(args.gf_layout_steps):
+            gf_step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        gf_ms = allreduce_max(start.elapsed_time(end) / args.gf_layout_steps, world)
+        blk = p.n_orb * p.n_orb * 16
+        pts_r = p.n_kz * p.n_E / world
+        gf_info = {"s_per_step": gf_ms / 1e3, "steps": args.gf_layout_steps,
+                   "vs_halo_step": gf_ms / step_ms,
+                   "slab_digest_equal_to_halo_exchange": bool(same == 1.0),
+                   "a2a_bytes_per_rank_approx": int(2 * pts_r * (prob.n_slab + p.n_A) * blk),
+                   "note": "G from the GF (k,E)-point layout -> atom slabs (NCCL all_to_all_single, halo "
+                           "included) + preprocess_D + K2 + K3 + Sigma back to points (all_to_all_single)"}
+        del g_pts
+        torch.cuda.empty_cache()
+
     prob.free()
     del prob
     torch.cuda.synchronize()
@@ -450,6 +495,8 @@ def run_gpu(args, p, grid, idx) -> None:
             line["parity_check_max_rel_dev"] = check
         if pi_info is not None:
             line["pi"] = pi_info
+        if gf_info is not None:
+            line["gf_layout"] = gf_info
         if e2e is not None:
             line["e2e"] = e2e
         if cpu is not None:
@@ -475,6 +522,8 @@ def main():
     ap.add_argument("--ref-pairs", type=int, default=1, help="pairs per step of --impl reference")
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--pi-steps", type=int, default=1, help="timed Pi evaluations after Sigma (0 = skip)")
+    ap.add_argument("--gf-layout-steps", type=int, default=0,
+                    help="N>1: timed steps starting from the GF (k,E)-point layout (two all-to-alls)")
     args = ap.parse_args()
 
     from paper_1912_08810_b200.inputs import config

@@ -111,3 +111,101 @@ def exchange_halos(slabs, plan: HaloPlan, group=None) -> None:
 
 def halo_bytes(plan: HaloPlan, bytes_per_atom: int, polarities: int = 2) -> int:
     return polarities * plan.halo_atoms() * bytes_per_atom
+
+
+# ---------------------------------------------------------------------------
+# GF-phase layout <-> SSE atom slabs
+#
+# The GF phase owns flattened (k, E) points in contiguous chunks
+# (distsim._PointLayout, distsim.py:130-150): rank r holds G[points_r, all
+# atoms].  The SSE phase needs atom slabs (owned atoms + halo) over all points.
+# One all-to-all moves each rank's point rows of every destination's slab
+# (halo included: no separate halo round), and one all-to-all returns Sigma to
+# the point owners: the tiled scheme's two rounds (distsim.py:300-315) with
+# T_E = 1, on NCCL.
+# ---------------------------------------------------------------------------
+
+
+def point_chunks(n_kz: int, n_e: int, world: int) -> list[tuple[int, int]]:
+    """Flattened (k, E) ownership of the GF phase (distsim.py:117-120,130-150)."""
+    return [chunk(n_kz * n_e, world, r) for r in range(world)]
+
+
+def _slabs(idx: np.ndarray, world: int):
+    out = []
+    n_a = idx.shape[0]
+    for r in range(world):
+        lo, hi = chunk(n_a, world, r)
+        glo, ghi = slab_range(idx, lo, hi) if hi > lo else (lo, hi)
+        out.append((lo, hi, glo, ghi))
+    return out
+
+
+def points_to_atom_slab(g_pts, idx: np.ndarray, n_kz: int, n_e: int, group=None):
+    """[pts_r, NA, No, No] (this rank's GF points) -> atom-major slab [gA, Nkz, NE, No, No].
+
+    Collective over the group; every rank passes its own point rows.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pts = point_chunks(n_kz, n_e, world)
+    slabs = _slabs(idx, world)
+    no2 = g_pts.shape[-1] * g_pts.shape[-2]
+    flat = g_pts.reshape(g_pts.shape[0], g_pts.shape[1], no2)
+    send = torch.cat([flat[:, glo:ghi].reshape(-1) for (_, _, glo, ghi) in slabs]) if flat.numel() else \
+        flat.new_zeros(0)
+    send_sizes = [flat.shape[0] * (ghi - glo) * no2 for (_, _, glo, ghi) in slabs]
+    lo, hi, glo, ghi = slabs[rank]
+    gA = ghi - glo
+    recv_sizes = [(pe - ps) * gA * no2 for (ps, pe) in pts]
+    recv = flat.new_empty(sum(recv_sizes))
+    _all_to_all(recv, send, recv_sizes, send_sizes, group)
+    slab = flat.new_empty((gA, n_kz * n_e, no2))
+    pos = 0
+    for (ps, pe), sz in zip(pts, recv_sizes):
+        if pe > ps:
+            slab[:, ps:pe] = recv[pos:pos + sz].view(pe - ps, gA, no2).transpose(0, 1)
+        pos += sz
+    n_o = g_pts.shape[-1]
+    return slab.view(gA, n_kz, n_e, n_o, n_o)
+
+
+def atom_slab_to_points(sig, idx: np.ndarray, n_kz: int, n_e: int, group=None):
+    """Owned-atom Sigma [oA, Nkz, NE, No, No] -> this rank's GF points [pts_r, NA, No, No]."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pts = point_chunks(n_kz, n_e, world)
+    slabs = _slabs(idx, world)
+    n_a = idx.shape[0]
+    oA, n_o = sig.shape[0], sig.shape[-1]
+    no2 = n_o * n_o
+    flat = sig.reshape(oA, n_kz * n_e, no2)
+    import torch
+
+    send = torch.cat([flat[:, ps:pe].transpose(0, 1).reshape(-1) for (ps, pe) in pts])
+    send_sizes = [(pe - ps) * oA * no2 for (ps, pe) in pts]
+    ps, pe = pts[rank]
+    recv_sizes = [(pe - ps) * (hi - lo) * no2 for (lo, hi, _, _) in slabs]
+    recv = flat.new_empty(sum(recv_sizes))
+    _all_to_all(recv, send, recv_sizes, send_sizes, group)
+    out = flat.new_empty((pe - ps, n_a, no2))
+    pos = 0
+    for (lo, hi, _, _), sz in zip(slabs, recv_sizes):
+        if hi > lo:
+            out[:, lo:hi] = recv[pos:pos + sz].view(pe - ps, hi - lo, no2)
+        pos += sz
+    return out.view(pe - ps, n_a, n_o, n_o)
+
+
+def _all_to_all(recv, send, recv_sizes, send_sizes, group):
+    """all_to_all_single on complex tensors (NCCL/gloo see their real view)."""
+    import torch
+    import torch.distributed as dist
+
+    r = torch.view_as_real(recv).reshape(-1) if recv.is_complex() else recv
+    s = torch.view_as_real(send).reshape(-1) if send.is_complex() else send
+    f = 2 if recv.is_complex() else 1
+    dist.all_to_all_single(r, s, [x * f for x in recv_sizes], [x * f for x in send_sizes], group=group)

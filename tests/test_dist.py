@@ -131,3 +131,47 @@ def test_two_rank_gloo_sharded_sigma_matches_single_process():
     assert [(x[0], x[1]) for x in parts] == [(0, 5), (5, 9)]
     # identical per-atom arithmetic on identical inputs: bitwise
     assert np.array_equal(got_l, ref_l) and np.array_equal(got_g, ref_g)
+
+
+def _a2a_worker(rank, world, port, p, seed, result_q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    idx = build_neighbor_map(p.n_A, p.n_B).idx
+    full = inputs.atom_keyed_electron(seed, inputs.G_LESSER, p, np.arange(p.n_A))  # [Nkz, NE, NA, No, No]
+    flat = full.reshape(p.n_kz * p.n_E, p.n_A, p.n_orb, p.n_orb)
+    ps, pe = sdist.point_chunks(p.n_kz, p.n_E, world)[rank]
+    g_pts = torch.from_numpy(np.ascontiguousarray(flat[ps:pe]))
+    slab = sdist.points_to_atom_slab(g_pts, idx, p.n_kz, p.n_E)
+    plan = sdist.halo_plan(idx, world, rank)
+    want = np.moveaxis(full[:, :, plan.glo:plan.ghi], 2, 0)
+    ok_fwd = np.array_equal(slab.numpy(), want)
+    own = slab[plan.lo - plan.glo:plan.hi - plan.glo] * 2  # stand-in for this rank's Sigma
+    back = sdist.atom_slab_to_points(own.contiguous(), idx, p.n_kz, p.n_E)
+    ok_back = np.array_equal(back.numpy(), 2 * flat[ps:pe])
+    res = [None] * world
+    dist.all_gather_object(res, (ok_fwd, ok_back))
+    if rank == 0:
+        result_q.put(res)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gf_points_to_atom_slabs_all_to_all(world):
+    """GF (k, E)-point layout -> atom slabs with halos -> Sigma back, one all-to-all each."""
+    import multiprocessing as mp
+
+    p = SimParams(n_kz=2, n_qz=2, n_E=7, n_w=2, n_A=10, n_B=4, n_orb=2)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, p, 4, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(f and b for f, b in res), res
