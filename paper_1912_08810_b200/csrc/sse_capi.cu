@@ -407,6 +407,7 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
     ba.g_sa = gs.sa;
     ba.g_sk = gs.sk;
     ba.g_se = gs.se;
+    ba.swz = sse::pi_vt_swizzle(no, ncol);
     CHECK(profiled(ds, st, SSE_PROF_PI_BUILD, 0.0, [&] { return sse::launch_pi_build(ba, st); }));
     sse::PiArgs pa{};
     pa.G[0] = G_l;
@@ -430,6 +431,7 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
     pa.g_sk = gs.sk;
     pa.g_se = gs.se;
     pa.g_atom_of_chunk0 = out.atom0 + a0 - g.atom0;
+    pa.swz = ba.swz;
     double flops = 0;  // 8 per complex MAC, both chain polarities, valid (E + off < NE) terms
     for (int64_t w = 0; w < d->nw; ++w) flops += (double)std::max<int64_t>(0, d->ne - off[w]);
     flops *= 16.0 * n * nqz * d->nkz * no2 * ncol;

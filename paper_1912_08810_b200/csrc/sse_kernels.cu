@@ -151,6 +151,14 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// same without `volatile`: lets the scheduler interleave the shared-memory
+// operand loads with the DMMAs (the per-accumulator order is data-dependent)
+__device__ __forceinline__ void dmma884_nv(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
 template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32)
 sigma_dmma_kernel(SigmaArgs p) {
@@ -703,7 +711,9 @@ pi_build_kernel(PiBuildArgs p) {
               im = fma(u[t].y, b.x, im);
             }
           }
-          out[(long long)(n * no + pp) * ncol + c] = masked ? make_double2(0.0, 0.0) : make_double2(re, im);
+          const int kap = n * no + pp;
+          out[(long long)kap * ncol + (c ^ (((kap >> 1) & 1) ? p.swz : 0))] =
+              masked ? make_double2(0.0, 0.0) : make_double2(re, im);
         }
       }
       }
@@ -1052,6 +1062,408 @@ pi_dmma_kernel(PiArgs p, int chunk_atoms) {
 }
 
 // --------------------------------------------------------------------------
+// K6 v2 (TMA, half stages, two CTAs per SM): the production Pi kernel.
+// CTA = (chunk atom, chain polarity, E-chunk, q) with q fastest, so the Nqz
+// CTAs streaming the same V run side by side and share it through L2.
+// 9 warps x 3x3 tiles (one q); every (k, E) stage of V is copied in two
+// kappa halves into a 2-slot ring (41.5 KB slots at No = 12), so two CTAs
+// fit one SM (18 warps, 5/5/4/4 per SMSP instead of 3/2/2/2).  The inner
+// loop carries no divisions: stage coordinates advance incrementally, A rows
+// come from per-stage pointers (register double buffer across iterations and
+// stages), B fragments are two LDS.64 per column tile (the real-embedding
+// swap is a per-lane address offset, the negation a per-lane sign mask).
+// Accumulation order equals K6's: (k, E, kappa, h) ascending per output.
+// --------------------------------------------------------------------------
+constexpr int kPi2Slots = 2;
+
+__device__ __forceinline__ double xor_sign(double x, unsigned mask) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  asm volatile("xor.b32 %0, %0, %1;" : "+r"(hi) : "r"(mask));
+  double r;
+  asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
+// 112 registers: 2 x 9 warps x 32 x 112 = 64.5 K registers per SM
+// A row for invalid (w, E + off_w >= NE) rows: zeros, so the loads need no predicate
+__device__ double2 kPiZeroRow[kPiMaxNo * kPiMaxNo];
+constexpr int kPi2Pad = 64;  // double2 past the ring: B reads of discarded columns stay in bounds
+
+__global__ void __launch_bounds__(kPiWarps * 32, 2)
+pi_dmma2_kernel(PiArgs p, int chunk_atoms) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int no2 = p.no * p.no, ncol = p.ncol;
+  const int khp = (no2 + 3) / 4;        // kappa quads per stage
+  const int kh0 = (khp + 1) / 2;        // quads in the first half
+  const int slot_vec = kh0 * 4 * ncol;  // double2 per slot (the larger half)
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPi2Slots * slot_vec + kPi2Pad);
+  uint64_t* empty = full + kPi2Slots;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bx = blockIdx.x;
+  const int q = bx % p.nqz;
+  bx /= p.nqz;
+  const int ec = bx % p.echunks;
+  bx /= p.echunks;
+  const int pol = bx % 2;
+  const int la = bx / 2;
+  const int wg = blockIdx.y * kPiWarps + warp;
+  const bool active = wg < p.warp_groups;  // idle warps still take part in the barriers
+  const int n_ntile = (2 * ncol + 7) / 8;
+  const int gn = (n_ntile + 2) / 3;
+  const int mg = active ? wg / gn : 0, ng = active ? wg % gn : 0;
+  const int pcol = lane & 3;
+
+  // rows past No^2 in a slot are never copied: keep them finite (zero); they meet
+  // the clamped (finite) A of ragged quads, and their products are discarded zeros
+  for (int i = threadIdx.x; i < kPi2Slots * slot_vec + kPi2Pad; i += blockDim.x) ring[i] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPi2Slots; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kPiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zero stores before async-proxy writes
+  __syncthreads();
+
+  const double2* __restrict__ G1 = pol ? p.G[1] : p.G[0];
+  const double2* __restrict__ VT = (pol ? p.VT[1] : p.VT[0]) + (long long)la * p.nkz * p.ne * no2 * ncol;
+  const double2* g_atom = G1 + (p.g_atom_of_chunk0 + la) * p.g_sa;
+
+  int off_t[3];
+  bool row_ok[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int w = (mg * 3 + t) * 8 + (lane >> 2);
+    row_ok[t] = active && w < p.nw;
+    off_t[t] = row_ok[t] ? __ldg(p.off + w) : 0;
+  }
+  // B fragments (doubles within a kappa row of the slot): tile u reads column
+  // c0 + 4u; the re-row takes component `im`, the im-row the other component,
+  // sign-flipped when it is Im V.  Columns >= ncol feed discarded outputs.
+  const int nc0 = ng * 3 * 8 + (lane >> 2);
+  const int im = nc0 & 1;
+  const int b_off = 2 * (nc0 >> 1) + im;
+  const unsigned b_mask = im ? 0u : 0x80000000u;
+  int off_min = 1 << 30;
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+    if (row_ok[t]) off_min = min(off_min, off_t[t]);
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
+
+  double acc[3][3][2];
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+#pragma unroll
+    for (int u = 0; u < 3; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+
+  const int e_lo = ec * p.e_per_chunk, e_hi = min(p.ne, e_lo + p.e_per_chunk);
+  const int ne_c = e_hi - e_lo;
+  const int n_st = p.nkz * ne_c;
+  const int n_ss = 2 * n_st;  // half stages
+
+  // producer of half stage ss (lane 0 of warp ss % kPiWarps)
+  auto produce = [&](int ss) {
+    const int slot = ss & 1;
+    if (ss >= kPi2Slots) mbar_wait(empty + slot, (uint32_t)(((ss - kPi2Slots) >> 1) & 1));
+    const int st = ss >> 1, half = ss & 1;
+    const int k = st / ne_c, e = e_lo + st % ne_c;
+    const int r0 = half ? kh0 * 4 : 0;
+    const int r1 = half ? no2 : min(no2, kh0 * 4);
+    if (r1 <= r0) {  // empty half (khp == 1)
+      mbar_arrive(full + slot);
+      return;
+    }
+    const uint32_t bytes = (uint32_t)(r1 - r0) * ncol * 16;
+    mbar_arrive_expect_tx(full + slot, bytes);
+    bulk_g2s(ring + slot * slot_vec, VT + (((long long)k * p.ne + e) * no2 + r0) * ncol, bytes, full + slot);
+  };
+
+  // A rows of a stage: G1[(k+q) % Nkz, e + off_t, atom] (zero row when invalid)
+  const double2* rows[3];
+  auto stage_rows = [&](int k, int e) {
+    int kp = k + q;
+    if (kp >= p.nkz) kp -= p.nkz;
+    const double2* base = g_atom + (long long)kp * p.g_sk + (long long)e * p.g_se;
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+      rows[t] = (row_ok[t] && e + off_t[t] < p.ne) ? base + off_t[t] * p.g_se : kPiZeroRow;
+  };
+  const int kap_max = no2 - 1;
+  auto load_a = [&](double2 (&a)[3], int kq) {
+    const int kap = min(kq * 4 + pcol, kap_max);  // ragged last quad: any finite element
+#pragma unroll
+    for (int t = 0; t < 3; ++t) a[t] = __ldg(rows[t] + kap);
+  };
+  auto mma = [&](const double2 (&a)[3], const double* sb) {
+    double b_re[3], b_im[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      b_re[u] = sb[b_off + 8 * u];
+      b_im[u] = xor_sign(sb[(b_off ^ 1) + 8 * u], b_mask);
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) dmma884(acc[t][u], a[t].x, b_re[u]);
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int u = 0; u < 3; ++u) dmma884(acc[t][u], a[t].y, b_im[u]);
+  };
+
+  if (threadIdx.x == 0 && n_ss > 0) produce(0);
+  int k = 0, e = e_lo;
+  stage_rows(k, e);
+  double2 a[3];
+  load_a(a, 0);
+  bool live = active && e + off_min < p.ne;  // warp-uniform, per stage
+  for (int ss = 0; ss < n_ss; ++ss) {
+    const int half = ss & 1;
+    if (lane == 0 && ss + 1 < n_ss && (ss + 1) % kPiWarps == warp) produce(ss + 1);
+    mbar_wait(full + half, (uint32_t)((ss >> 1) & 1));
+    const double* sb = reinterpret_cast<const double*>(ring + half * slot_vec) + pcol * 2 * ncol;
+    const int kq0 = half ? kh0 : 0, kq1 = half ? khp : kh0;
+    const bool stage_end = kq1 == khp;
+    const int kq_plain = stage_end ? kq1 - 1 : kq1;
+    if (live) {
+      // ping-pong: quad kq+1's A is loaded while quad kq multiplies
+#pragma unroll 2
+      for (int kq = kq0; kq < kq_plain; ++kq) {
+        double2 an[3];
+        load_a(an, kq + 1);
+        mma(a, sb);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) a[t] = an[t];
+        sb += 8 * ncol;
+      }
+    }
+    if (stage_end && kq0 < kq1) {  // last quad: prefetch the next stage's first quad
+      if (++e == e_hi) {
+        e = e_lo;
+        ++k;
+      }
+      const bool live_now = live;
+      double2 an[3];
+      if (ss + 1 < n_ss) {
+        stage_rows(k, e);
+        load_a(an, 0);
+      }
+      if (live_now) mma(a, sb);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) a[t] = an[t];
+      live = active && e + off_min < p.ne;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + half);
+  }
+
+  if (!active) return;
+  double2* part = p.partial + ((((long long)la * 2 + pol) * p.nqz + q) * p.echunks + ec) * p.nw * ncol;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int w = (mg * 3 + t) * 8 + (lane >> 2);
+    if (w >= p.nw) continue;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int c = (ng * 3 + u) * 4 + (lane & 3);
+      if (c < ncol)
+        part[(long long)w * ncol + c] = make_double2(p.energy_weight * acc[t][u][0], p.energy_weight * acc[t][u][1]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K6 v3 (production for No >= 3): as v2 (TMA half stages, 2 CTAs per SM, q
+// fastest), but each warp owns ONE 8-row m-tile (8 lags w) across 9 n-tiles
+// (72 real columns = 36 complex chains), so no two warps of a CTA load the same
+// G1 row (v2: 3x), and one A fragment per quad lets the register prefetch run
+// two quads ahead across half-stage and stage boundaries.  B: per n-tile two
+// LDS.64 (component swap by lane address, sign by lane mask) from the slot.
+// Same per-output accumulation order as K6/v2: (k, E, kappa quad, h).
+// --------------------------------------------------------------------------
+constexpr int kPi3NT = 9;     // n-tiles per warp
+constexpr int kPi3Sub = 6;    // sub-stages per (k, E) stage (6 quads each at No = 12)
+constexpr int kPi3Slots = 4;  // ring slots: the producer runs kPi3Slots - 1 sub-stages ahead
+
+__global__ void __launch_bounds__(kPiWarps * 32, 3)
+pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int no2 = p.no * p.no, ncol = p.ncol;
+  const int khp = (no2 + 3) / 4;                     // kappa quads per stage (>= 2 here)
+  const int qs = 2 * ((khp + 2 * kPi3Sub - 1) / (2 * kPi3Sub));  // quads per sub-stage (even)
+  const int slot_vec = qs * 4 * ncol;                // double2 per slot
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPi3Slots * slot_vec + kPi2Pad);
+  uint64_t* empty = full + kPi3Slots;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bx = blockIdx.x;
+  const int q = bx % p.nqz;
+  bx /= p.nqz;
+  const int ec = bx % p.echunks;
+  bx /= p.echunks;
+  const int pol = bx % 2;
+  const int la = bx / 2;
+  const int m_tiles = (p.nw + 7) / 8;
+  const int n_groups = ((2 * ncol + 7) / 8 + kPi3NT - 1) / kPi3NT;
+  const int wg = blockIdx.y * kPiWarps + warp;
+  const bool active = wg < m_tiles * n_groups;  // idle warps still take part in the barriers
+  const int mt = active ? wg % m_tiles : 0, ng = active ? wg / m_tiles : 0;
+  const int pcol = lane & 3;
+
+  for (int i = threadIdx.x; i < kPi3Slots * slot_vec + kPi2Pad; i += blockDim.x) ring[i] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPi3Slots; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kPiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  const double2* __restrict__ G1 = pol ? p.G[1] : p.G[0];
+  const double2* __restrict__ VT = (pol ? p.VT[1] : p.VT[0]) + (long long)la * p.nkz * p.ne * no2 * ncol;
+  const double2* g_atom = G1 + (p.g_atom_of_chunk0 + la) * p.g_sa;
+
+  const int w = mt * 8 + (lane >> 2);
+  const bool row_ok = active && w < p.nw;
+  const int off = row_ok ? __ldg(p.off + w) : 0;
+  int off_min = row_ok ? off : (1 << 30);
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
+  const int nc0 = ng * kPi3NT * 8 + (lane >> 2);
+  const int im = nc0 & 1;
+  // column of tile 0 in the (swizzled) slot row: kappa rows with bit 1 set hold
+  // column c at c ^ swz; the xor keeps tile u's column at +4u (8u doubles)
+  const int b_off = 2 * ((nc0 >> 1) ^ (((pcol >> 1) & 1) ? p.swz : 0)) + im;
+  const int b_dim = im ? -1 : 1;          // the other component of the same column
+  const unsigned b_mask = im ? 0u : 0x80000000u;
+
+  double acc[kPi3NT][2];
+#pragma unroll
+  for (int u = 0; u < kPi3NT; ++u) acc[u][0] = acc[u][1] = 0.0;
+
+  const int e_lo = ec * p.e_per_chunk, e_hi = min(p.ne, e_lo + p.e_per_chunk);
+  const int ne_c = e_hi - e_lo;
+  const int n_st = p.nkz * ne_c;
+  const int n_ss = kPi3Sub * n_st;
+
+  auto produce = [&](int t) {
+    const int slot = t % kPi3Slots;
+    if (t >= kPi3Slots) mbar_wait(empty + slot, (uint32_t)(((t - kPi3Slots) / kPi3Slots) & 1));
+    const int st = t / kPi3Sub, j = t % kPi3Sub;
+    const int k = st / ne_c, e = e_lo + st % ne_c;
+    const int r0 = min(j * qs * 4, no2), r1 = min((j + 1) * qs * 4, no2);
+    if (r1 <= r0) {  // empty sub-stage (few quads)
+      mbar_arrive(full + slot);
+      return;
+    }
+    const uint32_t bytes = (uint32_t)(r1 - r0) * ncol * 16;
+    mbar_arrive_expect_tx(full + slot, bytes);
+    bulk_g2s(ring + slot * slot_vec, VT + (((long long)k * p.ne + e) * no2 + r0) * ncol, bytes, full + slot);
+  };
+  // this lane's A row of stage (k, e) at kappa = pcol (zero row when invalid)
+  auto row_of = [&](int k, int e) -> const double2* {
+    int kp = k + q;
+    if (kp >= p.nkz) kp -= p.nkz;
+    return (row_ok && e + off < p.ne)
+               ? g_atom + (long long)kp * p.g_sk + (long long)(e + off) * p.g_se + pcol
+               : kPiZeroRow + pcol;
+  };
+  // ragged last quad (No^2 % 4 != 0): lanes past No^2 read zeros, because the
+  // slot rows they meet may hold another sub-stage's (stale, finite) B
+  const int kq_last = (no2 - 1 - pcol) / 4;
+  const double2 *cur, *nxt;
+  auto load_a = [&](int kq) -> double2 {  // quad kq of the current stage, or kq - khp of the next
+    const double2* r = kq < khp ? cur : nxt;
+    const int qq = kq < khp ? kq : kq - khp;
+    return __ldg(qq <= kq_last ? r + qq * 4 : kPiZeroRow);
+  };
+
+  if (threadIdx.x == 0)
+    for (int t = 0; t < kPi3Slots - 1 && t < n_ss; ++t) produce(t);
+  int k = 0, e = e_lo;
+  int kn = 0, en = e_lo + 1;  // next stage
+  if (en == e_hi) {
+    en = e_lo;
+    ++kn;
+  }
+  cur = row_of(k, e);
+  nxt = n_st > 1 ? row_of(kn, en) : cur;
+  double2 a0 = load_a(0), a1 = load_a(1);
+  int kq = 0, j = 0, slot = 0;
+  uint32_t phase = 0;
+  for (int ss = 0; ss < n_ss; ++ss) {
+    const int t = ss + kPi3Slots - 1;
+    if (lane == 0 && t < n_ss && t % kPiWarps == warp) produce(t);
+    __syncwarp();  // reconverge before the warp-wide mma.sync
+    mbar_wait(full + slot, phase);
+    const bool live = active && e + off_min < p.ne;  // warp-uniform
+    const double* sb = reinterpret_cast<const double*>(ring + slot * slot_vec) + pcol * 2 * ncol + b_off;
+    const int kq1 = min((j + 1) * qs, khp);
+    // quads in pairs: a0 / a1 swap roles without register moves (a move would
+    // wait for the prefetch to land); sub-stages hold an even number of quads
+    // except the last one of an odd-khp stage
+    auto quad = [&](const double2& a, const double* b) {
+      double br[kPi3NT], bi[kPi3NT];
+#pragma unroll
+      for (int u = 0; u < kPi3NT; ++u) {
+        br[u] = b[8 * u];
+        bi[u] = xor_sign(b[8 * u + b_dim], b_mask);
+      }
+#pragma unroll
+      for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[u], a.x, br[u]);
+#pragma unroll
+      for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[u], a.y, bi[u]);
+    };
+    for (; kq + 1 < kq1; kq += 2) {
+      if (live) quad(a0, sb);
+      a0 = load_a(kq + 2);
+      if (live) quad(a1, sb + 8 * ncol);
+      a1 = load_a(kq + 3);
+      sb += 16 * ncol;
+    }
+    if (kq < kq1) {  // odd tail
+      if (live) quad(a0, sb);
+      a0 = a1;
+      a1 = load_a(kq + 2);
+      ++kq;
+    }
+    if (lane == 0) mbar_arrive(empty + slot);
+    if (++slot == kPi3Slots) {
+      slot = 0;
+      phase ^= 1u;
+    }
+    if (++j == kPi3Sub) {  // stage done: shift the stage window
+      j = 0;
+      kq -= khp;
+      k = kn;
+      e = en;
+      cur = nxt;
+      if (++en == e_hi) {
+        en = e_lo;
+        ++kn;
+      }
+      if (ss + 1 + kPi3Sub < n_ss) nxt = row_of(kn, en);
+    }
+  }
+
+  if (!active) return;
+  if (w >= p.nw) return;
+  double2* part = p.partial + ((((long long)la * 2 + pol) * p.nqz + q) * p.echunks + ec) * p.nw * ncol;
+#pragma unroll
+  for (int u = 0; u < kPi3NT; ++u) {
+    const int c = (ng * kPi3NT + u) * 4 + (lane & 3);
+    if (c < ncol)
+      part[(long long)w * ncol + c] = make_double2(p.energy_weight * acc[u][0], p.energy_weight * acc[u][1]);
+  }
+}
+
+// --------------------------------------------------------------------------
 // K7: Pi assembly (sse.py:393-406): chain = sum of the E-chunk partials in
 // order; Pi[q,w,a,1+s] = i chain_s, Pi[q,w,a,0] = -i sum_s chain_s.
 // --------------------------------------------------------------------------
@@ -1322,21 +1734,66 @@ cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
-  const size_t stage_bytes = (size_t)a.no * a.no * a.ncol * 16;
-  const size_t smem = kPiStages * stage_bytes + 2 * kPiStages * 8;
+// K6 selection (env SSE_PI_KERNEL, read per call): 3 = one m-tile per warp,
+// quarter-stage ring (default); 2 = 3x3 tiles per warp, half stages; 1 = two
+// momenta per CTA, whole stages; 0 = direct (no TMA).  A variant whose ring
+// does not fit in shared memory (or v3 with fewer than 2 kappa quads) falls
+// back to the next one.  All accumulate in the same order (bitwise equal).
+static size_t pi_smem(int v, int no, int ncol) {
+  const int khp = (no * no + 3) / 4;
+  if (v == 3)
+    return ((size_t)kPi3Slots * 2 * ((khp + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) * 4 * ncol + kPi2Pad) * 16 +
+           2 * kPi3Slots * 8;
+  if (v == 2) return ((size_t)kPi2Slots * ((khp + 1) / 2) * 4 * ncol + kPi2Pad) * 16 + 2 * kPi2Slots * 8;
+  if (v == 1) return (size_t)kPiStages * no * no * ncol * 16 + 2 * kPiStages * 8;
+  return 0;
+}
+static int pi_kernel_choice(int no, int ncol) {
   const char* env = getenv("SSE_PI_KERNEL");
-  const bool direct = (env && env[0] == '0') || smem > 220 * 1024;
+  int v = (env && env[0] >= '0' && env[0] <= '3') ? env[0] - '0' : 3;
+  if (v == 3 && (no * no + 3) / 4 < 2) v = 2;
+  while (v > 0 && pi_smem(v, no, ncol) > 220 * 1024) --v;
+  return v;
+}
+// column swizzle of V rows for K6 v3 (conflict-free B reads): column c of
+// kappa row r is stored at c ^ (2 * ((r >> 1) & 1)); needs ncol % 4 == 0
+int pi_vt_swizzle(int no, int ncol) { return (pi_kernel_choice(no, ncol) == 3 && ncol % 4 == 0) ? 2 : 0; }
+
+cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
+  const int v = pi_kernel_choice(a.no, a.ncol);
+  if (a.swz != (v == 3 && a.ncol % 4 == 0 ? 2 : 0)) return cudaErrorInvalidValue;  // K5 / K6 disagree
+  const size_t smem = pi_smem(v, a.no, a.ncol);
   const unsigned gy = (unsigned)((a.warp_groups + kPiWarps - 1) / kPiWarps);
-  if (direct) {
-    dim3 grid((unsigned)((long long)chunk_atoms * 2 * a.nqz * a.echunks), gy);
-    pi_dmma_direct_kernel<<<grid, kPiWarps * 32, 0, st>>>(a, chunk_atoms);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(pi_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int qblocks = (a.nqz + kPiQB - 1) / kPiQB;
-    dim3 grid((unsigned)((long long)chunk_atoms * 2 * qblocks * a.echunks), gy);
-    pi_dmma_kernel<<<grid, kPiWarps * 32, smem, st>>>(a, chunk_atoms);
+  const unsigned gx = (unsigned)((long long)chunk_atoms * 2 * a.echunks * a.nqz);
+  cudaError_t e = cudaSuccess;
+  switch (v) {
+    case 3: {
+      e = cudaFuncSetAttribute(pi_dmma3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)  // two CTAs per SM need the full shared-memory carveout
+        e = cudaFuncSetAttribute(pi_dmma3_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      const int groups = ((a.nw + 7) / 8) * (((2 * a.ncol + 7) / 8 + kPi3NT - 1) / kPi3NT);
+      pi_dmma3_kernel<<<dim3(gx, (unsigned)((groups + kPiWarps - 1) / kPiWarps)), kPiWarps * 32, smem, st>>>(
+          a, chunk_atoms);
+      break;
+    }
+    case 2:
+      e = cudaFuncSetAttribute(pi_dmma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(pi_dmma2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      pi_dmma2_kernel<<<dim3(gx, gy), kPiWarps * 32, smem, st>>>(a, chunk_atoms);
+      break;
+    case 1: {
+      e = cudaFuncSetAttribute(pi_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      const int qblocks = (a.nqz + kPiQB - 1) / kPiQB;
+      dim3 grid((unsigned)((long long)chunk_atoms * 2 * qblocks * a.echunks), gy);
+      pi_dmma_kernel<<<grid, kPiWarps * 32, smem, st>>>(a, chunk_atoms);
+      break;
+    }
+    default:
+      pi_dmma_direct_kernel<<<dim3(gx, gy), kPiWarps * 32, 0, st>>>(a, chunk_atoms);
   }
   return cudaGetLastError();
 }

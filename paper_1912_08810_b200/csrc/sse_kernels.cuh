@@ -81,6 +81,7 @@ struct PiBuildArgs {
   int nkz, ne, nb, no;
   int atom_begin, chunk_atoms;  // chunk within the output slab (dH rows, nbr rows)
   long long g_sa, g_sk, g_se;
+  int swz;                      // V column swizzle (pi_vt_swizzle)
 };
 struct PiArgs {
   const double2* G[2];      // G slab per polarity
@@ -93,6 +94,7 @@ struct PiArgs {
   double energy_weight;
   long long g_sa, g_sk, g_se;
   long long g_atom_of_chunk0;  // G-slab index of the chunk's first output atom
+  int swz;                     // V column swizzle (must match K5's)
 };
 struct PiAssembleArgs {
   const double2* partial;
@@ -102,6 +104,7 @@ struct PiAssembleArgs {
 };
 cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st);
 cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st);
+int pi_vt_swizzle(int no, int ncol);
 cudaError_t launch_pi_assemble(const PiAssembleArgs& a, cudaStream_t st);
 
 cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st);

@@ -94,16 +94,25 @@ def test_pi_hoisting_is_value_neutral():
     (2, 2, 17, 5, 5, 4, 10),    # No = 10 (small config), 5 atoms (odd) with NB even
     (4, 3, 9, 3, 4, 1, 5),      # NB = 1 (XOR partner slot), Nqz < Nkz
     (1, 1, 12, 11, 3, 2, 4),    # Nw close to NE (most E + off >= NE terms dropped)
+    (2, 2, 7, 3, 4, 2, 1),      # No = 1: one kappa quad, empty second half stage
+    (3, 2, 11, 4, 4, 2, 3),     # No = 3: No^2 = 9, ragged last quad
 ])
-def test_pi_shapes_against_oracle(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o):
+def test_pi_shapes_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_a, n_b, n_o):
+    """Every K6 variant (0 direct, 1 TMA 2-q, 2 TMA half stages, 3 one m-tile per warp) vs the oracle."""
     p = SimParams(n_kz=n_kz, n_qz=n_qz, n_E=n_e, n_w=n_w, n_A=n_a, n_B=n_b, n_orb=n_o)
     g_l, g_g, _, _, dh = inputs.stream_instance(5, p, dh_scale=0.05)
     nmap = build_neighbor_map(n_a, n_b)
     grid = default_grid(p)
-    out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
     ch_l, ch_g = orc.pi_chains(g_l, g_g, dh, nmap.idx, np.array(grid.offsets), grid.energy_weight, n_qz)
     ref_l, ref_g = orc.pi_from_chains(ch_l, ch_g)
-    assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL
+    outs = []
+    for choice in ("3", "2", "1", "0"):
+        monkeypatch.setenv("SSE_PI_KERNEL", choice)
+        out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
+        assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
+        outs.append(out)
+    for o in outs[1:]:
+        assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
 
 
 def test_pi_point_mask_and_atom_range():
