@@ -152,6 +152,20 @@ int sse_pi_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_
                   const unsigned char* mask, double* Pi_l, double* Pi_g, void* stream,
                   sse_timing* t);
 
+/* The SSE phase of one Born iteration in one call (self_consistent_loop body,
+ * sse.py:532-534: dc = preprocess_D(g_ph, nmap); sigma = sse_sigma(...);
+ * pi = sse_pi(g_e, dH, nmap, grid, n_qz)).  Host arrays as in sse_sigma_c128
+ * and sse_pi_c128, but D_l / D_g are the RAW phonon tensors
+ * [Nqz, Nw, NA, NB+1, 3, 3] (preprocess_D runs on the device) and G is
+ * uploaded once for both Sigma and Pi.  Sigma [Nkz, NE, NA, No, No] and Pi
+ * [Nqz, Nw, NA, NB+1, 3, 3] are written in full.  Same numbers as the three
+ * separate calls (bitwise). */
+int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double* G_g,
+                   const double* D_l, const double* D_g, const double* dH,
+                   const int64_t* nmap, const int64_t* off, const double* wt,
+                   double energy_weight, double* Sig_l, double* Sig_g, double* Pi_l,
+                   double* Pi_g, sse_timing* t);
+
 /* Layout transform K1 (to_atom_major / to_grid_major, sse.py:48-55):
  * [Nkz, NE, NA, blk] <-> [NA, Nkz, NE, blk], blk = block_doubles doubles.
  * to_atom_major = 1: grid -> atom major; 0: atom -> grid major.  Device ptrs. */

@@ -27,6 +27,7 @@ EXPORTED = (
     "sse_sigma_device",
     "sse_pi_c128",
     "sse_pi_device",
+    "sse_phase_c128",
     "sse_layout_transform",
     "sse_preprocess_D",
     "sse_fill_synthetic",
@@ -114,6 +115,7 @@ def load() -> ctypes.CDLL:
         lib.sse_sigma_c128_slab.argtypes = [_P, pdims, i32, pslab, pslab] + [_P] * 7 + [_P, _P, _P, ptim]
         lib.sse_pi_c128.argtypes = [_P, pdims, _P, _P, _P, _P, _P, dbl, _P, i64, i64, _P, _P, ptim]
         lib.sse_pi_device.argtypes = [_P, pdims, pslab, pslab, _P, _P, _P, _P, _P, dbl, _P, _P, _P, _P, ptim]
+        lib.sse_phase_c128.argtypes = [_P, pdims] + [_P] * 8 + [dbl] + [_P] * 4 + [ptim]
         lib.sse_profile_begin.argtypes = [_P]
         lib.sse_profile_end.argtypes = [_P, ctypes.POINTER(SseProfile)]
         lib.sse_sigma_device.argtypes = [_P, pdims, pslab, pslab] + [_P] * 6 + [_P, _P, _P, _P, _P, ptim]

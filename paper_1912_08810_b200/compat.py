@@ -14,6 +14,12 @@ time:
 :func:`paper_1912_08810_b200.sse.sse_sigma` that returns the reference's own
 ``SelfEnergyTensor`` type; ``unpatch_reference()`` restores the originals.
 The reference stays read-only.
+
+With ``loop=True`` (default) ``self_consistent_loop`` (bound in negflow.sse,
+negflow.cli and the package root) is rebound to
+:func:`paper_1912_08810_b200.loop.self_consistent_loop`, whose SSE phase is
+one device call (G uploaded once, preprocess_D on the GPU); the GF phase
+stays the reference's ``gf_phase``.
 """
 
 from __future__ import annotations
@@ -27,6 +33,8 @@ _TARGETS = ("negflow.sse", "negflow.distsim", "negflow.cli", "negflow")
 # sse_pi is bound by name in negflow.sse (self_consistent_loop sse.py:534,
 # count_sse_phase sse.py:450), negflow.cli (cli.py:223) and the package root.
 _PI_TARGETS = ("negflow.sse", "negflow.cli", "negflow")
+# self_consistent_loop: sse.py:495, re-exported at __init__.py:22, bound in cli.py:28
+_LOOP_TARGETS = ("negflow.sse", "negflow.cli", "negflow")
 _saved: dict[tuple[str, str], object] = {}
 
 
@@ -53,6 +61,23 @@ def make_pi_drop_in(self_energy_cls, **kwargs):
     return sse_pi
 
 
+def make_loop_drop_in(**kwargs):
+    """self_consistent_loop with the reference signature, types and GF phase."""
+    from .loop import self_consistent_loop as _loop
+
+    def self_consistent_loop(dev, nmap, params, grid=None, max_iter=20, tol=1e-8, variant=None, solver="dense",
+                             threads=1, initial_sigma=None, initial_pi=None):
+        ref_sse = importlib.import_module("negflow.sse")
+        ref_gf = importlib.import_module("negflow.gf")
+        return _loop(dev, nmap, params, grid, max_iter, tol,
+                     variant if variant is not None else ref_sse.SseVariant.REFERENCE, solver, threads,
+                     initial_sigma, initial_pi, gf_phase=ref_sse.gf_phase, self_energy_cls=ref_gf.SelfEnergyTensor,
+                     result_cls=ref_sse.LoopResult, **kwargs)
+
+    self_consistent_loop.__doc__ = "B200 drop-in for negflow.sse.self_consistent_loop (sse.py:495-535)."
+    return self_consistent_loop
+
+
 def _bind(name: str, attr: str, fn) -> None:
     mod = importlib.import_module(name)
     if (name, attr) not in _saved:
@@ -60,8 +85,8 @@ def _bind(name: str, attr: str, fn) -> None:
     setattr(mod, attr, fn)
 
 
-def patch_reference(pi: bool = True, **kwargs) -> None:
-    """Rebind every reference lookup of ``sse_sigma`` (and ``sse_pi``) to the B200 path."""
+def patch_reference(pi: bool = True, loop: bool = True, **kwargs) -> None:
+    """Rebind every reference lookup of ``sse_sigma`` (``sse_pi``, ``self_consistent_loop``) to the B200 path."""
     gf = importlib.import_module("negflow.gf")
     drop_in = make_drop_in(gf.SelfEnergyTensor, **kwargs)
     for name in _TARGETS:
@@ -70,6 +95,10 @@ def patch_reference(pi: bool = True, **kwargs) -> None:
         pi_drop_in = make_pi_drop_in(gf.SelfEnergyTensor, **kwargs)
         for name in _PI_TARGETS:
             _bind(name, "sse_pi", pi_drop_in)
+    if loop:
+        loop_drop_in = make_loop_drop_in(**kwargs)
+        for name in _LOOP_TARGETS:
+            _bind(name, "self_consistent_loop", loop_drop_in)
 
 
 def unpatch_reference() -> None:

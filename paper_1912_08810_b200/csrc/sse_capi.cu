@@ -94,7 +94,7 @@ struct DevState {
   cudaStream_t stream = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev[6] = {};
   DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev;
-  DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2];
+  DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2], draw[2];
   std::vector<unsigned char> pi_mask_host;
   // host copies of the small tables last uploaded (skip re-uploads: a pageable
   // upload would otherwise serialise the host with the stream on every call)
@@ -465,6 +465,7 @@ struct HostCall {
   const int64_t *nmap, *off;  // nmap rows of hs atoms
   const double* wt;
   double *S_l, *S_g;
+  bool dc_resident = false;  // Dc already in ds.dc (device preprocess_D of sse_phase_c128)
 };
 
 cudaEvent_t pipe_event(DevState& ds, size_t i) {
@@ -581,10 +582,11 @@ int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi,
                                rows, cudaMemcpyHostToDevice, ds.s_h2d));
         copied = need;
       }
-      for (int p = 0; p < 2; ++p)
-        CU(cudaMemcpy2DAsync((char*)ds.dc[p].ptr + a0 * dc_row, on * dc_row,
-                             Dh[p] + (lo + a0 - c.hs.atom0) * dc_row, hdc_pitch, n * dc_row, dc_rows,
-                             cudaMemcpyHostToDevice, ds.s_h2d));
+      if (!c.dc_resident)
+        for (int p = 0; p < 2; ++p)
+          CU(cudaMemcpy2DAsync((char*)ds.dc[p].ptr + a0 * dc_row, on * dc_row,
+                               Dh[p] + (lo + a0 - c.hs.atom0) * dc_row, hdc_pitch, n * dc_row, dc_rows,
+                               cudaMemcpyHostToDevice, ds.s_h2d));
       CU(cudaMemcpyAsync((char*)ds.dh.ptr + a0 * dh_atom, dHh + a0 * dh_atom, n * dh_atom,
                          cudaMemcpyHostToDevice, ds.s_h2d));
       cudaEvent_t in = pipe_event(ds, ei++), done = pipe_event(ds, ei++);
@@ -606,9 +608,37 @@ int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi,
   CU(cudaEventSynchronize(ds.ev[1]));
   if (t) {
     t->total_ms = std::max(t->total_ms, (double)elapsed(ds.ev[0], ds.ev[1]));
-    t->h2d_bytes += 2 * (g_bytes + dc_bytes) + dh_bytes;
+    t->h2d_bytes += 2 * (g_bytes + (c.dc_resident ? 0 : dc_bytes)) + dh_bytes;
     t->d2h_bytes += 2 * s_bytes;
     t->kernel_launches += launches;
+  }
+  return SSE_OK;
+}
+
+// Reverse-slot table of the owned edges (device.py:53-66): for owned atom a and
+// slot s, b = idx[a, s] (as a D-slab index) and the first r with idx[b, r] == a.
+int preprocess_tables(const int64_t* nmap, int64_t na, int64_t nb, int64_t d_atom0, int64_t d_natoms,
+                      int64_t out_atom0, int64_t out_natoms, std::vector<int>& nbr, std::vector<int>& rev) {
+  nbr.assign(out_natoms * nb, 0);
+  rev.assign(out_natoms * nb, 0);
+  auto in_slab = [&](int64_t x) { return x >= d_atom0 && x < d_atom0 + d_natoms; };
+  for (int64_t la = 0; la < out_natoms; ++la) {
+    const int64_t a = out_atom0 + la;
+    if (!in_slab(a)) return fail(SSE_EINVAL, "atom %lld is not in the D slab", (long long)a);
+    for (int64_t s = 0; s < nb; ++s) {
+      const int64_t b = nmap[a * nb + s];
+      if (b < 0 || b >= na)
+        return fail(SSE_EINVAL, "neighbor index %lld of atom %lld outside [0, %lld)", (long long)b,
+                    (long long)a, (long long)na);
+      int64_t r = 0;
+      while (r < nb && nmap[b * nb + r] != a) ++r;
+      if (r == nb)
+        return fail(SSE_EINVAL, "missing neighbor slot: atom %lld not in neighbor list of %lld",
+                    (long long)a, (long long)b);
+      if (!in_slab(b)) return fail(SSE_EINVAL, "neighbor atom %lld is not in the D slab", (long long)b);
+      nbr[la * nb + s] = (int)(b - d_atom0);
+      rev[la * nb + s] = (int)r;
+    }
   }
   return SSE_OK;
 }
@@ -893,6 +923,121 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
   return SSE_OK;
 }
 
+// SSE phase of one Born iteration (sse.py:532-534) in one call: G^<> and raw
+// D^<> uploaded once, preprocess_D on the device, Sigma (pipelined chunks, G
+// kept resident) then Pi on the same G, both results downloaded.
+int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double* G_g, const double* D_l,
+                   const double* D_g, const double* dH, const int64_t* nmap, const int64_t* off, const double* wt,
+                   double energy_weight, double* Sig_l, double* Sig_g, double* Pi_l, double* Pi_g,
+                   sse_timing* t) {
+  if (!ctx) return fail(SSE_EINVAL, "context is NULL");
+  CHECK(validate_dims(d));
+  CHECK(validate_grid(d, off, wt));
+  if (!G_l || !G_g || !D_l || !D_g || !dH || !nmap || !Sig_l || !Sig_g || !Pi_l || !Pi_g)
+    return fail(SSE_EINVAL, "NULL tensor pointer");
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->flops = alg_flops(d, off, d->na);
+  }
+  const int nd = (int)ctx->devs.size();
+  if (t) t->n_devices = nd;
+  const int64_t per = (d->na + nd - 1) / nd;
+  const size_t blk = (size_t)d->norb * d->norb * 16;
+  const size_t d_row = (size_t)(d->nb + 1) * 9 * 16, d_rows = (size_t)(d->nqz * d->nw);
+  const size_t dc_row = (size_t)d->nb * 9 * 16;
+  const size_t pi_row = d_row, pi_rows = d_rows;
+  const sse_slab full{0, d->na, 0, 0};
+  auto on_device = [&](DevState& ds, int64_t lo, int64_t hi, sse_timing* tt) -> int {
+    const int64_t on = hi - lo;
+    if (on <= 0) return SSE_OK;
+    CU(cudaSetDevice(ds.device));
+    int64_t glo = lo, ghi = hi;
+    for (int64_t i = lo * d->nb; i < hi * d->nb; ++i) {
+      if (nmap[i] < 0 || nmap[i] >= d->na)
+        return fail(SSE_EINVAL, "neighbor index %lld outside [0, %lld)", (long long)nmap[i], (long long)d->na);
+      glo = std::min(glo, nmap[i]);
+      ghi = std::max(ghi, nmap[i] + 1);
+    }
+    const int64_t gn = ghi - glo;
+    cudaStream_t st = ds.stream;
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, st));
+    // raw D of the G slab's atoms, then Dc of the owned atoms (sse.py:105-113)
+    std::vector<int> nbr, rev;
+    CHECK(preprocess_tables(nmap, d->na, d->nb, glo, gn, lo, on, nbr, rev));
+    const char* Dh[2] = {(const char*)D_l, (const char*)D_g};
+    for (int p = 0; p < 2; ++p) {
+      CHECK(ds.draw[p].ensure(d_rows * gn * d_row));
+      CHECK(ds.dc[p].ensure(d_rows * on * dc_row));
+      CU(cudaMemcpy2DAsync(ds.draw[p].ptr, gn * d_row, Dh[p] + glo * d_row, d->na * d_row, gn * d_row, d_rows,
+                           cudaMemcpyHostToDevice, st));
+    }
+    CHECK(upload_cached(ds.pp_nbr, ds.pp_nbr_host, nbr, st));
+    CHECK(upload_cached(ds.pp_rev, ds.pp_rev_host, rev, st));
+    for (int p = 0; p < 2; ++p)
+      CHECK(profiled(ds, st, SSE_PROF_PREPROCESS, 0.0, [&] {
+        return sse::launch_preprocess_D(d->nqz, d->nw, gn, glo, lo, on, d->nb, ds.pp_nbr.as<int>(),
+                                        ds.pp_rev.as<int>(), ds.draw[p].as<double2>(), ds.dc[p].as<double2>(),
+                                        st);
+      }));
+    // Sigma: the pipelined host call with Dc resident; leaves the G slab in ds.g
+    HostCall c{d, SSE_VARIANT_BATCHED_FUSED, full, full, G_l, G_g, nullptr, nullptr, dH, nmap, off, wt, Sig_l, Sig_g};
+    c.dc_resident = true;
+    sse_timing ts{};
+    CHECK(host_call_on_device(ds, c, lo, hi, &ts));
+    // Pi on the resident G slab and owned dH
+    int launches = ts.kernel_launches + 2;
+    for (int p = 0; p < 2; ++p) CHECK(ds.pi_out[p].ensure(pi_rows * on * pi_row));
+    const sse_slab gs{glo, gn, 0, 0}, os{lo, on, 0, 0};
+    CHECK(pi_on_device(ds, d, gs, os, ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dh.as<double2>(),
+                       nmap + lo * d->nb, off, energy_weight, nullptr, ds.pi_out[0].as<double2>(),
+                       ds.pi_out[1].as<double2>(), st, &launches));
+    double* Ph[2] = {Pi_l, Pi_g};
+    for (int p = 0; p < 2; ++p)
+      CU(cudaMemcpy2DAsync((char*)Ph[p] + lo * pi_row, d->na * pi_row, ds.pi_out[p].ptr, on * pi_row,
+                           on * pi_row, pi_rows, cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(e1, st));
+    CU(cudaEventSynchronize(e1));
+    if (tt) {
+      tt->total_ms = std::max(tt->total_ms, (double)elapsed(e0, e1));
+      tt->h2d_bytes += ts.h2d_bytes + 2 * d_rows * gn * d_row;
+      tt->d2h_bytes += ts.d2h_bytes + 2 * pi_rows * on * pi_row;
+      tt->kernel_launches += launches;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return SSE_OK;
+  };
+  if (nd == 1) return on_device(ctx->devs[0], 0, d->na, t);
+  std::vector<int> rcs(nd, SSE_OK);
+  std::vector<sse_timing> ts(nd);
+  std::vector<std::string> errs(nd);
+  std::vector<std::thread> th;
+  for (int i = 0; i < nd; ++i)
+    th.emplace_back([&, i] {
+      std::memset(&ts[i], 0, sizeof(sse_timing));
+      const int64_t lo = std::min<int64_t>(i * per, d->na), hi = std::min<int64_t>((i + 1) * per, d->na);
+      rcs[i] = on_device(ctx->devs[i], lo, hi, &ts[i]);
+      if (rcs[i] != SSE_OK) errs[i] = g_last_error;
+    });
+  for (auto& x : th) x.join();
+  for (int i = 0; i < nd; ++i) {
+    if (rcs[i] != SSE_OK) {
+      g_last_error = errs[i];
+      return rcs[i];
+    }
+    if (t) {
+      t->total_ms = std::max(t->total_ms, ts[i].total_ms);
+      t->h2d_bytes += ts[i].h2d_bytes;
+      t->d2h_bytes += ts[i].d2h_bytes;
+      t->kernel_launches += ts[i].kernel_launches;
+    }
+  }
+  return SSE_OK;
+}
+
 int sse_layout_transform(sse_ctx* ctx, int64_t nkz, int64_t ne, int64_t na, int64_t block_doubles,
                          int to_atom_major, const double* src, double* dst, void* stream) {
   if (!ctx || ctx->devs.empty()) return fail(SSE_EINVAL, "context is NULL");
@@ -918,27 +1063,8 @@ int sse_preprocess_D(sse_ctx* ctx, int64_t nqz, int64_t nw, int64_t na, int64_t 
       out_natoms < 1 || d_atom0 < 0 || out_atom0 < 0 || d_atom0 + d_natoms > na ||
       out_atom0 + out_natoms > na)
     return fail(SSE_EINVAL, "invalid preprocess_D arguments");
-  // reverse-slot table of the owned edges (device.py:53-66): first r with idx[b, r] == a
-  std::vector<int> nbr(out_natoms * nb), rev(out_natoms * nb);
-  auto in_slab = [&](int64_t x) { return x >= d_atom0 && x < d_atom0 + d_natoms; };
-  for (int64_t la = 0; la < out_natoms; ++la) {
-    const int64_t a = out_atom0 + la;
-    if (!in_slab(a)) return fail(SSE_EINVAL, "atom %lld is not in the D slab", (long long)a);
-    for (int64_t s = 0; s < nb; ++s) {
-      const int64_t b = nmap[a * nb + s];
-      if (b < 0 || b >= na)
-        return fail(SSE_EINVAL, "neighbor index %lld of atom %lld outside [0, %lld)", (long long)b,
-                    (long long)a, (long long)na);
-      int64_t r = 0;
-      while (r < nb && nmap[b * nb + r] != a) ++r;
-      if (r == nb)
-        return fail(SSE_EINVAL, "missing neighbor slot: atom %lld not in neighbor list of %lld",
-                    (long long)a, (long long)b);
-      if (!in_slab(b)) return fail(SSE_EINVAL, "neighbor atom %lld is not in the D slab", (long long)b);
-      nbr[la * nb + s] = (int)(b - d_atom0);
-      rev[la * nb + s] = (int)r;
-    }
-  }
+  std::vector<int> nbr, rev;
+  CHECK(preprocess_tables(nmap, na, nb, d_atom0, d_natoms, out_atom0, out_natoms, nbr, rev));
   DevState& ds = ctx->devs[0];
   CU(cudaSetDevice(ds.device));
   cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;

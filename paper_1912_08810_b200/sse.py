@@ -241,6 +241,82 @@ def sse_pi(
     return _SE(lesser=out_l, greater=out_g)
 
 
+def sse_phase(
+    g_e,
+    g_ph,
+    dh: Array,
+    nmap,
+    grid,
+    n_qz: int,
+    *,
+    n_gpus: int | None = None,
+    timing: dict | None = None,
+):
+    """The SSE phase of one Born iteration in one library call.
+
+    Equivalent to the body of ``self_consistent_loop`` (sse.py:532-534)::
+
+        dc = preprocess_D(g_ph, nmap)
+        sigma = sse_sigma(variant, g_e, dc, dh, nmap, grid)
+        pi = sse_pi(g_e, dh, nmap, grid, n_qz)
+
+    but G is uploaded once for Sigma and Pi and preprocess_D runs on the
+    device (libsse ``sse_phase_c128``).  Every arrangement of the reference
+    gives the same Sigma here (the kernels are arrangement-independent), so
+    there is no variant argument.  Returns ``(sigma, pi)``.  Errors as the
+    three reference calls (ValueError for inconsistent shapes or a map that
+    is not reverse-closed, device.py:55-57).
+    """
+    if g_e.kind != "electron":
+        raise ValueError("sse_sigma expects an electron tensor")
+    if g_ph.kind != "phonon":
+        raise ValueError("preprocess_D expects the phonon Green's tensor")
+    g_l, g_g = g_e.lesser, g_e.greater
+    n_kz, n_e, n_a, n_o, n_o2 = g_l.shape
+    n_b = nmap.n_B
+    if n_o != n_o2:
+        raise ValueError(f"electron blocks must be square, got {n_o}x{n_o2}")
+    if n_a != nmap.n_A:
+        raise ValueError(f"electron tensor has {n_a} atoms but the neighbor map has {nmap.n_A}")
+    d_l, d_g = g_ph.lesser, g_ph.greater
+    if d_l.shape[2:] != (n_a, n_b + 1, 3, 3):
+        raise ValueError(f"phonon tensor must be [Nqz, Nw, {n_a}, {n_b + 1}, 3, 3], got {d_l.shape}")
+    if d_l.shape[0] != n_qz:
+        raise ValueError(f"phonon tensor has {d_l.shape[0]} momenta for n_qz={n_qz}")
+    n_w = d_l.shape[1]
+    dh = np.asarray(dh)
+    if dh.shape != (n_a, n_b, 3, n_o, n_o):
+        raise ValueError(f"dH must have shape {(n_a, n_b, 3, n_o, n_o)}, got {dh.shape}")
+    fmap = grid.frequency_map
+    if len(fmap) < n_w:
+        raise ValueError(f"frequency map has {len(fmap)} entries for n_w={n_w}")
+    offsets = np.array([int(fmap[w][0]) for w in range(n_w)], dtype=np.int64)
+    weights = np.array([float(fmap[w][1]) for w in range(n_w)], dtype=np.float64)
+    from .types import SelfEnergyTensor as _SE
+
+    sig_l = np.zeros(g_l.shape, dtype=np.complex128)
+    sig_g = np.zeros(g_l.shape, dtype=np.complex128)
+    pi_l = np.zeros(d_l.shape, dtype=np.complex128)
+    pi_g = np.zeros(d_l.shape, dtype=np.complex128)
+    if g_l.size == 0 or d_l.size == 0:
+        return _SE(lesser=sig_l, greater=sig_g), _SE(lesser=pi_l, greater=pi_g)
+    idx = np.ascontiguousarray(nmap.idx, dtype=np.int64)
+    if idx.size and (idx.min() < 0 or idx.max() >= n_a):
+        raise ValueError(f"neighbor map entries must lie in [0, {n_a})")
+    arrays = [_f64(g_l), _f64(g_g), _f64(d_l), _f64(d_g), _f64(dh)]
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    tim = _lib.SseTiming()
+    ctx = _lib.context(n_gpus=n_gpus or _default_gpus())
+    rc = _lib.load().sse_phase_c128(
+        ctx.handle, ctypes.byref(dims), *[_ptr(a) for a in arrays], _ptr(idx), _ptr(offsets), _ptr(weights),
+        float(grid.energy_weight), _ptr(sig_l), _ptr(sig_g), _ptr(pi_l), _ptr(pi_g), ctypes.byref(tim),
+    )
+    _lib.check(rc)
+    if timing is not None:
+        timing.update(tim.as_dict())
+    return _SE(lesser=sig_l, greater=sig_g), _SE(lesser=pi_l, greater=pi_g)
+
+
 # ---------------------------------------------------------------------------
 # device-resident API (torch CUDA tensors, complex128)
 # ---------------------------------------------------------------------------
