@@ -291,6 +291,67 @@ def e2e_phase(args, p, grid, idx, rank, world, local_rank) -> dict:
     return out
 
 
+def phase_e2e(args, p, grid, idx, local_rank) -> dict:
+    """the whole SSE phase of a Born iteration (preprocess_D + Sigma + Pi) through
+    sse_phase (C ABI sse_phase_c128) from pinned host memory, N = 1."""
+    import torch
+
+    from paper_1912_08810_b200 import inputs
+    from paper_1912_08810_b200 import sse as dev
+    from paper_1912_08810_b200.sse import Profile
+    from paper_1912_08810_b200.types import GreensTensor, NeighborMap
+
+    no2 = p.n_orb * p.n_orb
+    cuda = torch.device("cuda", local_rank)
+    pin = dict(dtype=torch.complex128, pin_memory=True)
+    e_shape = (p.n_kz, p.n_E, p.n_A, p.n_orb, p.n_orb)
+    ph_shape = (p.n_qz, p.n_w, p.n_A, p.n_B + 1, 3, 3)
+    g_host = [torch.empty(e_shape, **pin) for _ in range(2)]
+    d_host = [torch.empty(ph_shape, **pin) for _ in range(2)]
+    out = [torch.empty(e_shape, **pin) for _ in range(2)] + [torch.empty(ph_shape, **pin) for _ in range(2)]
+    dh_host = torch.empty((p.n_A, p.n_B, 3, p.n_orb, p.n_orb), **pin)
+    for pol, tid in ((0, inputs.G_LESSER), (1, inputs.G_GREATER)):
+        tmp = torch.empty(e_shape, dtype=torch.complex128, device=cuda)
+        dev.fill_synthetic(tmp, 0, tid, 0, p.n_A, p.n_kz * p.n_E, no2, no2, p.n_A * no2)
+        g_host[pol].copy_(tmp)
+        del tmp
+    slots = (p.n_B + 1) * 9
+    for pol, tid in ((0, inputs.D_LESSER), (1, inputs.D_GREATER)):
+        d = torch.empty(ph_shape, dtype=torch.complex128, device=cuda)
+        dev.fill_synthetic(d, 0, tid, 0, p.n_A, p.n_qz * p.n_w, slots, slots, p.n_A * slots)
+        d_host[pol].copy_(d)
+        del d
+    dht = torch.empty(dh_host.shape, dtype=torch.complex128, device=cuda)
+    inner = p.n_B * 3 * no2
+    dev.fill_synthetic(dht, 0, inputs.DH, 0, p.n_A, 1, inner, inner, 0, scale=inputs.DH_SCALE)
+    dh_host.copy_(dht)
+    del dht
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    g = GreensTensor(g_host[0].numpy(), g_host[1].numpy())
+    gph = GreensTensor(d_host[0].numpy(), d_host[1].numpy())
+    outs = tuple(o.numpy() for o in out)
+    nmap = NeighborMap(idx)
+
+    def call(tim):
+        dev.sse_phase(g, gph, dh_host.numpy(), nmap, grid, p.n_qz, device=local_rank, out=outs, timing=tim)
+
+    call({})
+    times = []
+    with Profile(device=local_rank) as prof:
+        for _ in range(args.phase_steps):
+            tim = {}
+            call(tim)
+            times.append(tim["total_ms"])
+    res = {"value": float(np.mean(times)) / 1e3, "unit": "s", "steps": args.phase_steps, "warmup": 1,
+           "h2d_bytes_per_step": int(tim["h2d_bytes"]), "d2h_bytes_per_step": int(tim["d2h_bytes"]),
+           "kernel_ms_per_step": {k: v["ms"] / args.phase_steps for k, v in prof.result.items() if v["launches"]},
+           "path": "sse_phase (C ABI sse_phase_c128): G<> + raw D<> + dH in once, device preprocess_D, "
+                   "pipelined Sigma (K2+K3), Pi (K5-K7) on the resident G, Sigma + Pi out"}
+    del g, gph, outs, g_host, d_host, out, dh_host
+    return res
+
+
 def load_traffic():
     path = os.path.join(REPO, "profiles", "sigma_kernel_traffic.json")
     try:
@@ -452,6 +513,10 @@ def run_gpu(args, p, grid, idx) -> None:
     if args.e2e:
         e2e = e2e_phase(args, p, grid, idx, rank, world, local_rank)
 
+    phase = None
+    if args.phase_steps > 0 and world == 1:
+        phase = phase_e2e(args, p, grid, idx, local_rank)
+
     cpu = None
     if rank == 0 and world == 1 and args.cpu_pairs > 0:
         s = cpu_sample(p, grid, idx, args.cpu_pairs)
@@ -499,6 +564,8 @@ def run_gpu(args, p, grid, idx) -> None:
             line["gf_layout"] = gf_info
         if e2e is not None:
             line["e2e"] = e2e
+        if phase is not None:
+            line["sse_phase_e2e"] = phase
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -522,6 +589,8 @@ def main():
     ap.add_argument("--ref-pairs", type=int, default=1, help="pairs per step of --impl reference")
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--pi-steps", type=int, default=1, help="timed Pi evaluations after Sigma (0 = skip)")
+    ap.add_argument("--phase-steps", type=int, default=0,
+                    help="N=1: timed SSE phases (preprocess_D + Sigma + Pi) through sse_phase from pinned host memory")
     ap.add_argument("--gf-layout-steps", type=int, default=0,
                     help="N>1: timed steps starting from the GF (k,E)-point layout (two all-to-alls)")
     args = ap.parse_args()

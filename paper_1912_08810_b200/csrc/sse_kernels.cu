@@ -159,6 +159,17 @@ __device__ __forceinline__ void dmma884_nv(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// x with its sign bit xor-ed with `mask` (0 or 0x80000000) on the integer pipe
+// (an FP64 negation would issue on the FP64 pipe the DMMAs use)
+__device__ __forceinline__ double xor_sign(double x, unsigned mask) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  asm volatile("xor.b32 %0, %0, %1;" : "+r"(hi) : "r"(mask));
+  double r;
+  asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
 template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32)
 sigma_dmma_kernel(SigmaArgs p) {
@@ -722,6 +733,135 @@ pi_build_kernel(PiBuildArgs p) {
 }
 
 // --------------------------------------------------------------------------
+// K5 v2 (DMMA, No % 4 == 0): the same V on FP64 tensor cores.  Per (point,
+// chain polarity, s) two real-embedded GEMMs:
+//   U_s = [dH_{s,0}; dH_{s,1}; dH_{s,2}] (3No x No) @ G2_s (No x No)
+//   W_s = U_s (3No x No) @ [dH_{s,0} | dH_{s,1} | dH_{s,2}] (No x 3No)
+// W_s[(j,p)][(i,n)] = V_ij[p][n].  A warp owns one 8-row m-tile of U/W: the C
+// fragments of the first GEMM are, lane for lane, the A fragments of the
+// second (U[m][4kh + lane%4] is n-tile kh of the first product), so U never
+// leaves registers.  W is scattered into a shared-memory image of the point's
+// V block ([(n,p)][(s,i,j)], column-swizzled like K5) and written to HBM by
+// one bulk async copy (TMA) per point and polarity, double-buffered so the
+// store of one polarity overlaps the products of the next.
+// --------------------------------------------------------------------------
+constexpr int kPB2Warps = 20;     // 4 slots x 5 m-tiles at No = 12, NB = 4
+constexpr int kPB2Energies = 16;  // energies per CTA (dH staged once per CTA)
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int NO>
+__global__ void __launch_bounds__(kPB2Warps * 32, 1)
+pi_build_dmma_kernel(PiBuildArgs p) {
+  constexpr int NO2 = NO * NO, MROWS = 3 * NO, MT = (MROWS + 7) / 8;
+  constexpr int KH = NO / 4;         // k-steps per real/imaginary half
+  constexpr int NT1 = NO / 4;        // n-tiles of U (2No real columns)
+  constexpr int NT2 = 3 * NO / 4;    // n-tiles of W (6No real columns)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nb = p.nb, ncol = nb * 9;
+  const int vt_vec = NO2 * ncol;  // double2 per point and polarity
+  double2* vt = reinterpret_cast<double2*>(smem_raw);          // [2][No2][ncol]
+  double2* sdh = vt + 2 * vt_vec;                               // [nb][3][No][No]
+  double2* sg2 = sdh + nb * 3 * NO2;                            // [nb][No][No]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e_groups = (p.ne + kPB2Energies - 1) / kPB2Energies;
+  int bx = blockIdx.x;
+  const int eg = bx % e_groups;
+  bx /= e_groups;
+  const int k = bx % p.nkz;
+  const int la = bx / p.nkz;
+  const int e0 = eg * kPB2Energies, e1 = min(p.ne, e0 + kPB2Energies);
+
+  const double2* dH = p.dH + (long long)(p.atom_begin + la) * nb * 3 * NO2;
+  for (int x = threadIdx.x; x < nb * 3 * NO2; x += blockDim.x) sdh[x] = dH[x];
+
+  const int im = (lane >> 2) & 1;                  // this lane's B column is an imaginary part
+  const unsigned neg = im ? 0u : 0x80000000u;      // the im-row of a real column is -Im
+  const int kl = lane & 3;
+  const int tasks = nb * MT;
+  int step = 0;  // (point, polarity) counter: buffer = step & 1
+  for (int e = e0; e < e1; ++e) {
+    const bool masked = p.mask && !p.mask[k * p.ne + e];
+    for (int pol = 0; pol < 2; ++pol, ++step) {
+      double2* buf = vt + (step & 1) * vt_vec;
+      const double2* G2 = pol ? p.G[0] : p.G[1];  // chain pol 0 (lesser): G2 = G>; pol 1: G2 = G<
+      __syncthreads();  // sg2 / buf readers of the previous steps are done
+      if (threadIdx.x == 0 && step >= 2) bulk_wait_read<1>();  // buf's store (two steps ago) has read it
+      for (int x = threadIdx.x; x < nb * NO2; x += blockDim.x) {
+        const int ss = x / NO2, rr = x % NO2;
+        const long long lb = p.nbr[la * nb + ss];
+        sg2[x] = masked ? make_double2(0.0, 0.0)
+                        : G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e * p.g_se + rr];
+      }
+      __syncthreads();
+      for (int task = warp; task < tasks; task += kPB2Warps) {
+        const int ss = task / MT, mt = task % MT;
+        const int m = mt * 8 + (lane >> 2);
+        const bool m_ok = m < MROWS;
+        const int mj = m_ok ? m / NO : 0, mp = m_ok ? m % NO : 0;
+        const double2* dsr = sdh + ((ss * 3 + mj) * NO + mp) * NO;  // row (j, p) of D_s
+        const double2* g2 = sg2 + ss * NO2;
+        double u[NT1][2];
+#pragma unroll
+        for (int nt = 0; nt < NT1; ++nt) u[nt][0] = u[nt][1] = 0.0;
+#pragma unroll
+        for (int kh = 0; kh < KH; ++kh) {
+          const int r = 4 * kh + kl;
+          const double2 a = m_ok ? dsr[r] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int nt = 0; nt < NT1; ++nt) {
+            const double2 g = g2[r * NO + ((nt * 8 + (lane >> 2)) >> 1)];
+            dmma884_nv(u[nt], a.x, im ? g.y : g.x);
+            dmma884_nv(u[nt], a.y, xor_sign(im ? g.x : g.y, neg));
+          }
+        }
+        double w[NT2][2];
+#pragma unroll
+        for (int nt = 0; nt < NT2; ++nt) w[nt][0] = w[nt][1] = 0.0;
+#pragma unroll
+        for (int kh = 0; kh < KH; ++kh) {
+          const int t = 4 * kh + kl;  // U[m][t] = u[kh] of this lane
+#pragma unroll
+          for (int nt = 0; nt < NT2; ++nt) {
+            const int cc = (nt * 8 + (lane >> 2)) >> 1, i = cc / NO, n = cc % NO;
+            const double2 h = sdh[((ss * 3 + i) * NO + t) * NO + n];
+            dmma884_nv(w[nt], u[kh][0], im ? h.y : h.x);
+            dmma884_nv(w[nt], u[kh][1], xor_sign(im ? h.x : h.y, neg));
+          }
+        }
+        if (m_ok) {
+#pragma unroll
+          for (int nt = 0; nt < NT2; ++nt) {
+            const int cc = nt * 4 + kl, i = cc / NO, n = cc % NO;
+            const int kap = n * NO + mp;
+            const int c = ss * 9 + i * 3 + mj;
+            buf[kap * ncol + (c ^ (((kap >> 1) & 1) ? p.swz : 0))] = make_double2(w[nt][0], w[nt][1]);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS visible to the bulk copy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double2* out = p.VT[pol] + (((long long)la * p.nkz + k) * p.ne + e) * vt_vec;
+        bulk_s2g(out, buf, (uint32_t)vt_vec * 16);
+        bulk_commit();
+      }
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// --------------------------------------------------------------------------
 // K6: Pi chains on FP64 tensor cores.  CTA = (chunk atom, chain polarity, q,
 // E-chunk); 9 warps, warp w covers a 3x3 block of 8x8 tiles of the
 // [Nw x 2*ncol] real-embedded chain block (rows = frequencies w, columns =
@@ -1076,14 +1216,6 @@ pi_dmma_kernel(PiArgs p, int chunk_atoms) {
 // --------------------------------------------------------------------------
 constexpr int kPi2Slots = 2;
 
-__device__ __forceinline__ double xor_sign(double x, unsigned mask) {
-  unsigned lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
-  asm volatile("xor.b32 %0, %0, %1;" : "+r"(hi) : "r"(mask));
-  double r;
-  asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
-  return r;
-}
 
 // 112 registers: 2 x 9 warps x 32 x 112 = 64.5 K registers per SM
 // A row for invalid (w, E + off_w >= NE) rows: zeros, so the loads need no predicate
@@ -1720,8 +1852,37 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
   return cudaGetLastError();
 }
 
+template <int NO>
+static cudaError_t launch_pi_build_dmma(const PiBuildArgs& a, cudaStream_t st) {
+  const size_t smem = ((size_t)2 * NO * NO * a.nb * 9 + (size_t)a.nb * 3 * NO * NO + (size_t)a.nb * NO * NO) * 16;
+  cudaError_t e = cudaFuncSetAttribute(pi_build_dmma_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPB2Energies - 1) / kPB2Energies);
+  pi_build_dmma_kernel<NO><<<(unsigned)blocks, kPB2Warps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// K5 selection: the DMMA build for No in {4, 8, 12, 16} when its shared memory
+// fits (V image x2 + dH + G2), else (or with SSE_PI_BUILD=0) the DFMA build
+static bool pi_build_dmma_ok(const PiBuildArgs& a) {
+  const char* env = getenv("SSE_PI_BUILD");
+  if (env && env[0] == '0') return false;
+  if (a.no % 4 || a.no > 16) return false;
+  const size_t smem = ((size_t)2 * a.no * a.no * a.nb * 9 + (size_t)a.nb * 4 * a.no * a.no) * 16;
+  return smem <= 220 * 1024;
+}
+
 cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
   if (a.no > kPiMaxNo) return cudaErrorInvalidValue;
+  if (pi_build_dmma_ok(a)) {
+    switch (a.no) {
+      case 4: return launch_pi_build_dmma<4>(a, st);
+      case 8: return launch_pi_build_dmma<8>(a, st);
+      case 12: return launch_pi_build_dmma<12>(a, st);
+      case 16: return launch_pi_build_dmma<16>(a, st);
+      default: break;
+    }
+  }
   const int tpe = a.nb * 3 * a.no;
   const int epg = tpe >= kPiBuildThreads ? 1 : kPiBuildThreads / tpe;
   const size_t smem = (size_t)(3 + epg) * a.nb * a.no * a.no * sizeof(double2);

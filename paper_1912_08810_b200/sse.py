@@ -250,6 +250,8 @@ def sse_phase(
     n_qz: int,
     *,
     n_gpus: int | None = None,
+    device: int | None = None,
+    out=None,
     timing: dict | None = None,
 ):
     """The SSE phase of one Born iteration in one library call.
@@ -265,7 +267,9 @@ def sse_phase(
     gives the same Sigma here (the kernels are arrangement-independent), so
     there is no variant argument.  Returns ``(sigma, pi)``.  Errors as the
     three reference calls (ValueError for inconsistent shapes or a map that
-    is not reverse-closed, device.py:55-57).
+    is not reverse-closed, device.py:55-57).  ``device`` pins the call to one
+    GPU (else ``n_gpus`` devices split the atoms); ``out`` = (Sigma<, Sigma>,
+    Pi<, Pi>) C-contiguous complex128 host arrays (e.g. pinned) to fill.
     """
     if g_e.kind != "electron":
         raise ValueError("sse_sigma expects an electron tensor")
@@ -294,10 +298,16 @@ def sse_phase(
     weights = np.array([float(fmap[w][1]) for w in range(n_w)], dtype=np.float64)
     from .types import SelfEnergyTensor as _SE
 
-    sig_l = np.zeros(g_l.shape, dtype=np.complex128)
-    sig_g = np.zeros(g_l.shape, dtype=np.complex128)
-    pi_l = np.zeros(d_l.shape, dtype=np.complex128)
-    pi_g = np.zeros(d_l.shape, dtype=np.complex128)
+    if out is not None:
+        sig_l, sig_g, pi_l, pi_g = (np.asarray(o) for o in out)
+        for o, shape in ((sig_l, g_l.shape), (sig_g, g_l.shape), (pi_l, d_l.shape), (pi_g, d_l.shape)):
+            if o.shape != shape or o.dtype != np.complex128 or not o.flags.c_contiguous:
+                raise ValueError(f"out arrays must be C-contiguous complex128 of shape {shape}")
+    else:
+        sig_l = np.zeros(g_l.shape, dtype=np.complex128)
+        sig_g = np.zeros(g_l.shape, dtype=np.complex128)
+        pi_l = np.zeros(d_l.shape, dtype=np.complex128)
+        pi_g = np.zeros(d_l.shape, dtype=np.complex128)
     if g_l.size == 0 or d_l.size == 0:
         return _SE(lesser=sig_l, greater=sig_g), _SE(lesser=pi_l, greater=pi_g)
     idx = np.ascontiguousarray(nmap.idx, dtype=np.int64)
@@ -306,7 +316,7 @@ def sse_phase(
     arrays = [_f64(g_l), _f64(g_g), _f64(d_l), _f64(d_g), _f64(dh)]
     dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
     tim = _lib.SseTiming()
-    ctx = _lib.context(n_gpus=n_gpus or _default_gpus())
+    ctx = _lib.context(device=device) if device is not None else _lib.context(n_gpus=n_gpus or _default_gpus())
     rc = _lib.load().sse_phase_c128(
         ctx.handle, ctypes.byref(dims), *[_ptr(a) for a in arrays], _ptr(idx), _ptr(offsets), _ptr(weights),
         float(grid.energy_weight), _ptr(sig_l), _ptr(sig_g), _ptr(pi_l), _ptr(pi_g), ctypes.byref(tim),

@@ -93,6 +93,8 @@ def test_pi_hoisting_is_value_neutral():
     (3, 3, 30, 10, 6, 4, 12),   # the No of the paper configs
     (2, 2, 17, 5, 5, 4, 10),    # No = 10 (small config), 5 atoms (odd) with NB even
     (4, 3, 9, 3, 4, 1, 5),      # NB = 1 (XOR partner slot), Nqz < Nkz
+    (2, 2, 13, 5, 5, 2, 8),     # No = 8 (DMMA operand build), NB = 2
+    (2, 1, 9, 4, 5, 4, 16),     # No = 16 (largest DMMA orbital count)
     (1, 1, 12, 11, 3, 2, 4),    # Nw close to NE (most E + off >= NE terms dropped)
     (2, 2, 7, 3, 4, 2, 1),      # No = 1: one kappa quad, empty second half stage
     (3, 2, 11, 4, 4, 2, 3),     # No = 3: No^2 = 9, ragged last quad
@@ -113,6 +115,11 @@ def test_pi_shapes_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_a, n_b, n
         outs.append(out)
     for o in outs[1:]:
         assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
+    # the DFMA operand build (K5 v1; the DMMA build serves No % 4 == 0)
+    monkeypatch.setenv("SSE_PI_KERNEL", "3")
+    monkeypatch.setenv("SSE_PI_BUILD", "0")
+    out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
+    assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL
 
 
 def test_pi_point_mask_and_atom_range():
