@@ -45,6 +45,16 @@ def k3_kernel_name() -> str:
           "sigma_dmma_slide_kernel<12,12,3> (K3 TMA sliding window, 12 warps x 3 row tiles)")
 
 
+def k6_kernel_name() -> str:
+    """The K6 variant libsse launches for the bench workload (SSE_PI_KERNEL, default 3)."""
+    return {
+        "0": "pi_dmma_direct_kernel (K6 direct)",
+        "1": "pi_dmma_kernel (K6 v1, 2 momenta per CTA)",
+        "2": "pi_dmma2_kernel (K6 v2, half stages)",
+    }.get(os.environ.get("SSE_PI_KERNEL", "3"),
+          "pi_dmma3_kernel (K6 v3: one m-tile x 9 n-tiles per warp, quarter-stage TMA ring of V, 3 CTAs/SM)")
+
+
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -450,7 +460,7 @@ def run_gpu(args, p, grid, idx) -> None:
         pi_info = {
             "s_per_eval": pi_ms / 1e3, "steps": args.pi_steps, "tflops": pi_flops / (pi_ms * 1e-3) / 1e12,
             "flops_alg": pi_flops,
-            "roofline": {"bound": "tensor", "kernel": "pi_dmma_kernel (K6, TMA-staged V operand)",
+            "roofline": {"bound": "tensor", "kernel": k6_kernel_name(),
                          "achieved": k6_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": k6_tflops / FP64_PEAK_TFLOPS},
             "kernels": {k: pprof.result[k] for k in ("pi_build", "pi", "pi_assemble")},
