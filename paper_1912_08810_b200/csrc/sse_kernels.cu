@@ -1421,6 +1421,11 @@ constexpr int kPi3NT = 9;     // n-tiles per warp
 constexpr int kPi3Sub = 6;    // sub-stages per (k, E) stage (6 quads each at No = 12)
 constexpr int kPi3Slots = 4;  // ring slots: the producer runs kPi3Slots - 1 sub-stages ahead
 
+// LAST_PRODUCES: the warp that releases a slot last refills it (a shared-memory
+// counter per slot, atom.inc with wrap-around), so no warp ever blocks on an
+// empty barrier; otherwise lane 0 of warp t % 9 refills slot t after waiting
+// for every warp's release (empty mbarrier).
+template <bool LAST_PRODUCES>
 __global__ void __launch_bounds__(kPiWarps * 32, 3)
 pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1431,6 +1436,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   double2* ring = reinterpret_cast<double2*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPi3Slots * slot_vec + kPi2Pad);
   uint64_t* empty = full + kPi3Slots;
+  unsigned* rel = reinterpret_cast<unsigned*>(empty + kPi3Slots);  // releases per slot
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx = blockIdx.x;
   const int q = bx % p.nqz;
@@ -1451,6 +1457,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
     for (int s = 0; s < kPi3Slots; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, kPiWarps);
+      rel[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1486,7 +1493,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
 
   auto produce = [&](int t) {
     const int slot = t % kPi3Slots;
-    if (t >= kPi3Slots) mbar_wait(empty + slot, (uint32_t)(((t - kPi3Slots) / kPi3Slots) & 1));
+    if (!LAST_PRODUCES && t >= kPi3Slots) mbar_wait(empty + slot, (uint32_t)(((t - kPi3Slots) / kPi3Slots) & 1));
     const int st = t / kPi3Sub, j = t % kPi3Sub;
     const int k = st / ne_c, e = e_lo + st % ne_c;
     const int r0 = min(j * qs * 4, no2), r1 = min((j + 1) * qs * 4, no2);
@@ -1517,7 +1524,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   };
 
   if (threadIdx.x == 0)
-    for (int t = 0; t < kPi3Slots - 1 && t < n_ss; ++t) produce(t);
+    for (int t = 0; t < (LAST_PRODUCES ? kPi3Slots : kPi3Slots - 1) && t < n_ss; ++t) produce(t);
   int k = 0, e = e_lo;
   int kn = 0, en = e_lo + 1;  // next stage
   if (en == e_hi) {
@@ -1530,8 +1537,10 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   int kq = 0, j = 0, slot = 0;
   uint32_t phase = 0;
   for (int ss = 0; ss < n_ss; ++ss) {
-    const int t = ss + kPi3Slots - 1;
-    if (lane == 0 && t < n_ss && t % kPiWarps == warp) produce(t);
+    if (!LAST_PRODUCES) {
+      const int t = ss + kPi3Slots - 1;
+      if (lane == 0 && t < n_ss && t % kPiWarps == warp) produce(t);
+    }
     __syncwarp();  // reconverge before the warp-wide mma.sync
     mbar_wait(full + slot, phase);
     const bool live = active && e + off_min < p.ne;  // warp-uniform
@@ -1565,7 +1574,21 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
       a1 = load_a(kq + 2);
       ++kq;
     }
-    if (lane == 0) mbar_arrive(empty + slot);
+    if (LAST_PRODUCES) {
+      if (lane == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.inc.u32 %0, [%1], %2;"
+                     : "=r"(old)
+                     : "r"(smem_u32(rel + slot)), "r"((unsigned)(kPiWarps - 1))
+                     : "memory");
+        if (old == kPiWarps - 1 && ss + kPi3Slots < n_ss) {  // last release: refill the slot
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          produce(ss + kPi3Slots);
+        }
+      }
+    } else if (lane == 0) {
+      mbar_arrive(empty + slot);
+    }
     if (++slot == kPi3Slots) {
       slot = 0;
       phase ^= 1u;
@@ -1904,7 +1927,7 @@ static size_t pi_smem(int v, int no, int ncol) {
   const int khp = (no * no + 3) / 4;
   if (v == 3)
     return ((size_t)kPi3Slots * 2 * ((khp + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) * 4 * ncol + kPi2Pad) * 16 +
-           2 * kPi3Slots * 8;
+           2 * kPi3Slots * 8 + kPi3Slots * 4;
   if (v == 2) return ((size_t)kPi2Slots * ((khp + 1) / 2) * 4 * ncol + kPi2Pad) * 16 + 2 * kPi2Slots * 8;
   if (v == 1) return (size_t)kPiStages * no * no * ncol * 16 + 2 * kPiStages * 8;
   return 0;
@@ -1929,13 +1952,14 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   switch (v) {
     case 3: {
-      e = cudaFuncSetAttribute(pi_dmma3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess)  // two CTAs per SM need the full shared-memory carveout
-        e = cudaFuncSetAttribute(pi_dmma3_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      const char* pe = getenv("SSE_PI_PRODUCER");  // 1: the last releaser refills (default: round robin)
+      auto kern = (pe && pe[0] == '1') ? pi_dmma3_kernel<true> : pi_dmma3_kernel<false>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)  // several CTAs per SM need the full shared-memory carveout
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
       const int groups = ((a.nw + 7) / 8) * (((2 * a.ncol + 7) / 8 + kPi3NT - 1) / kPi3NT);
-      pi_dmma3_kernel<<<dim3(gx, (unsigned)((groups + kPiWarps - 1) / kPiWarps)), kPiWarps * 32, smem, st>>>(
-          a, chunk_atoms);
+      kern<<<dim3(gx, (unsigned)((groups + kPiWarps - 1) / kPiWarps)), kPiWarps * 32, smem, st>>>(a, chunk_atoms);
       break;
     }
     case 2:

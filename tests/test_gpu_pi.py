@@ -113,6 +113,10 @@ def test_pi_shapes_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_a, n_b, n
         out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
         assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
         outs.append(out)
+    monkeypatch.setenv("SSE_PI_KERNEL", "3")
+    monkeypatch.setenv("SSE_PI_PRODUCER", "1")  # v3 with the last releaser refilling
+    outs.append(sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz))
+    monkeypatch.delenv("SSE_PI_PRODUCER")
     for o in outs[1:]:
         assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
     # the DFMA operand build (K5 v1; the DMMA build serves No % 4 == 0)
