@@ -209,3 +209,21 @@ def _all_to_all(recv, send, recv_sizes, send_sizes, group):
     s = torch.view_as_real(send).reshape(-1) if send.is_complex() else send
     f = 2 if recv.is_complex() else 1
     dist.all_to_all_single(r, s, [x * f for x in recv_sizes], [x * f for x in send_sizes], group=group)
+
+
+def a2a_bytes(idx: np.ndarray, n_kz: int, n_e: int, n_o: int, world: int, rank: int,
+              polarities: int = 2) -> dict:
+    """Bytes rank ``rank`` receives in the two all-to-alls of one SSE step (G in, Sigma back).
+
+    Own rows are included (they are copied, not sent), matching the reference's
+    model that counts a process's whole window (comm.dace_volume, comm.py:86-106).
+    """
+    blk = n_o * n_o * 16 * polarities
+    pts = point_chunks(n_kz, n_e, world)
+    slabs = _slabs(idx, world)
+    lo, hi, glo, ghi = slabs[rank]
+    ps, pe = pts[rank]
+    g_in = n_kz * n_e * (ghi - glo) * blk
+    sigma_in = (pe - ps) * idx.shape[0] * blk
+    return {"g_in": g_in, "sigma_back": sigma_in,
+            "g_in_from_peers": g_in - (pe - ps) * (ghi - glo) * blk}

@@ -175,3 +175,34 @@ def test_gf_points_to_atom_slabs_all_to_all(world):
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert all(f and b for f, b in res), res
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_a2a_bytes_within_reference_tiled_model(world):
+    """the all-to-all volume against the reference's tiled model with T_E = 1, T_A = P
+    (comm.dace_volume, comm.py:86-106: 32 Nkz (NE/T_E + 2 Nw)(NA/T_A + NB) No^2 bytes per direction)."""
+    from paper_1912_08810_b200.inputs import config
+
+    p, grid, nmap = config("paper")
+    model = 32 * p.n_kz * (p.n_E + 2 * p.n_w) * (p.n_A / world + p.n_B) * p.n_orb**2
+    for rank in range(world):
+        b = sdist.a2a_bytes(nmap.idx, p.n_kz, p.n_E, p.n_orb, world, rank)
+        assert b["g_in"] <= model
+        assert b["sigma_back"] <= model
+    ref = "/root/reference/pkg/src"
+    if os.path.isdir(ref):
+        import sys
+
+        sys.path.insert(0, ref)
+        try:
+            from negflow import comm
+            from negflow.params import SimParams as RefParams
+
+            rp = RefParams(n_kz=p.n_kz, n_qz=p.n_qz, n_E=p.n_E, n_w=p.n_w, n_A=p.n_A, n_B=p.n_B,
+                           n_orb=p.n_orb, bnum=p.bnum)
+            plan = comm.dace_volume(rp, 1, world)
+            assert abs(plan.per_process_bytes[comm.ELECTRON_G] - model) <= 1e-6 * model
+            if world > 1:
+                assert comm.optimize_tiles(rp, world).t_e == 1  # the tiling this all-to-all implements
+        finally:
+            sys.path.remove(ref)

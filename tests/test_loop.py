@@ -136,3 +136,23 @@ def test_sse_phase_rejects_non_reverse_closed_map():
                       frequency_map=tuple(zip(c.offsets.tolist(), c.weights.tolist())), energy_weight=0.1)
     with pytest.raises(ValueError, match="missing neighbor slot"):
         sse_phase(GreensTensor(c.g_l, c.g_g), GreensTensor(c.d_l, c.d_g), c.dh, NeighborMap(idx), grid, c.p.n_qz)
+
+
+@pytest.mark.gpu
+def test_sse_phase_multi_gpu_bitwise():
+    """Atoms split over 2 devices of the process (each device reads its own halo)."""
+    import torch
+
+    from paper_1912_08810_b200.sse import sse_phase
+    from tests.golden_cases import load_case
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    c = load_case("orb12_s5")
+    grid = EnergyGrid(values=tuple(np.linspace(-1, 1, c.p.n_E)),
+                      frequency_map=tuple(zip(c.offsets.tolist(), c.weights.tolist())), energy_weight=0.01)
+    args = (GreensTensor(c.g_l, c.g_g), GreensTensor(c.d_l, c.d_g), c.dh, NeighborMap(c.idx), grid, c.p.n_qz)
+    s1, p1 = sse_phase(*args, n_gpus=1)
+    s2, p2 = sse_phase(*args, n_gpus=2)
+    for a, b in ((s1, s2), (p1, p2)):
+        assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
