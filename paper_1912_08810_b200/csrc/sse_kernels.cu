@@ -1425,13 +1425,20 @@ constexpr int kPi3Slots = 4;  // ring slots: the producer runs kPi3Slots - 1 sub
 // counter per slot, atom.inc with wrap-around), so no warp ever blocks on an
 // empty barrier; otherwise lane 0 of warp t % 9 refills slot t after waiting
 // for every warp's release (empty mbarrier).
-template <bool LAST_PRODUCES>
+// NOT/NBT > 0: No and NB fixed at compile time (the paper shapes), so every
+// sub-stage is a fixed, fully unrolled run of quad pairs with no branches.
+template <bool LAST_PRODUCES, int NOT, int NBT>
 __global__ void __launch_bounds__(kPiWarps * 32, 3)
 pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int no2 = p.no * p.no, ncol = p.ncol;
+  const int no = NOT > 0 ? NOT : p.no;
+  const int no2 = no * no, ncol = NBT > 0 ? 9 * NBT : p.ncol;
   const int khp = (no2 + 3) / 4;                     // kappa quads per stage (>= 2 here)
   const int qs = 2 * ((khp + 2 * kPi3Sub - 1) / (2 * kPi3Sub));  // quads per sub-stage (even)
+  // compile-time: every sub-stage holds exactly qs quads (qs even, khp % qs == 0)
+  constexpr int KHP_T = NOT > 0 ? (NOT * NOT + 3) / 4 : 0;
+  constexpr int QS_T = NOT > 0 ? 2 * ((KHP_T + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) : 0;
+  constexpr bool UNIFORM = NOT > 0 && NBT > 0 && KHP_T % QS_T == 0 && KHP_T / QS_T == kPi3Sub;
   const int slot_vec = qs * 4 * ncol;                // double2 per slot
   double2* ring = reinterpret_cast<double2*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPi3Slots * slot_vec + kPi2Pad);
@@ -1561,14 +1568,33 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
 #pragma unroll
       for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[u], a.y, bi[u]);
     };
-    for (; kq + 1 < kq1; kq += 2) {
-      if (live) quad(a0, sb);
-      a0 = load_a(kq + 2);
-      if (live) quad(a1, sb + 8 * ncol);
-      a1 = load_a(kq + 3);
-      sb += 16 * ncol;
+    if constexpr (UNIFORM) {
+      if (live) {
+#pragma unroll
+        for (int pr = 0; pr < QS_T / 2; ++pr) {
+          quad(a0, sb + 16 * pr * ncol);
+          a0 = load_a(kq + 2 * pr + 2);
+          quad(a1, sb + (16 * pr + 8) * ncol);
+          a1 = load_a(kq + 2 * pr + 3);
+        }
+      } else {
+#pragma unroll
+        for (int pr = 0; pr < QS_T / 2; ++pr) {
+          a0 = load_a(kq + 2 * pr + 2);
+          a1 = load_a(kq + 2 * pr + 3);
+        }
+      }
+      kq += QS_T;
+    } else {
+      for (; kq + 1 < kq1; kq += 2) {
+        if (live) quad(a0, sb);
+        a0 = load_a(kq + 2);
+        if (live) quad(a1, sb + 8 * ncol);
+        a1 = load_a(kq + 3);
+        sb += 16 * ncol;
+      }
     }
-    if (kq < kq1) {  // odd tail
+    if (!UNIFORM && kq < kq1) {  // odd tail
       if (live) quad(a0, sb);
       a0 = a1;
       a1 = load_a(kq + 2);
@@ -1953,7 +1979,10 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
   switch (v) {
     case 3: {
       const char* pe = getenv("SSE_PI_PRODUCER");  // 1: the last releaser refills (default: round robin)
-      auto kern = (pe && pe[0] == '1') ? pi_dmma3_kernel<true> : pi_dmma3_kernel<false>;
+      const bool last = pe && pe[0] == '1';
+      const bool fixed = a.no == 12 && a.nb == 4;    // the paper shapes: unrolled sub-stages
+      auto kern = fixed ? (last ? pi_dmma3_kernel<true, 12, 4> : pi_dmma3_kernel<false, 12, 4>)
+                        : (last ? pi_dmma3_kernel<true, 0, 0> : pi_dmma3_kernel<false, 0, 0>);
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e == cudaSuccess)  // several CTAs per SM need the full shared-memory carveout
         e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
