@@ -53,13 +53,17 @@ def test_library_is_sm100a_only():
     ("_ZN3sse22sigma_dmma_pipe_kernelILi12EEEvNS_9SigmaArgsE", 108),  # production K3 (2 stages x 54)
     ("_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", 54),        # simple K3
     ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELi3EEEvNS_9SigmaArgsE", 54),  # TMA sliding-window K3
+    ("_ZN3sse15pi_dmma3_kernelILb0ELi12ELi4EEEvNS_6PiArgsEi", 108),            # Pi K6 v3 (paper shapes)
+    ("_ZN3sse20pi_build_dmma_kernelILi12EEEvNS_11PiBuildArgsE", 72),            # Pi K5 v2
 ])
 def test_fp64_tensor_core_sass_present(kernel, dmma):
-    """The Sigma kernels issue DMMA.8x8x4 (FP64 tensor cores), not a CPU/DFMA fallback."""
+    """The Sigma / Pi kernels issue DMMA.8x8x4 (FP64 tensor cores), not a CPU/DFMA fallback."""
     out = subprocess.run(["cuobjdump", "-sass", "-fun", kernel, _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert out.count("DMMA.8x8x4") >= dmma
-    if "slide" in kernel:  # operands staged by the TMA engine (bulk async copies + mbarriers)
-        assert "UBLKCP" in out and "SYNCS" in out
+    if "slide" in kernel or "pi_dmma3" in kernel:  # operands staged by the TMA engine (bulk copies + mbarriers)
+        assert "UBLKCP.S.G" in out and "SYNCS" in out
+    if "pi_build" in kernel:  # V written by a bulk async store (shared -> global)
+        assert "UBLKCP.G.S" in out
 
 
 def test_version_and_no_cpu_fallback():
@@ -116,3 +120,22 @@ def test_types_mirror_reference_validation():
         NeighborMap(np.zeros((2, 2)))
     with pytest.raises(ValueError, match="outside"):
         EnergyGrid(values=(0.0, 1.0), frequency_map=((2, 1.0),), energy_weight=1.0)
+
+
+def test_sse_phase_argument_errors():
+    """The fused SSE phase validates like the three reference calls, before any device work."""
+    from paper_1912_08810_b200.sse import sse_phase
+
+    p, g, dc, dh, nmap, grid = _instance()
+    rng = np.random.default_rng(1)
+    ph = GreensTensor(rng.standard_normal(p.phonon_shape) + 0j, rng.standard_normal(p.phonon_shape) + 0j)
+    with pytest.raises(ValueError, match="expects an electron tensor"):
+        sse_phase(ph, ph, dh, nmap, grid, p.n_qz)
+    with pytest.raises(ValueError, match="phonon"):
+        sse_phase(g, g, dh, nmap, grid, p.n_qz)
+    with pytest.raises(ValueError, match="momenta"):
+        sse_phase(g, ph, dh, nmap, grid, p.n_qz + 1)
+    with pytest.raises(ValueError, match="dH must have shape"):
+        sse_phase(g, ph, dh[:, :1], nmap, grid, p.n_qz)
+    with pytest.raises(ValueError, match="out arrays"):
+        sse_phase(g, ph, dh, nmap, grid, p.n_qz, out=(np.zeros(3),) * 4)
