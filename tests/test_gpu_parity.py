@@ -132,17 +132,19 @@ def test_all_sigma_kernels_bitwise(monkeypatch, name):
     assert dev <= TOL
 
 
-@pytest.mark.parametrize("n_e, n_w, n_o, n_a", [
-    (24, 6, 12, 10),    # the smoke shape: 6 offsets < 12 ring stages (pipelined fallback)
-    (48, 12, 12, 6),    # sliding-window kernel, one CTA tile, segments of exactly 12 stages
-    (64, 20, 12, 5),    # sliding-window kernel, two CTA tiles, window clipped at E = 0
-    (40, 13, 10, 6),    # No = 10 (padded DMMA embedding; ring too large: pipelined kernel)
-    (31, 16, 4, 7),     # No = 4, ragged last tile
+@pytest.mark.parametrize("n_e, n_w, n_o, n_a, n_b", [
+    (24, 6, 12, 10, 4),    # the smoke shape: 6 offsets < 12 ring stages (pipelined fallback)
+    (48, 12, 12, 6, 4),    # sliding-window kernel, one CTA tile, segments of exactly 12 stages
+    (64, 20, 12, 5, 4),    # sliding-window kernel, two CTA tiles, window clipped at E = 0
+    (40, 13, 10, 6, 4),    # No = 10 (padded DMMA embedding; ring too large: pipelined kernel)
+    (31, 16, 4, 7, 4),     # No = 4, ragged last tile
+    (30, 14, 12, 9, 6),    # NB = 6 neighbour slots
+    (20, 13, 17, 5, 2),    # No = 17 > 16: the DFMA kernel (K3g)
 ])
-def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a):
+def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a, n_b):
     """Shapes that exercise the K3 ring/window logic, checked against the oracle
     (pinned to the reference by tests/test_oracle.py) for every kernel choice."""
-    p = SimParams(n_kz=3, n_qz=2, n_E=n_e, n_w=n_w, n_A=n_a, n_B=4, n_orb=n_o)
+    p = SimParams(n_kz=3, n_qz=2, n_E=n_e, n_w=n_w, n_A=n_a, n_B=n_b, n_orb=n_o)
     g_l, g_g, d_l, d_g, dh = inputs.stream_instance(11, p, dh_scale=0.05)
     nmap = build_neighbor_map(p.n_A, p.n_B)
     grid = default_grid(p)

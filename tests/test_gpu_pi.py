@@ -95,6 +95,8 @@ def test_pi_hoisting_is_value_neutral():
     (4, 3, 9, 3, 4, 1, 5),      # NB = 1 (XOR partner slot), Nqz < Nkz
     (2, 2, 13, 5, 5, 2, 8),     # No = 8 (DMMA operand build), NB = 2
     (2, 1, 9, 4, 5, 4, 16),     # No = 16 (largest DMMA orbital count)
+    (1, 1, 80, 75, 3, 2, 4),    # Nw = 75: 10 lag tiles (two warp groups per CTA column)
+    (2, 2, 9, 3, 14, 6, 4),     # NB = 6: 54 chains, 14 real n-tiles (two n-groups in K6 v3)
     (1, 1, 12, 11, 3, 2, 4),    # Nw close to NE (most E + off >= NE terms dropped)
     (2, 2, 7, 3, 4, 2, 1),      # No = 1: one kappa quad, empty second half stage
     (3, 2, 11, 4, 4, 2, 3),     # No = 3: No^2 = 9, ragged last quad
