@@ -789,21 +789,42 @@ pi_build_dmma_kernel(PiBuildArgs p) {
   const unsigned neg = im ? 0u : 0x80000000u;      // the im-row of a real column is -Im
   const int kl = lane & 3;
   const int tasks = nb * MT;
+  // G2 blocks of (point e, chain polarity pol): element x = (s, rr); the next
+  // step's first kPB2Prefetch * blockDim elements are loaded into registers
+  // while the current step multiplies (the rest, if any, synchronously)
+  constexpr int kPB2Prefetch = 2;
+  auto g2_elem = [&](int e_, int pol_, int x) -> double2 {
+    if (p.mask && !p.mask[k * p.ne + e_]) return make_double2(0.0, 0.0);
+    const double2* G2 = pol_ ? p.G[0] : p.G[1];  // chain pol 0 (lesser): G2 = G>; pol 1: G2 = G<
+    const int ss = x / NO2, rr = x % NO2;
+    const long long lb = p.nbr[la * nb + ss];
+    return G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e_ * p.g_se + rr];
+  };
+  double2 pf[kPB2Prefetch];
+  auto fetch = [&](int e_, int pol_) {
+#pragma unroll
+    for (int i = 0; i < kPB2Prefetch; ++i) {
+      const int x = threadIdx.x + i * blockDim.x;
+      pf[i] = x < nb * NO2 ? g2_elem(e_, pol_, x) : make_double2(0.0, 0.0);
+    }
+  };
+  if (e0 < e1) fetch(e0, 0);
   int step = 0;  // (point, polarity) counter: buffer = step & 1
   for (int e = e0; e < e1; ++e) {
-    const bool masked = p.mask && !p.mask[k * p.ne + e];
     for (int pol = 0; pol < 2; ++pol, ++step) {
       double2* buf = vt + (step & 1) * vt_vec;
-      const double2* G2 = pol ? p.G[0] : p.G[1];  // chain pol 0 (lesser): G2 = G>; pol 1: G2 = G<
       __syncthreads();  // sg2 / buf readers of the previous steps are done
       if (threadIdx.x == 0 && step >= 2) bulk_wait_read<1>();  // buf's store (two steps ago) has read it
-      for (int x = threadIdx.x; x < nb * NO2; x += blockDim.x) {
-        const int ss = x / NO2, rr = x % NO2;
-        const long long lb = p.nbr[la * nb + ss];
-        sg2[x] = masked ? make_double2(0.0, 0.0)
-                        : G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e * p.g_se + rr];
+#pragma unroll
+      for (int i = 0; i < kPB2Prefetch; ++i) {
+        const int x = threadIdx.x + i * blockDim.x;
+        if (x < nb * NO2) sg2[x] = pf[i];
       }
+      for (int x = threadIdx.x + kPB2Prefetch * blockDim.x; x < nb * NO2; x += blockDim.x)
+        sg2[x] = g2_elem(e, pol, x);
       __syncthreads();
+      if (pol == 0) fetch(e, 1);
+      else if (e + 1 < e1) fetch(e + 1, 0);
       for (int task = warp; task < tasks; task += kPB2Warps) {
         const int ss = task / MT, mt = task % MT;
         const int m = mt * 8 + (lane >> 2);
