@@ -51,8 +51,9 @@ def k6_kernel_name() -> str:
         "0": "pi_dmma_direct_kernel (K6 direct)",
         "1": "pi_dmma_kernel (K6 v1, 2 momenta per CTA)",
         "2": "pi_dmma2_kernel (K6 v2, half stages)",
-    }.get(os.environ.get("SSE_PI_KERNEL", "3"),
-          "pi_dmma3_kernel (K6 v3: one m-tile x 9 n-tiles per warp, quarter-stage TMA ring of V, 3 CTAs/SM)")
+        "3": "pi_dmma3_kernel (K6 v3: one m-tile x 9 n-tiles per warp, TMA ring of V, 3 CTAs/SM)",
+    }.get(os.environ.get("SSE_PI_KERNEL", "4"),
+          "pi_dmma4_kernel<12,4> (K6 v4: two m-tiles x 9 n-tiles per warp, TMA ring of V, 3 CTAs/SM)")
 
 
 def env_rank():

@@ -1666,6 +1666,231 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
 }
 
 // --------------------------------------------------------------------------
+// K6 v4 (fixed shapes No = 12, NB = 4): as v3 but each warp owns TWO 8-lag
+// m-tiles (5 warps per CTA for 9 lag tiles), so every B value read from shared
+// memory feeds two DMMAs (v3: one); the last warp of an odd tile count runs
+// the one-tile path.  Same per-output accumulation order (bitwise equal).
+// --------------------------------------------------------------------------
+constexpr int kPi4Warps = 5;
+
+template <int NOT, int NBT>
+__global__ void __launch_bounds__(kPi4Warps * 32, 3)
+pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
+  constexpr int NO2 = NOT * NOT, NCOL = 9 * NBT;
+  constexpr int KHP = (NO2 + 3) / 4;
+  constexpr int QS = 2 * ((KHP + 2 * kPi3Sub - 1) / (2 * kPi3Sub));
+  static_assert(NO2 % 4 == 0 && KHP % QS == 0 && KHP / QS == kPi3Sub && 2 * NCOL <= 8 * kPi3NT,
+                "fixed-shape K6 v4 needs whole quads, uniform sub-stages and <= 9 n-tiles");
+  constexpr int SLOT = QS * 4 * NCOL;  // double2 per slot
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPi3Slots * SLOT + kPi2Pad);
+  uint64_t* empty = full + kPi3Slots;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bx = blockIdx.x;
+  const int q = bx % p.nqz;
+  bx /= p.nqz;
+  const int ec = bx % p.echunks;
+  bx /= p.echunks;
+  const int pol = bx % 2;
+  const int la = bx / 2;
+  const int m_tiles = (p.nw + 7) / 8;
+  const int wg = blockIdx.y * kPi4Warps + warp;
+  const int mt0 = 2 * wg;
+  const bool active = mt0 < m_tiles;
+  const bool two = mt0 + 1 < m_tiles;  // warp-uniform
+  const int pcol = lane & 3;
+
+  for (int i = threadIdx.x; i < kPi3Slots * SLOT + kPi2Pad; i += blockDim.x) ring[i] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPi3Slots; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kPi4Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  const double2* __restrict__ G1 = pol ? p.G[1] : p.G[0];
+  const double2* __restrict__ VT = (pol ? p.VT[1] : p.VT[0]) + (long long)la * p.nkz * p.ne * NO2 * NCOL;
+  const double2* g_atom = G1 + (p.g_atom_of_chunk0 + la) * p.g_sa;
+
+  int w[2], off[2];
+  bool row_ok[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    w[t] = (mt0 + t) * 8 + (lane >> 2);
+    row_ok[t] = active && w[t] < p.nw;
+    off[t] = row_ok[t] ? __ldg(p.off + w[t]) : 0;
+  }
+  int off_min = row_ok[0] ? off[0] : (1 << 30);
+  if (row_ok[1]) off_min = min(off_min, off[1]);
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
+  const int nc0 = lane >> 2;
+  const int im = nc0 & 1;
+  const int b_off = 2 * ((nc0 >> 1) ^ (((pcol >> 1) & 1) ? p.swz : 0)) + im;
+  const int b_dim = im ? -1 : 1;
+  const unsigned b_mask = im ? 0u : 0x80000000u;
+
+  double acc[2][kPi3NT][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+
+  const int e_lo = ec * p.e_per_chunk, e_hi = min(p.ne, e_lo + p.e_per_chunk);
+  const int ne_c = e_hi - e_lo;
+  const int n_st = p.nkz * ne_c;
+  const int n_ss = kPi3Sub * n_st;
+
+  auto produce = [&](int t) {
+    const int slot = t % kPi3Slots;
+    if (t >= kPi3Slots) mbar_wait(empty + slot, (uint32_t)(((t - kPi3Slots) / kPi3Slots) & 1));
+    const int st = t / kPi3Sub, j = t % kPi3Sub;
+    const int k = st / ne_c, e = e_lo + st % ne_c;
+    constexpr uint32_t bytes = (uint32_t)SLOT * 16;
+    mbar_arrive_expect_tx(full + slot, bytes);
+    bulk_g2s(ring + slot * SLOT, VT + (((long long)k * p.ne + e) * NO2 + j * QS * 4) * NCOL, bytes, full + slot);
+  };
+  auto row_of = [&](int t, int k, int e) -> const double2* {
+    int kp = k + q;
+    if (kp >= p.nkz) kp -= p.nkz;
+    return (row_ok[t] && e + off[t] < p.ne)
+               ? g_atom + (long long)kp * p.g_sk + (long long)(e + off[t]) * p.g_se + pcol
+               : kPiZeroRow + pcol;
+  };
+  const double2 *cur[2], *nxt[2];
+  auto load_a = [&](int t, int kq) -> double2 {
+    const double2* r = kq < KHP ? cur[t] : nxt[t];
+    const int qq = kq < KHP ? kq : kq - KHP;
+    return __ldg(r + qq * 4);
+  };
+
+  if (threadIdx.x == 0)
+    for (int t = 0; t < kPi3Slots - 1 && t < n_ss; ++t) produce(t);
+  int k = 0, e = e_lo;
+  int kn = 0, en = e_lo + 1;
+  if (en == e_hi) {
+    en = e_lo;
+    ++kn;
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    cur[t] = row_of(t, k, e);
+    nxt[t] = n_st > 1 ? row_of(t, kn, en) : cur[t];
+  }
+  double2 a0[2], a1[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    a0[t] = load_a(t, 0);
+    a1[t] = load_a(t, 1);
+  }
+  int kq = 0, j = 0, slot = 0;
+  uint32_t phase = 0;
+  // one quad: B read once per n-tile, used by both m-tiles (T = tiles in use)
+  auto quad2 = [&](const double2 (&a)[2], const double* b) {
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) {
+      const double br = b[8 * u];
+      dmma884_nv(acc[0][u], a[0].x, br);
+      dmma884_nv(acc[1][u], a[1].x, br);
+    }
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) {
+      const double bi = xor_sign(b[8 * u + b_dim], b_mask);
+      dmma884_nv(acc[0][u], a[0].y, bi);
+      dmma884_nv(acc[1][u], a[1].y, bi);
+    }
+  };
+  auto quad1 = [&](const double2 (&a)[2], const double* b) {
+    double br[kPi3NT], bi[kPi3NT];
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) {
+      br[u] = b[8 * u];
+      bi[u] = xor_sign(b[8 * u + b_dim], b_mask);
+    }
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[0][u], a[0].x, br[u]);
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[0][u], a[0].y, bi[u]);
+  };
+  for (int ss = 0; ss < n_ss; ++ss) {
+    const int t = ss + kPi3Slots - 1;
+    if (lane == 0 && t < n_ss && t % kPi4Warps == warp) produce(t);
+    __syncwarp();
+    mbar_wait(full + slot, phase);
+    const bool live = active && e + off_min < p.ne;
+    const double* sb = reinterpret_cast<const double*>(ring + slot * SLOT) + pcol * 2 * NCOL + b_off;
+    if (live && two) {
+#pragma unroll
+      for (int pr = 0; pr < QS / 2; ++pr) {
+        quad2(a0, sb + 16 * pr * NCOL);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) a0[tt] = load_a(tt, kq + 2 * pr + 2);
+        quad2(a1, sb + (16 * pr + 8) * NCOL);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) a1[tt] = load_a(tt, kq + 2 * pr + 3);
+      }
+    } else if (live) {
+#pragma unroll
+      for (int pr = 0; pr < QS / 2; ++pr) {
+        quad1(a0, sb + 16 * pr * NCOL);
+        a0[0] = load_a(0, kq + 2 * pr + 2);
+        quad1(a1, sb + (16 * pr + 8) * NCOL);
+        a1[0] = load_a(0, kq + 2 * pr + 3);
+      }
+    } else {
+#pragma unroll
+      for (int pr = 0; pr < QS / 2; ++pr) {
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          a0[tt] = load_a(tt, kq + 2 * pr + 2);
+          a1[tt] = load_a(tt, kq + 2 * pr + 3);
+        }
+      }
+    }
+    kq += QS;
+    if (lane == 0) mbar_arrive(empty + slot);
+    if (++slot == kPi3Slots) {
+      slot = 0;
+      phase ^= 1u;
+    }
+    if (++j == kPi3Sub) {
+      j = 0;
+      kq -= KHP;
+      k = kn;
+      e = en;
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) cur[tt] = nxt[tt];
+      if (++en == e_hi) {
+        en = e_lo;
+        ++kn;
+      }
+      if (ss + 1 + kPi3Sub < n_ss) {
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) nxt[tt] = row_of(tt, kn, en);
+      }
+    }
+  }
+
+  if (!active) return;
+  double2* part = p.partial + ((((long long)la * 2 + pol) * p.nqz + q) * p.echunks + ec) * p.nw * NCOL;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    if (!row_ok[t]) continue;
+#pragma unroll
+    for (int u = 0; u < kPi3NT; ++u) {
+      const int c = u * 4 + (lane & 3);
+      if (c < NCOL)
+        part[(long long)w[t] * NCOL + c] =
+            make_double2(p.energy_weight * acc[t][u][0], p.energy_weight * acc[t][u][1]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // K7: Pi assembly (sse.py:393-406): chain = sum of the E-chunk partials in
 // order; Pi[q,w,a,1+s] = i chain_s, Pi[q,w,a,0] = -i sum_s chain_s.
 // --------------------------------------------------------------------------
@@ -1972,6 +2197,7 @@ cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
 // back to the next one.  All accumulate in the same order (bitwise equal).
 static size_t pi_smem(int v, int no, int ncol) {
   const int khp = (no * no + 3) / 4;
+  if (v == 4) v = 3;  // same ring as v3
   if (v == 3)
     return ((size_t)kPi3Slots * 2 * ((khp + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) * 4 * ncol + kPi2Pad) * 16 +
            2 * kPi3Slots * 8 + kPi3Slots * 4;
@@ -1981,23 +2207,34 @@ static size_t pi_smem(int v, int no, int ncol) {
 }
 static int pi_kernel_choice(int no, int ncol) {
   const char* env = getenv("SSE_PI_KERNEL");
-  int v = (env && env[0] >= '0' && env[0] <= '3') ? env[0] - '0' : 3;
+  int v = (env && env[0] >= '0' && env[0] <= '4') ? env[0] - '0' : 4;
+  if (v == 4 && !(no == 12 && ncol == 36)) v = 3;  // v4 exists for the paper shapes only
   if (v == 3 && (no * no + 3) / 4 < 2) v = 2;
   while (v > 0 && pi_smem(v, no, ncol) > 220 * 1024) --v;
   return v;
 }
 // column swizzle of V rows for K6 v3 (conflict-free B reads): column c of
 // kappa row r is stored at c ^ (2 * ((r >> 1) & 1)); needs ncol % 4 == 0
-int pi_vt_swizzle(int no, int ncol) { return (pi_kernel_choice(no, ncol) == 3 && ncol % 4 == 0) ? 2 : 0; }
+int pi_vt_swizzle(int no, int ncol) { return (pi_kernel_choice(no, ncol) >= 3 && ncol % 4 == 0) ? 2 : 0; }
 
 cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
   const int v = pi_kernel_choice(a.no, a.ncol);
-  if (a.swz != (v == 3 && a.ncol % 4 == 0 ? 2 : 0)) return cudaErrorInvalidValue;  // K5 / K6 disagree
+  if (a.swz != (v >= 3 && a.ncol % 4 == 0 ? 2 : 0)) return cudaErrorInvalidValue;  // K5 / K6 disagree
   const size_t smem = pi_smem(v, a.no, a.ncol);
   const unsigned gy = (unsigned)((a.warp_groups + kPiWarps - 1) / kPiWarps);
   const unsigned gx = (unsigned)((long long)chunk_atoms * 2 * a.echunks * a.nqz);
   cudaError_t e = cudaSuccess;
   switch (v) {
+    case 4: {
+      e = cudaFuncSetAttribute(pi_dmma4_kernel<12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(pi_dmma4_kernel<12, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+      const int pairs = ((a.nw + 7) / 8 + 1) / 2;
+      pi_dmma4_kernel<12, 4><<<dim3(gx, (unsigned)((pairs + kPi4Warps - 1) / kPi4Warps)), kPi4Warps * 32, smem, st>>>(
+          a, chunk_atoms);
+      break;
+    }
     case 3: {
       const char* pe = getenv("SSE_PI_PRODUCER");  // 1: the last releaser refills (default: round robin)
       const bool last = pe && pe[0] == '1';

@@ -110,7 +110,7 @@ def test_pi_shapes_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_a, n_b, n
     ch_l, ch_g = orc.pi_chains(g_l, g_g, dh, nmap.idx, np.array(grid.offsets), grid.energy_weight, n_qz)
     ref_l, ref_g = orc.pi_from_chains(ch_l, ch_g)
     outs = []
-    for choice in ("3", "2", "1", "0"):
+    for choice in ("4", "3", "2", "1", "0"):
         monkeypatch.setenv("SSE_PI_KERNEL", choice)
         out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
         assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
