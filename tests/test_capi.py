@@ -54,13 +54,14 @@ def test_library_is_sm100a_only():
     ("_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", 54),        # simple K3
     ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELi3EEEvNS_9SigmaArgsE", 54),  # TMA sliding-window K3
     ("_ZN3sse15pi_dmma3_kernelILb0ELi12ELi4EEEvNS_6PiArgsEi", 108),            # Pi K6 v3 (paper shapes)
+    ("_ZN3sse15pi_dmma4_kernelILi12ELi4EEEvNS_6PiArgsEi", 216),                # Pi K6 v4 (default, paper)
     ("_ZN3sse20pi_build_dmma_kernelILi12EEEvNS_11PiBuildArgsE", 72),            # Pi K5 v2
 ])
 def test_fp64_tensor_core_sass_present(kernel, dmma):
     """The Sigma / Pi kernels issue DMMA.8x8x4 (FP64 tensor cores), not a CPU/DFMA fallback."""
     out = subprocess.run(["cuobjdump", "-sass", "-fun", kernel, _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert out.count("DMMA.8x8x4") >= dmma
-    if "slide" in kernel or "pi_dmma3" in kernel:  # operands staged by the TMA engine (bulk copies + mbarriers)
+    if "slide" in kernel or "pi_dmma3" in kernel or "pi_dmma4" in kernel:  # operands staged by the TMA engine (bulk copies + mbarriers)
         assert "UBLKCP.S.G" in out and "SYNCS" in out
     if "pi_build" in kernel:  # V written by a bulk async store (shared -> global)
         assert "UBLKCP.G.S" in out
