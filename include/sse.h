@@ -143,6 +143,30 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
                 const double* dH, const int64_t* nmap, const int64_t* off,
                 double energy_weight, const unsigned char* mask, int64_t atom_lo,
                 int64_t atom_hi, double* Pi_l, double* Pi_g, sse_timing* t);
+/* The same with the Sigma blocks scattered straight into the (k,E)-point layout
+ * buffers of the point owners (the GF phase's layout, the tiled
+ * scheme's return round distsim.py:300-315, here fused into the kernel's
+ * epilogue as NVLink peer stores).  Rank r owns flattened points
+ * [pt_lo[r], pt_lo[r+1]) (pt = k*NE + E, pt_lo[0] = 0, pt_lo[nranks] = Nkz*NE);
+ * its buffers S_l[r] / S_g[r] are [pt_lo[r+1]-pt_lo[r], NA, No, No] device
+ * pointers valid in this process (own allocation or sse_ipc_open).  The
+ * caller synchronises the ranks before the owners read.  nranks <= 8. */
+int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
+                             const sse_slab* out, const double* G_l, const double* G_g,
+                             const double* Dc_l, const double* Dc_g, const double* dH,
+                             const int64_t* nmap, const int64_t* off, const double* wt,
+                             int nranks, const int64_t* pt_lo, double* const* S_l,
+                             double* const* S_g, void* stream, sse_timing* t);
+
+/* Library-owned device memory that can be shared with peer processes, and CUDA
+ * IPC export / import of it (handles are SSE_IPC_HANDLE_BYTES opaque bytes). */
+#define SSE_IPC_HANDLE_BYTES 64
+int sse_dev_alloc(sse_ctx* ctx, size_t bytes, void** out);
+int sse_dev_free(sse_ctx* ctx, void* ptr);
+int sse_ipc_handle(sse_ctx* ctx, void* dptr, unsigned char* handle);
+int sse_ipc_open(sse_ctx* ctx, const unsigned char* handle, void** out);
+int sse_ipc_close(sse_ctx* ctx, void* ptr);
+
 /* Device-resident Pi of an owned atom range: g = slab with the owned atoms and
  * all their neighbours; dH [out.natoms, NB, 3, No, No]; nmap HOST [out.natoms, NB]
  * (global ids); Pi_* device [Nqz, Nw, out.natoms, NB+1, 3, 3]. */

@@ -14,6 +14,7 @@ import threading
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsse.so")
 
 SSE_OK, SSE_EINVAL, SSE_ECUDA, SSE_ECOMM, SSE_ENOMEM = 0, 1, 2, 3, 4
+IPC_HANDLE_BYTES = 64
 
 # Exported symbols, exactly those declared in include/sse.h.
 EXPORTED = (
@@ -25,6 +26,12 @@ EXPORTED = (
     "sse_sigma_c128",
     "sse_sigma_c128_slab",
     "sse_sigma_device",
+    "sse_sigma_device_scatter",
+    "sse_dev_alloc",
+    "sse_dev_free",
+    "sse_ipc_handle",
+    "sse_ipc_open",
+    "sse_ipc_close",
     "sse_pi_c128",
     "sse_pi_device",
     "sse_phase_c128",
@@ -119,6 +126,12 @@ def load() -> ctypes.CDLL:
         lib.sse_profile_begin.argtypes = [_P]
         lib.sse_profile_end.argtypes = [_P, ctypes.POINTER(SseProfile)]
         lib.sse_sigma_device.argtypes = [_P, pdims, pslab, pslab] + [_P] * 6 + [_P, _P, _P, _P, _P, ptim]
+        lib.sse_sigma_device_scatter.argtypes = [_P, pdims, pslab, pslab] + [_P] * 8 + [i32, _P, _P, _P, _P, ptim]
+        lib.sse_dev_alloc.argtypes = [_P, ctypes.c_size_t, ctypes.POINTER(_P)]
+        lib.sse_dev_free.argtypes = [_P, _P]
+        lib.sse_ipc_handle.argtypes = [_P, _P, ctypes.c_char_p]
+        lib.sse_ipc_open.argtypes = [_P, ctypes.c_char_p, ctypes.POINTER(_P)]
+        lib.sse_ipc_close.argtypes = [_P, _P]
         lib.sse_layout_transform.argtypes = [_P, i64, i64, i64, i64, i32, _P, _P, _P]
         lib.sse_preprocess_D.argtypes = [_P, i64, i64, i64, i64, _P, i64, i64, i64, i64, _P, _P, _P]
         lib.sse_fill_synthetic.argtypes = [

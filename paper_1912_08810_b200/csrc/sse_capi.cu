@@ -285,9 +285,17 @@ struct DevPtrs {
 };
 
 // K2 + K3 for owned atoms [a0, a0 + n) of the out slab (tables already uploaded).
+// Peer scatter of Sigma into the (k,E)-point layout buffers of the owner ranks
+struct ScatterCfg {
+  int nranks = 0;
+  int64_t na = 0;
+  int64_t pt_lo[sse::kMaxScatter + 1] = {};
+  double2* S[2][sse::kMaxScatter] = {};
+};
+
 int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
               const DevPtrs& p, const int64_t* off, int64_t a0, int64_t n, cudaStream_t st,
-              int npol, int* launches) {
+              int npol, int* launches, const ScatterCfg* sc = nullptr) {
   const int no = (int)d->norb;
   const size_t opb = sse::operator_bytes(no, (int)d->nb, (int)d->nqz, (int)d->nw, (int)n);
   CHECK(ds.op[0].ensure(opb));
@@ -339,6 +347,14 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   sa.lookahead = getenv("SSE_SLIDE_LOOKAHEAD") ? atoi(getenv("SSE_SLIDE_LOOKAHEAD")) : 0;
   for (int64_t w = 1; w < d->nw; ++w)
     if (off[w] < off[w - 1] || off[w] > off[w - 1] + 1) sa.off_slide = 0;
+  if (sc && sc->nranks > 0) {
+    sa.scatter_ranks = sc->nranks;
+    sa.scatter_na = sc->na;
+    sa.scatter_atom0 = out.atom0 + a0;
+    for (int r = 0; r <= sc->nranks; ++r) sa.pt_lo[r] = sc->pt_lo[r];
+    for (int pol = 0; pol < 2; ++pol)
+      for (int r = 0; r < sc->nranks; ++r) sa.S_rank[pol][r] = sc->S[pol][r];
+  }
   CHECK(profiled(ds, st, SSE_PROF_SIGMA, alg_flops(d, off, n, npol),
                  [&] { return sse::launch_sigma(sa, (int)n, st); }));
   if (launches) *launches += 2;
@@ -347,12 +363,12 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
 
 int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
                     const DevPtrs& p, const int64_t* nmap, const int64_t* off, const double* wt,
-                    cudaStream_t st, int* launches, int npol = 2) {
+                    cudaStream_t st, int* launches, int npol = 2, const ScatterCfg* sc = nullptr) {
   CHECK(prepare_tables(ds, d, g, out, nmap, off, wt, st));
   const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d), out.natoms);
   for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk)
     CHECK(run_chunk(ds, d, g, out, p, off, a0, std::min<int64_t>(chunk, out.natoms - a0), st, npol,
-                    launches));
+                    launches, sc));
   return SSE_OK;
 }
 
@@ -800,6 +816,98 @@ int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const s
     t->sigma_ms = t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
     t->kernel_launches = launches;
   }
+  return SSE_OK;
+}
+
+int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
+                             const double* G_l, const double* G_g, const double* Dc_l, const double* Dc_g,
+                             const double* dH, const int64_t* nmap, const int64_t* off, const double* wt,
+                             int nranks, const int64_t* pt_lo, double* const* S_l, double* const* S_g,
+                             void* stream, sse_timing* t) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
+  CHECK(validate_dims(d));
+  CHECK(validate_grid(d, off, wt));
+  CHECK(validate_slab(d, g, "G"));
+  CHECK(validate_slab(d, out, "output"));
+  if (!G_l || !G_g || !Dc_l || !Dc_g || !dH || !nmap || !pt_lo || !S_l || !S_g)
+    return fail(SSE_EINVAL, "NULL tensor pointer");
+  if (nranks < 1 || nranks > sse::kMaxScatter)
+    return fail(SSE_EINVAL, "scatter needs 1..%d ranks (got %d)", sse::kMaxScatter, nranks);
+  ScatterCfg sc;
+  sc.nranks = nranks;
+  sc.na = d->na;
+  if (pt_lo[0] != 0 || pt_lo[nranks] != d->nkz * d->ne)
+    return fail(SSE_EINVAL, "point ranges must cover [0, Nkz*NE)");
+  for (int r = 0; r <= nranks; ++r) {
+    if (r > 0 && pt_lo[r] < pt_lo[r - 1]) return fail(SSE_EINVAL, "point ranges must be non-decreasing");
+    sc.pt_lo[r] = pt_lo[r];
+  }
+  for (int r = 0; r < nranks; ++r) {
+    if ((!S_l[r] || !S_g[r]) && pt_lo[r + 1] > pt_lo[r]) return fail(SSE_EINVAL, "NULL scatter target");
+    sc.S[0][r] = (double2*)S_l[r];
+    sc.S[1][r] = (double2*)S_g[r];
+  }
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->flops = alg_flops(d, off, out->natoms);
+    t->n_devices = 1;
+    CU(cudaEventRecord(ds.ev[0], st));
+  }
+  int launches = 0;
+  const DevPtrs p{(const double2*)G_l, (const double2*)G_g, (const double2*)Dc_l,
+                  (const double2*)Dc_g, (const double2*)dH, nullptr, nullptr};
+  CHECK(sigma_on_device(ds, d, *g, *out, p, nmap, off, wt, st, &launches, 2, &sc));
+  if (t) {
+    CU(cudaEventRecord(ds.ev[1], st));
+    CU(cudaEventSynchronize(ds.ev[1]));
+    t->sigma_ms = t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
+    t->kernel_launches = launches;
+  }
+  return SSE_OK;
+}
+
+int sse_dev_alloc(sse_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || ctx->devs.size() != 1 || !out) return fail(SSE_EINVAL, "device allocation needs a 1-device context");
+  CU(cudaSetDevice(ctx->devs[0].device));
+  *out = nullptr;
+  cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc", __LINE__);
+  return SSE_OK;
+}
+
+int sse_dev_free(sse_ctx* ctx, void* ptr) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device free needs a 1-device context");
+  CU(cudaSetDevice(ctx->devs[0].device));
+  if (ptr) CU(cudaFree(ptr));
+  return SSE_OK;
+}
+
+int sse_ipc_handle(sse_ctx* ctx, void* dptr, unsigned char* handle) {
+  if (!ctx || ctx->devs.size() != 1 || !dptr || !handle) return fail(SSE_EINVAL, "invalid IPC export");
+  CU(cudaSetDevice(ctx->devs[0].device));
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, dptr));
+  static_assert(sizeof(h) == SSE_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  return SSE_OK;
+}
+
+int sse_ipc_open(sse_ctx* ctx, const unsigned char* handle, void** out) {
+  if (!ctx || ctx->devs.size() != 1 || !handle || !out) return fail(SSE_EINVAL, "invalid IPC import");
+  CU(cudaSetDevice(ctx->devs[0].device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CU(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return SSE_OK;
+}
+
+int sse_ipc_close(sse_ctx* ctx, void* ptr) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "invalid IPC close");
+  CU(cudaSetDevice(ctx->devs[0].device));
+  if (ptr) CU(cudaIpcCloseMemHandle(ptr));
   return SSE_OK;
 }
 

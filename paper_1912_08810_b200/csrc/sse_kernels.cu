@@ -151,6 +151,17 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Base of the Sigma block (k, E) of chunk atom la: the slab (s_* strides), or
+// the point-layout buffer of the owner rank of point k*NE + E (peer scatter).
+__device__ __forceinline__ double2* sigma_block(const SigmaArgs& p, int pol, int la, int k, int e) {
+  if (p.scatter_ranks == 0)
+    return p.S[pol] + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk + (long long)e * p.s_se;
+  const long long pt = (long long)k * p.ne + e;
+  int r = 0;
+  while (r + 1 < p.scatter_ranks && pt >= p.pt_lo[r + 1]) ++r;
+  return p.S_rank[pol][r] + ((pt - p.pt_lo[r]) * p.scatter_na + p.scatter_atom0 + la) * (long long)(p.no * p.no);
+}
+
 // same without `volatile`: lets the scheduler interleave the shared-memory
 // operand loads with the DMMAs (the per-accumulator order is data-dependent)
 __device__ __forceinline__ void dmma884_nv(double (&c)[2], double a, double b) {
@@ -248,12 +259,10 @@ sigma_dmma_kernel(SigmaArgs p) {
   }
 
   // epilogue: lane holds (Re, Im) of C[row][n = 4 nt + (lane & 3)]; Sigma = i C
-  double2* __restrict__ S = p.S[pol];
 #pragma unroll
   for (int t = 0; t < kRowTiles; ++t) {
     if (!v_row[t]) continue;
-    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
-                   (long long)e_row[t] * p.s_se + m_row[t] * NO;
+    double2* dst = sigma_block(p, pol, la, k, e_row[t]) + m_row[t] * NO;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n = 4 * nt + (lane & 3);
@@ -384,13 +393,11 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
   }
 
   // epilogue: lane holds (Re, Im) of C[row][n = 4 nt + (lane & 3)]; Sigma = i C
-  double2* __restrict__ S = p.S[pol];
 #pragma unroll
   for (int t = 0; t < kRowTiles; ++t) {
     if (!v_row[t]) continue;
     const int row = rbase + t * 8 + (lane >> 2);
-    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
-                   (long long)e_row[t] * p.s_se + (row - e_row[t] * NO) * NO;
+    double2* dst = sigma_block(p, pol, la, k, e_row[t]) + (row - e_row[t] * NO) * NO;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n = 4 * nt + (lane & 3);
@@ -626,12 +633,10 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     }
   }
 
-  double2* __restrict__ S = p.S[pol];
 #pragma unroll
   for (int t = 0; t < MT; ++t) {
     if (!v_row[t]) continue;
-    double2* dst = S + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
-                   (long long)e_row[t] * p.s_se + m_off[t] - pcol;
+    double2* dst = sigma_block(p, pol, la, k, e_row[t]) + m_off[t] - pcol;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n = 4 * nt + (lane & 3);
@@ -1968,8 +1973,7 @@ __global__ void sigma_generic_kernel(SigmaArgs p, int chunk_atoms) {
         }
       }
     }
-    double2* dst = p.S[pol] + (long long)(p.s_atom_begin + la) * p.s_sa + (long long)k * p.s_sk +
-                   (long long)e * p.s_se + m * no + n;
+    double2* dst = sigma_block(p, pol, la, k, e) + m * no + n;
     *dst = make_double2(-im, re);
   }
 }

@@ -44,6 +44,12 @@ struct OperatorArgs {
   int npol;               // polarities to process (1 or 2)
 };
 
+// Peer scatter of Sigma: when scatter_ranks > 0 the block
+// (k, E, atom) is written straight into the (k,E)-point layout buffer of the
+// rank owning point pt = k*NE + E (NVLink peer memory, CUDA IPC):
+//   S_rank[pol][r] + ((pt - pt_lo[r]) * scatter_na + scatter_atom0 + la) * No^2
+constexpr int kMaxScatter = 8;
+
 struct SigmaArgs {
   const double2* G[2];
   const double2* M[2];    // operator of the chunk (layout per kernel)
@@ -59,6 +65,10 @@ struct SigmaArgs {
   int npol;               // polarities to process (1 or 2)
   int off_slide;          // 1: offsets non-decreasing with steps <= 1 (sliding-window K3 eligible)
   int lookahead;          // sliding-window K3 producer lookahead (0 = default)
+  int scatter_ranks;      // 0: write S with the s_* strides
+  long long scatter_na, scatter_atom0;
+  long long pt_lo[kMaxScatter + 1];
+  double2* S_rank[2][kMaxScatter];
 };
 
 // Phonon self-energy Pi (sse.py:332-428), chains in the V form

@@ -17,6 +17,7 @@ individual isend/irecv.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -227,3 +228,87 @@ def a2a_bytes(idx: np.ndarray, n_kz: int, n_e: int, n_o: int, world: int, rank: 
     sigma_in = (pe - ps) * idx.shape[0] * blk
     return {"g_in": g_in, "sigma_back": sigma_in,
             "g_in_from_peers": g_in - (pe - ps) * (ghi - glo) * blk}
+
+
+# ---------------------------------------------------------------------------
+# Sigma straight into the owners' point-layout buffers (NVLink peer stores)
+# ---------------------------------------------------------------------------
+
+
+class PeerPointBuffers:
+    """This rank's GF-layout Sigma buffers [pts_r, NA, No, No] (both polarities), mapped
+    into every rank of the group by CUDA IPC, so the Sigma kernel's epilogue can store
+    each (k, E, atom) block directly into its owner's buffer over NVLink
+    (``sse.sigma_device_scatter``): the return all-to-all fused into the compute.
+
+    Collective over the group (handle exchange); call :meth:`close` on every rank.
+    """
+
+    def __init__(self, n_kz: int, n_e: int, n_a: int, n_o: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.group = group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("peer scatter supports up to 8 ranks")
+        self.pts = point_chunks(n_kz, n_e, self.world)
+        self.pt_lo = [a for a, _ in self.pts] + [self.pts[-1][1]]
+        ps, pe = self.pts[self.rank]
+        self.shape = (pe - ps, n_a, n_o, n_o)
+        nbytes = max(1, (pe - ps) * n_a * n_o * n_o * 16)
+        self._lib = _lib.load()
+        self._ctx = _lib.context(device=device)
+        self.local = []
+        for _ in range(2):
+            ptr = _lib._P()
+            _lib.check(self._lib.sse_dev_alloc(self._ctx.handle, nbytes, ctypes.byref(ptr)))
+            self.local.append(ptr.value)
+        handles = []
+        for ptr in self.local:
+            h = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+            _lib.check(self._lib.sse_ipc_handle(self._ctx.handle, ctypes.c_void_p(ptr), h))
+            handles.append(h.raw)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, handles, group=group)
+        self.remote = []  # [pol][rank] device pointers valid in this process
+        self._opened = []
+        for pol in range(2):
+            row = []
+            for r in range(self.world):
+                if r == self.rank:
+                    row.append(self.local[pol])
+                    continue
+                ptr = _lib._P()
+                _lib.check(self._lib.sse_ipc_open(self._ctx.handle, everyone[r][pol], ctypes.byref(ptr)))
+                self._opened.append(ptr.value)
+                row.append(ptr.value)
+            self.remote.append(row)
+        dev = torch.device("cuda", device)
+        self.tensors = [_wrap_device(ptr, self.shape, dev) for ptr in self.local]
+
+    def close(self) -> None:
+        from . import _lib
+
+        for ptr in self._opened:
+            _lib.check(self._lib.sse_ipc_close(self._ctx.handle, ctypes.c_void_p(ptr)))
+        self._opened = []
+        self.tensors = []
+        for ptr in self.local:
+            _lib.check(self._lib.sse_dev_free(self._ctx.handle, ctypes.c_void_p(ptr)))
+        self.local = []
+
+
+class _CudaArray:
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<c16", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap_device(ptr: int, shape, device):
+    """A torch complex128 view of library-owned device memory (no copy)."""
+    import torch
+
+    return torch.as_tensor(_CudaArray(ptr, shape), device=device)

@@ -104,6 +104,14 @@ class ShardProblem:
             out_atom0=self.lo, atom_major=True, stream=stream,
         )
 
+    def sigma_scatter(self, peer, stream=None) -> None:
+        """Sigma of the owned atoms written into the point owners' buffers (dist.PeerPointBuffers)."""
+        dev.sigma_device_scatter(
+            self.g[0], self.g[1], self.dc[0], self.dc[1], self.dh, self.idx[self.lo:self.hi],
+            self.offsets, self.weights, peer.remote[0], peer.remote[1], peer.pt_lo, n_a=self.p.n_A,
+            g_atom0=self.glo, out_atom0=self.lo, atom_major=True, stream=stream,
+        )
+
     def pi(self, stream=None) -> None:
         """Phonon self-energy Pi of the owned atoms (sse.py:409-428), [Nqz, Nw, oA, NB+1, 3, 3]."""
         t, p = self.torch, self.p

@@ -420,6 +420,50 @@ def sigma_device(
     return tim.as_dict() if sync_timing else None
 
 
+def sigma_device_scatter(
+    g_l, g_g, dc_l, dc_g, dh, nmap_rows: Array, offsets, weights, targets_l, targets_g, pt_lo, *,
+    n_a: int, g_atom0: int = 0, out_atom0: int = 0, atom_major: bool = False, stream=None,
+    sync_timing: bool = False,
+) -> dict | None:
+    """:func:`sigma_device` with Sigma written into the (k,E)-point layout buffers of the owners.
+
+    ``targets_*[r]``: device pointers (int) of rank r's [pt_lo[r+1]-pt_lo[r], NA, No, No]
+    buffers, valid in this process (CUDA IPC mappings of the peers'); ``pt_lo``: the
+    GF phase's point partition (``dist.point_chunks``), length nranks + 1.
+    """
+    if atom_major:
+        g_atoms, n_kz, n_e, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
+    else:
+        n_kz, n_e, g_atoms, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
+    n_qz, n_w, o_atoms, n_b = dc_l.shape[:4]
+    if dh.shape[0] != o_atoms:
+        raise ValueError("Dc/dH rows must match the owned atom count")
+    idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    if idx.shape != (o_atoms, n_b):
+        raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    nranks = len(targets_l)
+    if len(targets_g) != nranks or len(pt_lo) != nranks + 1:
+        raise ValueError("one target per rank and nranks + 1 point bounds")
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    wts = np.ascontiguousarray(weights, dtype=np.float64)
+    bounds = np.ascontiguousarray(pt_lo, dtype=np.int64)
+    tl = (ctypes.c_void_p * nranks)(*[int(x) for x in targets_l])
+    tg = (ctypes.c_void_p * nranks)(*[int(x) for x in targets_g])
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    gs = _lib.SseSlab(g_atom0, g_atoms, int(atom_major), 0)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, int(atom_major), 0)
+    tim = _lib.SseTiming()
+    ctx = _device_ctx(g_l)
+    rc = _lib.load().sse_sigma_device_scatter(
+        ctx.handle, ctypes.byref(dims), ctypes.byref(gs), ctypes.byref(os_),
+        _dptr(g_l), _dptr(g_g), _dptr(dc_l), _dptr(dc_g), _dptr(dh),
+        _ptr(idx), _ptr(offs), _ptr(wts), nranks, _ptr(bounds), tl, tg,
+        _stream_ptr(stream), ctypes.byref(tim) if sync_timing else None,
+    )
+    _lib.check(rc)
+    return tim.as_dict() if sync_timing else None
+
+
 def pi_device(
     g_l, g_g, dh, nmap_rows: Array, offsets, energy_weight: float, pi_l, pi_g, *, n_a: int, n_qz: int,
     g_atom0: int = 0, out_atom0: int = 0, atom_major: bool = False, point_mask=None, stream=None,

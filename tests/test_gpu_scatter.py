@@ -1,0 +1,83 @@
+"""Sigma scattered straight into the GF-layout point owners over NVLink.
+
+Two NCCL ranks (spawned processes, one GPU each): the peer-scatter epilogue
+(``sse_sigma_device_scatter`` into CUDA-IPC-mapped buffers) must equal, bitwise,
+Sigma computed into atom slabs and returned with the NCCL all-to-all
+(``dist.atom_slab_to_points``).
+"""
+
+import os
+import socket
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1912_08810_b200 import dist as sdist
+    from paper_1912_08810_b200.inputs import default_grid
+    from paper_1912_08810_b200.problem import ShardProblem
+    from paper_1912_08810_b200.types import SimParams, build_neighbor_map
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        p = SimParams(n_kz=3, n_qz=2, n_E=37, n_w=13, n_A=26, n_B=4, n_orb=12)
+        idx = build_neighbor_map(p.n_A, p.n_B).idx
+        prob = ShardProblem(p, rank=rank, world=world, device=rank, seed=3, grid=default_grid(p), idx=idx)
+        prob.allocate()
+        prob.fill(owned_g_only=False)
+        prob.preprocess()
+        prob.sigma()
+        ref = [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
+        peer = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=rank)
+        for t in peer.tensors:
+            t.fill_(float("nan"))
+        torch.cuda.synchronize()
+        dist.barrier()
+        prob.sigma_scatter(peer)
+        torch.cuda.synchronize()
+        dist.barrier()  # every rank's peer stores have landed
+        ok = all(torch.equal(peer.tensors[pol], ref[pol]) for pol in range(2))
+        finite = all(bool(torch.isfinite(torch.view_as_real(t)).all()) for t in peer.tensors)
+        dist.barrier()
+        peer.close()
+        res = [None] * world
+        dist.all_gather_object(res, (ok, finite))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_scatter_equals_all_to_all_return_bitwise():
+    import multiprocessing as mp
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    assert all(ok and fin for ok, fin in res), res
