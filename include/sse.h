@@ -158,6 +158,20 @@ int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
                              int nranks, const int64_t* pt_lo, double* const* S_l,
                              double* const* S_g, void* stream, sse_timing* t);
 
+/* Fully fused GF-layout step: G is READ from the point owners' buffers too
+ * (G_l[r] / G_g[r]: [pt_lo[r+1]-pt_lo[r], NA, No, No], TMA bulk copies over
+ * NVLink in the sliding-window K3 producer) and Sigma is scattered as in
+ * sse_sigma_device_scatter, so neither the G redistribution nor the Sigma
+ * return needs a separate collective.  Needs the sliding-window K3 (sliding
+ * offsets, Nw >= 12, No <= 16; else returns 1).  nmap: HOST [out.natoms, NB]
+ * global ids; Dc / dH for the owned atoms. */
+int sse_sigma_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out,
+                          const double* const* G_l, const double* const* G_g,
+                          const double* Dc_l, const double* Dc_g, const double* dH,
+                          const int64_t* nmap, const int64_t* off, const double* wt,
+                          int nranks, const int64_t* pt_lo, double* const* S_l,
+                          double* const* S_g, void* stream, sse_timing* t);
+
 /* Library-owned device memory that can be shared with peer processes, and CUDA
  * IPC export / import of it (handles are SSE_IPC_HANDLE_BYTES opaque bytes). */
 #define SSE_IPC_HANDLE_BYTES 64

@@ -291,6 +291,8 @@ struct ScatterCfg {
   int64_t na = 0;
   int64_t pt_lo[sse::kMaxScatter + 1] = {};
   double2* S[2][sse::kMaxScatter] = {};
+  bool gather = false;  // G read from the owners' point buffers too (sliding-window K3)
+  const double2* G[2][sse::kMaxScatter] = {};
 };
 
 int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
@@ -354,6 +356,11 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
     for (int r = 0; r <= sc->nranks; ++r) sa.pt_lo[r] = sc->pt_lo[r];
     for (int pol = 0; pol < 2; ++pol)
       for (int r = 0; r < sc->nranks; ++r) sa.S_rank[pol][r] = sc->S[pol][r];
+    if (sc->gather) {
+      sa.gather_ranks = sc->nranks;
+      for (int pol = 0; pol < 2; ++pol)
+        for (int r = 0; r < sc->nranks; ++r) sa.G_rank[pol][r] = sc->G[pol][r];
+    }
   }
   CHECK(profiled(ds, st, SSE_PROF_SIGMA, alg_flops(d, off, n, npol),
                  [&] { return sse::launch_sigma(sa, (int)n, st); }));
@@ -819,17 +826,22 @@ int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const s
   return SSE_OK;
 }
 
-int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
-                             const double* G_l, const double* G_g, const double* Dc_l, const double* Dc_g,
-                             const double* dH, const int64_t* nmap, const int64_t* off, const double* wt,
-                             int nranks, const int64_t* pt_lo, double* const* S_l, double* const* S_g,
-                             void* stream, sse_timing* t) {
+}  // extern "C"
+
+namespace {
+int sigma_peer_impl(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out, const double* G_l,
+                    const double* G_g, const double* const* G_l_ranks, const double* const* G_g_ranks,
+                    const double* Dc_l, const double* Dc_g, const double* dH, const int64_t* nmap,
+                    const int64_t* off, const double* wt, int nranks, const int64_t* pt_lo, double* const* S_l,
+                    double* const* S_g, void* stream, sse_timing* t) {
   if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
   CHECK(validate_dims(d));
   CHECK(validate_grid(d, off, wt));
   CHECK(validate_slab(d, g, "G"));
   CHECK(validate_slab(d, out, "output"));
-  if (!G_l || !G_g || !Dc_l || !Dc_g || !dH || !nmap || !pt_lo || !S_l || !S_g)
+  const bool gather = G_l_ranks != nullptr;
+  if ((!gather && (!G_l || !G_g)) || (gather && !G_g_ranks) || !Dc_l || !Dc_g || !dH || !nmap || !pt_lo || !S_l ||
+      !S_g)
     return fail(SSE_EINVAL, "NULL tensor pointer");
   if (nranks < 1 || nranks > sse::kMaxScatter)
     return fail(SSE_EINVAL, "scatter needs 1..%d ranks (got %d)", sse::kMaxScatter, nranks);
@@ -846,7 +858,15 @@ int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
     if ((!S_l[r] || !S_g[r]) && pt_lo[r + 1] > pt_lo[r]) return fail(SSE_EINVAL, "NULL scatter target");
     sc.S[0][r] = (double2*)S_l[r];
     sc.S[1][r] = (double2*)S_g[r];
+    if (gather) {
+      if ((!G_l_ranks[r] || !G_g_ranks[r]) && pt_lo[r + 1] > pt_lo[r]) return fail(SSE_EINVAL, "NULL gather source");
+      sc.G[0][r] = (const double2*)G_l_ranks[r];
+      sc.G[1][r] = (const double2*)G_g_ranks[r];
+    }
   }
+  sc.gather = gather;
+  if (gather && (g->atom0 != 0 || g->natoms != d->na))
+    return fail(SSE_EINVAL, "peer gather reads G by global atom id: pass the G slab [0, NA)");
   DevState& ds = ctx->devs[0];
   CU(cudaSetDevice(ds.device));
   cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
@@ -859,7 +879,10 @@ int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
   int launches = 0;
   const DevPtrs p{(const double2*)G_l, (const double2*)G_g, (const double2*)Dc_l,
                   (const double2*)Dc_g, (const double2*)dH, nullptr, nullptr};
-  CHECK(sigma_on_device(ds, d, *g, *out, p, nmap, off, wt, st, &launches, 2, &sc));
+  const int rc = sigma_on_device(ds, d, *g, *out, p, nmap, off, wt, st, &launches, 2, &sc);
+  if (rc == SSE_ECUDA && gather && std::string(g_last_error).find("not supported") != std::string::npos)
+    return fail(SSE_EINVAL, "peer gather needs the sliding-window K3 (sliding offsets, Nw >= 12, No <= 16)");
+  CHECK(rc);
   if (t) {
     CU(cudaEventRecord(ds.ev[1], st));
     CU(cudaEventSynchronize(ds.ev[1]));
@@ -867,6 +890,30 @@ int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g,
     t->kernel_launches = launches;
   }
   return SSE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sse_sigma_device_scatter(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
+                             const double* G_l, const double* G_g, const double* Dc_l, const double* Dc_g,
+                             const double* dH, const int64_t* nmap, const int64_t* off, const double* wt,
+                             int nranks, const int64_t* pt_lo, double* const* S_l, double* const* S_g,
+                             void* stream, sse_timing* t) {
+  return sigma_peer_impl(ctx, d, g, out, G_l, G_g, nullptr, nullptr, Dc_l, Dc_g, dH, nmap, off, wt, nranks, pt_lo,
+                         S_l, S_g, stream, t);
+}
+
+int sse_sigma_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out, const double* const* G_l,
+                          const double* const* G_g, const double* Dc_l, const double* Dc_g, const double* dH,
+                          const int64_t* nmap, const int64_t* off, const double* wt, int nranks,
+                          const int64_t* pt_lo, double* const* S_l, double* const* S_g, void* stream,
+                          sse_timing* t) {
+  if (!d) return fail(SSE_EINVAL, "dims is NULL");
+  const sse_slab all{0, d->na, 1, 0};
+  return sigma_peer_impl(ctx, d, &all, out, nullptr, nullptr, G_l, G_g, Dc_l, Dc_g, dH, nmap, off, wt, nranks,
+                         pt_lo, S_l, S_g, stream, t);
 }
 
 int sse_dev_alloc(sse_ctx* ctx, size_t bytes, void** out) {

@@ -554,15 +554,27 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     const int q = sg / p.nb, s = sg - q * p.nb;
     int kp = (k - q) % p.nkz;
     if (kp < 0) kp += p.nkz;
-    const long long slab = __ldg(p.nbr + la * p.nb + s) * p.g_sa + kp * p.g_sk;
+    const long long nb_atom = __ldg(p.nbr + la * p.nb + s);
+    const long long slab = nb_atom * p.g_sa + kp * p.g_sk;
     const double2* mf = Mf + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw + w) * BVEC;
     const int hi = seg_empty ? 0 : win_low(w - 1), lo = seg_empty ? 0 : win_low(w);
     if (t >= SB) mbar_wait(empty + slot, (uint32_t)(((t - SB) / SB) & 1));
     mbar_arrive_expect_tx(full + slot, (uint32_t)(BVEC + (hi - lo) * BLK) * 16);
     bulk_g2s(ring_b + slot * BVEC, mf, BVEC * 16, full + slot);
-    for (int e = hi - 1; e >= lo; --e) {
-      const int f = (sg * seg_blocks + top0 - e) & (R - 1);
-      bulk_g2s(ring_a + f * BLK, G + slab + (long long)e * p.g_se, BLK * 16, full + slot);
+    if (p.gather_ranks == 0) {
+      for (int e = hi - 1; e >= lo; --e) {
+        const int f = (sg * seg_blocks + top0 - e) & (R - 1);
+        bulk_g2s(ring_a + f * BLK, G + slab + (long long)e * p.g_se, BLK * 16, full + slot);
+      }
+    } else {  // G in the GF point layout of the owner ranks, read over NVLink (nbr = global atom ids)
+      int r = p.gather_ranks - 1;
+      for (int e = hi - 1; e >= lo; --e) {
+        const long long pt = (long long)kp * p.ne + e;
+        while (r > 0 && pt < p.pt_lo[r]) --r;  // e descends: the owner rank only moves down
+        const double2* src = p.G_rank[pol][r] + ((pt - p.pt_lo[r]) * p.scatter_na + nb_atom) * BLK;
+        const int f = (sg * seg_blocks + top0 - e) & (R - 1);
+        bulk_g2s(ring_a + f * BLK, src, BLK * 16, full + slot);
+      }
     }
   };
 
@@ -1549,7 +1561,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   // ragged last quad (No^2 % 4 != 0): lanes past No^2 read zeros, because the
   // slot rows they meet may hold another sub-stage's (stale, finite) B
   const int kq_last = (no2 - 1 - pcol) / 4;
-  const double2 *cur, *nxt;
+  const double2 *cur = nullptr, *nxt = nullptr;
   auto load_a = [&](int kq) -> double2 {  // quad kq of the current stage, or kq - khp of the next
     const double2* r = kq < khp ? cur : nxt;
     const int qq = kq < khp ? kq : kq - khp;
@@ -1766,7 +1778,7 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
                ? g_atom + (long long)kp * p.g_sk + (long long)(e + off[t]) * p.g_se + pcol
                : kPiZeroRow + pcol;
   };
-  const double2 *cur[2], *nxt[2];
+  const double2 *cur[2] = {nullptr, nullptr}, *nxt[2] = {nullptr, nullptr};
   auto load_a = [&](int t, int kq) -> double2 {
     const double2* r = kq < KHP ? cur[t] : nxt[t];
     const int qq = kq < KHP ? kq : kq - KHP;
@@ -2090,17 +2102,19 @@ static int sigma_kernel_choice() {
 }
 
 template <int NO>
-static void launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
+static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
   SigmaArgs a = a0;
   const int choice = sigma_kernel_choice();
   auto grid_for_rows = [&](int rows_per_cta) {
     a.ctas_per_ak = (a.rows + rows_per_cta - 1) / rows_per_cta;
     return dim3((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
   };
-  if (choice == 0) {
+  const bool slide_ok = a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw && SlideGeom<NO, 12, 3>::kFits;
+  if (a.gather_ranks > 0 && !slide_ok) return cudaErrorNotSupported;  // peer gather: sliding-window K3 only
+  if (choice == 0 && a.gather_ranks == 0) {
     const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  } else if (choice == 3 && a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw) {
+  } else if ((choice == 3 || a.gather_ranks > 0) && a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw) {
     // nw >= kSlideStages: the kSlideStages stages in flight span at most one
     // (q, s) segment boundary, so at most 2 * kTE + kSlideStages FIFO blocks
     // are live (SlideGeom::kNeed <= kRing); shorter segments use the
@@ -2111,7 +2125,7 @@ static void launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
       cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
       sigma_dmma_slide_kernel<NO, 12, 3><<<grid, 12 * 32, smem, st>>>(a);
-      return;
+      return cudaSuccess;
     }
     const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
@@ -2119,31 +2133,33 @@ static void launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
     const dim3 grid = grid_for_rows(kRowsPerCta);
     sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
   }
+  return cudaSuccess;
 }
 
 cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) {
   SigmaArgs a = a0;
   if (a.no <= kMaxDmmaOrb) {
     switch (a.no) {
-      case 1: launch_dmma<1>(a, chunk_atoms, st); break;
-      case 2: launch_dmma<2>(a, chunk_atoms, st); break;
-      case 3: launch_dmma<3>(a, chunk_atoms, st); break;
-      case 4: launch_dmma<4>(a, chunk_atoms, st); break;
-      case 5: launch_dmma<5>(a, chunk_atoms, st); break;
-      case 6: launch_dmma<6>(a, chunk_atoms, st); break;
-      case 7: launch_dmma<7>(a, chunk_atoms, st); break;
-      case 8: launch_dmma<8>(a, chunk_atoms, st); break;
-      case 9: launch_dmma<9>(a, chunk_atoms, st); break;
-      case 10: launch_dmma<10>(a, chunk_atoms, st); break;
-      case 11: launch_dmma<11>(a, chunk_atoms, st); break;
-      case 12: launch_dmma<12>(a, chunk_atoms, st); break;
-      case 13: launch_dmma<13>(a, chunk_atoms, st); break;
-      case 14: launch_dmma<14>(a, chunk_atoms, st); break;
-      case 15: launch_dmma<15>(a, chunk_atoms, st); break;
-      case 16: launch_dmma<16>(a, chunk_atoms, st); break;
+      case 1: { const cudaError_t e = launch_dmma<1>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 2: { const cudaError_t e = launch_dmma<2>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 3: { const cudaError_t e = launch_dmma<3>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 4: { const cudaError_t e = launch_dmma<4>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 5: { const cudaError_t e = launch_dmma<5>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 6: { const cudaError_t e = launch_dmma<6>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 7: { const cudaError_t e = launch_dmma<7>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 8: { const cudaError_t e = launch_dmma<8>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 9: { const cudaError_t e = launch_dmma<9>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 10: { const cudaError_t e = launch_dmma<10>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 11: { const cudaError_t e = launch_dmma<11>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 12: { const cudaError_t e = launch_dmma<12>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 13: { const cudaError_t e = launch_dmma<13>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 14: { const cudaError_t e = launch_dmma<14>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 15: { const cudaError_t e = launch_dmma<15>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
+      case 16: { const cudaError_t e = launch_dmma<16>(a, chunk_atoms, st); if (e != cudaSuccess) return e; break; }
       default: return cudaErrorInvalidValue;
     }
   } else {
+    if (a.gather_ranks > 0) return cudaErrorNotSupported;
     const long long total = (long long)a.nkz * a.ne * a.no * a.no * chunk_atoms;
     dim3 grid(grid_for(total, 256), a.npol);
     sigma_generic_kernel<<<grid, 256, 0, st>>>(a, chunk_atoms);

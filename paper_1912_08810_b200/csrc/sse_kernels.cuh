@@ -66,9 +66,14 @@ struct SigmaArgs {
   int off_slide;          // 1: offsets non-decreasing with steps <= 1 (sliding-window K3 eligible)
   int lookahead;          // sliding-window K3 producer lookahead (0 = default)
   int scatter_ranks;      // 0: write S with the s_* strides
-  long long scatter_na, scatter_atom0;
+  long long scatter_na, scatter_atom0;  // NA of the point buffers; global id of the chunk's first atom
   long long pt_lo[kMaxScatter + 1];
   double2* S_rank[2][kMaxScatter];
+  // peer gather (sliding-window K3 only): G block (k, E, atom) read from
+  // G_rank[pol][r] + ((k*NE + E - pt_lo[r]) * scatter_na + atom) * No^2 of the
+  // point owner r; nbr holds global atom ids
+  int gather_ranks;
+  const double2* G_rank[2][kMaxScatter];
 };
 
 // Phonon self-energy Pi (sse.py:332-428), chains in the V form

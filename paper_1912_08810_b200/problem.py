@@ -112,6 +112,16 @@ class ShardProblem:
             g_atom0=self.glo, out_atom0=self.lo, atom_major=True, stream=stream,
         )
 
+    def sigma_peer(self, peer_g, peer_s, stream=None) -> None:
+        """Sigma with G read from the GF point owners (peer_g) and written to them (peer_s):
+        no slab, no halo, no return collective (dist.PeerPointBuffers for both)."""
+        p = self.p
+        dev.sigma_device_peer(
+            peer_g.remote[0], peer_g.remote[1], self.dc[0], self.dc[1], self.dh, self.idx[self.lo:self.hi],
+            self.offsets, self.weights, peer_s.remote[0], peer_s.remote[1], peer_s.pt_lo, n_kz=p.n_kz, n_e=p.n_E,
+            n_a=p.n_A, n_o=p.n_orb, out_atom0=self.lo, device=self.device.index or 0, stream=stream,
+        )
+
     def pi(self, stream=None) -> None:
         """Phonon self-energy Pi of the owned atoms (sse.py:409-428), [Nqz, Nw, oA, NB+1, 3, 3]."""
         t, p = self.torch, self.p

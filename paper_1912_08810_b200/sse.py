@@ -464,6 +464,40 @@ def sigma_device_scatter(
     return tim.as_dict() if sync_timing else None
 
 
+def sigma_device_peer(
+    sources_l, sources_g, dc_l, dc_g, dh, nmap_rows: Array, offsets, weights, targets_l, targets_g, pt_lo, *,
+    n_kz: int, n_e: int, n_a: int, n_o: int, out_atom0: int, device: int, stream=None,
+    sync_timing: bool = False,
+) -> dict | None:
+    """Sigma of owned atoms with G read from, and Sigma written to, the GF point-layout buffers
+    of the owner ranks (``sse_sigma_device_peer``): ``sources_*[r]`` / ``targets_*[r]`` are
+    device pointers (int) of rank r's [pts_r, NA, No, No] buffers valid in this process."""
+    n_qz, n_w, o_atoms, n_b = dc_l.shape[:4]
+    if dh.shape[0] != o_atoms:
+        raise ValueError("Dc/dH rows must match the owned atom count")
+    idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    if idx.shape != (o_atoms, n_b):
+        raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    nranks = len(targets_l)
+    if not (len(targets_g) == len(sources_l) == len(sources_g) == nranks) or len(pt_lo) != nranks + 1:
+        raise ValueError("one source and target per rank and nranks + 1 point bounds")
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    wts = np.ascontiguousarray(weights, dtype=np.float64)
+    bounds = np.ascontiguousarray(pt_lo, dtype=np.int64)
+    arr = lambda xs: (ctypes.c_void_p * nranks)(*[int(x) for x in xs])  # noqa: E731
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, 1, 0)
+    tim = _lib.SseTiming()
+    ctx = _lib.context(device=device)
+    rc = _lib.load().sse_sigma_device_peer(
+        ctx.handle, ctypes.byref(dims), ctypes.byref(os_), arr(sources_l), arr(sources_g),
+        _dptr(dc_l), _dptr(dc_g), _dptr(dh), _ptr(idx), _ptr(offs), _ptr(wts), nranks, _ptr(bounds),
+        arr(targets_l), arr(targets_g), _stream_ptr(stream), ctypes.byref(tim) if sync_timing else None,
+    )
+    _lib.check(rc)
+    return tim.as_dict() if sync_timing else None
+
+
 def pi_device(
     g_l, g_g, dh, nmap_rows: Array, offsets, energy_weight: float, pi_l, pi_g, *, n_a: int, n_qz: int,
     g_atom0: int = 0, out_atom0: int = 0, atom_major: bool = False, point_mask=None, stream=None,

@@ -1,9 +1,10 @@
 """Sigma scattered straight into the GF-layout point owners over NVLink.
 
 Two NCCL ranks (spawned processes, one GPU each): the peer-scatter epilogue
-(``sse_sigma_device_scatter`` into CUDA-IPC-mapped buffers) must equal, bitwise,
-Sigma computed into atom slabs and returned with the NCCL all-to-all
-(``dist.atom_slab_to_points``).
+(``sse_sigma_device_scatter`` into CUDA-IPC-mapped buffers) and the fully fused
+variant that also reads G from the owners' point buffers with TMA
+(``sse_sigma_device_peer``) must equal, bitwise, Sigma computed into atom slabs
+and returned with the NCCL all-to-all (``dist.atom_slab_to_points``).
 """
 
 import os
@@ -52,17 +53,31 @@ def _worker(rank, world, port, q):
         dist.barrier()  # every rank's peer stores have landed
         ok = all(torch.equal(peer.tensors[pol], ref[pol]) for pol in range(2))
         finite = all(bool(torch.isfinite(torch.view_as_real(t)).all()) for t in peer.tensors)
+        # fully fused: G read from the point owners too (their GF-layout buffers)
+        peer_g = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=rank)
+        own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
+        for pol in range(2):
+            peer_g.tensors[pol].copy_(sdist.atom_slab_to_points(prob.g[pol][own].contiguous(), idx, p.n_kz, p.n_E))
+        for t in peer.tensors:
+            t.fill_(float("nan"))
+        torch.cuda.synchronize()
         dist.barrier()
+        prob.sigma_peer(peer_g, peer)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ok_fused = all(torch.equal(peer.tensors[pol], ref[pol]) for pol in range(2))
+        dist.barrier()
+        peer_g.close()
         peer.close()
         res = [None] * world
-        dist.all_gather_object(res, (ok, finite))
+        dist.all_gather_object(res, (ok, finite, ok_fused))
         if rank == 0:
             q.put(res)
     finally:
         dist.destroy_process_group()
 
 
-def test_peer_scatter_equals_all_to_all_return_bitwise():
+def test_peer_scatter_and_gather_equal_all_to_all_bitwise():
     import multiprocessing as mp
 
     import torch
@@ -80,4 +95,5 @@ def test_peer_scatter_equals_all_to_all_return_bitwise():
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
-    assert all(ok and fin for ok, fin in res), res
+    assert all(ok and fin for ok, fin, _ in res), res
+    assert all(fused for _, _, fused in res), res
