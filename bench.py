@@ -514,6 +514,47 @@ def run_gpu(args, p, grid, idx) -> None:
         del g_pts
         torch.cuda.empty_cache()
 
+    # SURVEY 8f-3 fused: G read from the GF point owners and Sigma written back to them inside
+    # the Sigma kernel (NVLink peer memory via CUDA IPC): no slab assembly, halo or return
+    # collective; one device-side all-reduce per step orders the peers' stores
+    fused_info = None
+    if args.gf_fused_steps > 0 and world > 1:
+        import torch.distributed as dist
+
+        own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
+        peer_g = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
+        for pol in range(2):
+            peer_g.tensors[pol].copy_(sdist.atom_slab_to_points(prob.g[pol][own].contiguous(), idx, p.n_kz, p.n_E))
+        peer_s = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
+        token = torch.zeros(1, device=prob.device)
+
+        def fused_step():
+            prob.preprocess()
+            prob.sigma_peer(peer_g, peer_s)
+            dist.all_reduce(token)  # every rank's peer stores done before anyone reads its points
+
+        fused_step()
+        ref_pts = [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
+        torch.cuda.synchronize()
+        same = float(all(torch.equal(peer_s.tensors[pol], ref_pts[pol]) for pol in range(2)))
+        same = -allreduce_max(-same, world)
+        del ref_pts
+        barrier(world)
+        start.record(stream)
+        for _ in range(args.gf_fused_steps):
+            fused_step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        fused_ms = allreduce_max(start.elapsed_time(end) / args.gf_fused_steps, world)
+        fused_info = {"s_per_step": fused_ms / 1e3, "steps": args.gf_fused_steps, "vs_halo_step": fused_ms / step_ms,
+                      "sigma_points_bitwise_equal_to_all_to_all": bool(same == 1.0),
+                      "note": "G read from the GF (k,E)-point owners by TMA over NVLink and Sigma stored to them "
+                              "from the K3 epilogue (CUDA IPC peer memory); preprocess_D + K2 + K3 + one "
+                              "device-side all-reduce per step"}
+        barrier(world)
+        peer_g.close()
+        peer_s.close()
+
     prob.free()
     del prob
     torch.cuda.synchronize()
@@ -573,6 +614,8 @@ def run_gpu(args, p, grid, idx) -> None:
             line["pi"] = pi_info
         if gf_info is not None:
             line["gf_layout"] = gf_info
+        if fused_info is not None:
+            line["gf_layout_fused"] = fused_info
         if e2e is not None:
             line["e2e"] = e2e
         if phase is not None:
@@ -602,6 +645,8 @@ def main():
     ap.add_argument("--pi-steps", type=int, default=1, help="timed Pi evaluations after Sigma (0 = skip)")
     ap.add_argument("--phase-steps", type=int, default=0,
                     help="N=1: timed SSE phases (preprocess_D + Sigma + Pi) through sse_phase from pinned host memory")
+    ap.add_argument("--gf-fused-steps", type=int, default=0,
+                    help="N>1: timed steps reading G from / writing Sigma to the GF point owners over NVLink")
     ap.add_argument("--gf-layout-steps", type=int, default=0,
                     help="N>1: timed steps starting from the GF (k,E)-point layout (two all-to-alls)")
     args = ap.parse_args()
