@@ -174,7 +174,8 @@ void destroy_dev(DevState& d) {
   cudaSetDevice(d.device);
   for (DevBuf* b : {&d.g[0], &d.g[1], &d.s[0], &d.s[1], &d.dc[0], &d.dc[1], &d.dh, &d.op[0],
                     &d.op[1], &d.nbr, &d.off, &d.wt, &d.tmp_g, &d.tmp_s, &d.pp_nbr, &d.pp_rev,
-                    &d.pi_vt[0], &d.pi_vt[1], &d.pi_part, &d.pi_mask, &d.pi_out[0], &d.pi_out[1]})
+                    &d.pi_vt[0], &d.pi_vt[1], &d.pi_part, &d.pi_mask, &d.pi_out[0], &d.pi_out[1],
+                    &d.draw[0], &d.draw[1]})
     b->release();
   for (auto& e : d.ev)
     if (e) cudaEventDestroy(e);
@@ -1115,9 +1116,7 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
     }
     const int64_t gn = ghi - glo;
     cudaStream_t st = ds.stream;
-    cudaEvent_t e0, e1;
-    CU(cudaEventCreate(&e0));
-    CU(cudaEventCreate(&e1));
+    cudaEvent_t e0 = ds.ev[4], e1 = ds.ev[5];  // ev[0..3] belong to the Sigma host call below
     CU(cudaEventRecord(e0, st));
     // raw D of the G slab's atoms, then Dc of the owned atoms (sse.py:105-113)
     std::vector<int> nbr, rev;
@@ -1161,8 +1160,6 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
       tt->d2h_bytes += ts.d2h_bytes + 2 * pi_rows * on * pi_row;
       tt->kernel_launches += launches;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     return SSE_OK;
   };
   if (nd == 1) return on_device(ctx->devs[0], 0, d->na, t);
