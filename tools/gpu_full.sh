@@ -14,7 +14,7 @@ echo "ncu launches rc=$?" >> gpurun_out/ncu_launch.log
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sigma_dmma -s 4 -c 1 -o gpurun_out/bench_k3 -f python $B > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
 timeout 300 python tools/profile_pi.py --atoms 96 --steps 1 > gpurun_out/pi_plain.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pi_dmma3 -s 1 -c 1 -o gpurun_out/pi_k6 -f python tools/profile_pi.py --atoms 96 --steps 1 > gpurun_out/ncu_pi.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pi_dmma[34] -s 1 -c 1 -o gpurun_out/pi_k6 -f python tools/profile_pi.py --atoms 96 --steps 1 > gpurun_out/ncu_pi.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:pi_build_dmma -s 1 -c 1 -o gpurun_out/pi_k5 -f python tools/profile_pi.py --atoms 96 --steps 1 >> gpurun_out/ncu_pi.log 2>&1
 echo "ncu pi rc=$?" >> gpurun_out/ncu_pi.log
 tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; tail -2 gpurun_out/bench.log; tail -1 gpurun_out/bench_phase.log; tail -1 gpurun_out/ncu_launch.log; tail -1 gpurun_out/ncu_full.log; tail -1 gpurun_out/ncu_pi.log; cat gpurun_out/pi_plain.log
