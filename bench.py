@@ -480,21 +480,27 @@ def run_gpu(args, p, grid, idx) -> None:
         # built from the owned atoms with the return collective itself
         g_pts = [sdist.atom_slab_to_points(prob.g[pol][prob.lo - prob.glo:prob.hi - prob.glo], idx, p.n_kz, p.n_E)
                  for pol in range(2)]
+        # raw D from the phonon GF phase's (q, w) points
+        d_own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
+        d_pts = [sdist.columns_to_points(prob.d[pol][:, :, d_own].reshape(p.n_qz * p.n_w, prob.n_owned, -1),
+                                         sdist.owned_ranges(p.n_A, world), p.n_qz * p.n_w, p.n_A, False)
+                 .view(-1, p.n_A, p.n_B + 1, 3, 3) for pol in range(2)]
         def digest(ts):  # bit-pattern checksum (int64 wrap-around sum): equal inputs <=> equal digests
             return [int(torch.view_as_real(t).view(torch.int64).sum()) for t in ts]
 
-        want = digest(prob.g)
+        want = digest(prob.g) + digest(prob.d)
 
         def gf_step():
             for pol in range(2):
                 prob.g[pol].copy_(sdist.points_to_atom_slab(g_pts[pol], idx, p.n_kz, p.n_E))
+                prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
             prob.preprocess()
             prob.sigma()
             return [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
 
         gf_step()
         torch.cuda.synchronize()
-        same = float(digest(prob.g) == want)
+        same = float(digest(prob.g) + digest(prob.d) == want)
         same = -allreduce_max(-same, world)  # min over ranks
         barrier(world)
         start.record(stream)
@@ -509,9 +515,10 @@ def run_gpu(args, p, grid, idx) -> None:
                    "vs_halo_step": gf_ms / step_ms,
                    "slab_digest_equal_to_halo_exchange": bool(same == 1.0),
                    "a2a_bytes_per_rank_approx": int(2 * pts_r * (prob.n_slab + p.n_A) * blk),
-                   "note": "G from the GF (k,E)-point layout -> atom slabs (NCCL all_to_all_single, halo "
-                           "included) + preprocess_D + K2 + K3 + Sigma back to points (all_to_all_single)"}
-        del g_pts
+                   "note": "G from the GF (k,E)-point layout and raw D from the phonon (q,w)-point layout -> "
+                           "atom slabs (NCCL all_to_all_single, halos included) + preprocess_D + K2 + K3 + Sigma "
+                           "back to points (all_to_all_single)"}
+        del g_pts, d_pts
         torch.cuda.empty_cache()
 
     # SURVEY 8f-3 fused: G read from the GF point owners and Sigma written back to them inside

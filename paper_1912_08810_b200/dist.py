@@ -142,63 +142,131 @@ def _slabs(idx: np.ndarray, world: int):
     return out
 
 
-def points_to_atom_slab(g_pts, idx: np.ndarray, n_kz: int, n_e: int, group=None):
-    """[pts_r, NA, No, No] (this rank's GF points) -> atom-major slab [gA, Nkz, NE, No, No].
+def points_to_columns(x_pts, ranges, n_pts: int, atom_major: bool, group=None):
+    """Point-distributed rows -> this rank's column slab, one all-to-all.
 
-    Collective over the group; every rank passes its own point rows.
+    ``x_pts``: this rank's point rows [pts_r, NA, *blk] (``point_chunks`` of
+    ``n_pts``); ``ranges[r] = (c0, c1)``: the atom columns rank r needs
+    (its slab with halo, or its owned atoms).  Returns this rank's
+    [c1-c0, n_pts, *blk] (``atom_major``) or [n_pts, c1-c0, *blk].
     """
-    import torch
     import torch.distributed as dist
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    pts = point_chunks(n_kz, n_e, world)
-    slabs = _slabs(idx, world)
-    no2 = g_pts.shape[-1] * g_pts.shape[-2]
-    flat = g_pts.reshape(g_pts.shape[0], g_pts.shape[1], no2)
-    send = torch.cat([flat[:, glo:ghi].reshape(-1) for (_, _, glo, ghi) in slabs]) if flat.numel() else \
-        flat.new_zeros(0)
-    send_sizes = [flat.shape[0] * (ghi - glo) * no2 for (_, _, glo, ghi) in slabs]
-    lo, hi, glo, ghi = slabs[rank]
-    gA = ghi - glo
-    recv_sizes = [(pe - ps) * gA * no2 for (ps, pe) in pts]
+    pts = [chunk(n_pts, world, r) for r in range(world)]
+    blk = tuple(x_pts.shape[2:])
+    nblk = int(np.prod(blk)) if blk else 1
+    flat = x_pts.reshape(x_pts.shape[0], x_pts.shape[1], nblk)
+    send = flat.new_empty(sum(flat.shape[0] * (c1 - c0) * nblk for c0, c1 in ranges))
+    pos = 0
+    for c0, c1 in ranges:
+        n = flat.shape[0] * (c1 - c0) * nblk
+        send[pos:pos + n] = flat[:, c0:c1].reshape(-1)
+        pos += n
+    send_sizes = [flat.shape[0] * (c1 - c0) * nblk for c0, c1 in ranges]
+    c0, c1 = ranges[rank]
+    width = c1 - c0
+    recv_sizes = [(pe - ps) * width * nblk for ps, pe in pts]
     recv = flat.new_empty(sum(recv_sizes))
     _all_to_all(recv, send, recv_sizes, send_sizes, group)
-    slab = flat.new_empty((gA, n_kz * n_e, no2))
+    out = flat.new_empty((width, n_pts, nblk) if atom_major else (n_pts, width, nblk))
     pos = 0
     for (ps, pe), sz in zip(pts, recv_sizes):
         if pe > ps:
-            slab[:, ps:pe] = recv[pos:pos + sz].view(pe - ps, gA, no2).transpose(0, 1)
+            part = recv[pos:pos + sz].view(pe - ps, width, nblk)
+            if atom_major:
+                out[:, ps:pe] = part.transpose(0, 1)
+            else:
+                out[ps:pe] = part
         pos += sz
-    n_o = g_pts.shape[-1]
-    return slab.view(gA, n_kz, n_e, n_o, n_o)
+    return out.view(*out.shape[:2], *blk)
+
+
+def columns_to_points(y, ranges, n_pts: int, n_a: int, atom_major: bool, group=None):
+    """This rank's columns ``ranges[rank]`` of every point -> the point owners' rows [pts_r, NA, *blk].
+
+    ``y``: [c1-c0, n_pts, *blk] (``atom_major``) or [n_pts, c1-c0, *blk]; the
+    ranges of all ranks must partition [0, NA) (owned atoms).
+    """
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    pts = [chunk(n_pts, world, r) for r in range(world)]
+    c0, c1 = ranges[rank]
+    width = c1 - c0
+    blk = tuple(y.shape[2:])
+    nblk = int(np.prod(blk)) if blk else 1
+    flat = y.reshape(y.shape[0], y.shape[1], nblk)
+    send = flat.new_empty(n_pts * width * nblk)
+    pos = 0
+    for ps, pe in pts:
+        n = (pe - ps) * width * nblk
+        part = flat[:, ps:pe].transpose(0, 1) if atom_major else flat[ps:pe]
+        send[pos:pos + n] = part.reshape(-1)
+        pos += n
+    send_sizes = [(pe - ps) * width * nblk for ps, pe in pts]
+    ps, pe = pts[rank]
+    recv_sizes = [(pe - ps) * (r1 - r0) * nblk for r0, r1 in ranges]
+    recv = flat.new_empty(sum(recv_sizes))
+    _all_to_all(recv, send, recv_sizes, send_sizes, group)
+    out = flat.new_empty((pe - ps, n_a, nblk))
+    pos = 0
+    for (r0, r1), sz in zip(ranges, recv_sizes):
+        if r1 > r0:
+            out[:, r0:r1] = recv[pos:pos + sz].view(pe - ps, r1 - r0, nblk)
+        pos += sz
+    return out.view(pe - ps, n_a, *blk)
+
+
+def halo_ranges(idx: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Each rank's atom slab (owned atoms + every neighbour f(a, s)): the columns it reads."""
+    return [(glo, ghi) for (_, _, glo, ghi) in _slabs(idx, world)]
+
+
+def owned_ranges(n_a: int, world: int) -> list[tuple[int, int]]:
+    return [chunk(n_a, world, r) for r in range(world)]
+
+
+def points_to_atom_slab(g_pts, idx: np.ndarray, n_kz: int, n_e: int, group=None):
+    """G: [pts_r, NA, No, No] (this rank's GF points) -> atom-major slab [gA, Nkz, NE, No, No].
+
+    Collective over the group; every rank passes its own point rows.
+    """
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    slab = points_to_columns(g_pts, halo_ranges(idx, world), n_kz * n_e, True, group)
+    return slab.view(slab.shape[0], n_kz, n_e, *g_pts.shape[2:])
 
 
 def atom_slab_to_points(sig, idx: np.ndarray, n_kz: int, n_e: int, group=None):
     """Owned-atom Sigma [oA, Nkz, NE, No, No] -> this rank's GF points [pts_r, NA, No, No]."""
     import torch.distributed as dist
 
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    pts = point_chunks(n_kz, n_e, world)
-    slabs = _slabs(idx, world)
+    world = dist.get_world_size(group)
     n_a = idx.shape[0]
-    oA, n_o = sig.shape[0], sig.shape[-1]
-    no2 = n_o * n_o
-    flat = sig.reshape(oA, n_kz * n_e, no2)
-    import torch
+    y = sig.reshape(sig.shape[0], n_kz * n_e, *sig.shape[3:])
+    return columns_to_points(y, owned_ranges(n_a, world), n_kz * n_e, n_a, True, group)
 
-    send = torch.cat([flat[:, ps:pe].transpose(0, 1).reshape(-1) for (ps, pe) in pts])
-    send_sizes = [(pe - ps) * oA * no2 for (ps, pe) in pts]
-    ps, pe = pts[rank]
-    recv_sizes = [(pe - ps) * (hi - lo) * no2 for (lo, hi, _, _) in slabs]
-    recv = flat.new_empty(sum(recv_sizes))
-    _all_to_all(recv, send, recv_sizes, send_sizes, group)
-    out = flat.new_empty((pe - ps, n_a, no2))
-    pos = 0
-    for (lo, hi, _, _), sz in zip(slabs, recv_sizes):
-        if hi > lo:
-            out[:, lo:hi] = recv[pos:pos + sz].view(pe - ps, hi - lo, no2)
-        pos += sz
-    return out.view(pe - ps, n_a, n_o, n_o)
+
+def phonon_points_to_slab(d_pts, idx: np.ndarray, n_qz: int, n_w: int, group=None):
+    """Raw D from the phonon GF phase's (q, w) points [pts_r, NA, NB+1, 3, 3] -> this rank's
+    grid-major D slab [Nqz, Nw, gA, NB+1, 3, 3] (halo included: preprocess_D reads D at f(a, s))."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    slab = points_to_columns(d_pts, halo_ranges(idx, world), n_qz * n_w, False, group)
+    return slab.view(n_qz, n_w, *slab.shape[1:])
+
+
+def pi_to_points(pi_owned, n_a: int, n_qz: int, n_w: int, group=None):
+    """Owned-atom Pi [Nqz, Nw, oA, NB+1, 3, 3] -> the phonon GF phase's (q, w) point owners
+    [pts_r, NA, NB+1, 3, 3] (the Pi return of the tiled scheme)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    y = pi_owned.reshape(n_qz * n_w, *pi_owned.shape[2:])
+    return columns_to_points(y, owned_ranges(n_a, world), n_qz * n_w, n_a, False, group)
 
 
 def _all_to_all(recv, send, recv_sizes, send_sizes, group):

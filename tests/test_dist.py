@@ -206,3 +206,64 @@ def test_a2a_bytes_within_reference_tiled_model(world):
                 assert comm.optimize_tiles(rp, world).t_e == 1  # the tiling this all-to-all implements
         finally:
             sys.path.remove(ref)
+
+
+def _phonon_a2a_worker(rank, world, port, p, seed, result_q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import sse_oracle as orc
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    idx = build_neighbor_map(p.n_A, p.n_B).idx
+    rng = np.random.default_rng(seed)
+    shape = (p.n_qz, p.n_w, p.n_A, p.n_B + 1, 3, 3)
+    d_full = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    pi_full = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    n_pts = p.n_qz * p.n_w
+    ps, pe = sdist.chunk(n_pts, world, rank)
+    # D arrives from the phonon GF phase's (q, w) points; preprocess_D on the slab == on the full tensor
+    d_pts = torch.from_numpy(np.ascontiguousarray(d_full.reshape(n_pts, *shape[2:])[ps:pe]))
+    slab = sdist.phonon_points_to_slab(d_pts, idx, p.n_qz, p.n_w).numpy()
+    plan = sdist.halo_plan(idx, world, rank)
+    ok_d = np.array_equal(slab, d_full[:, :, plan.glo:plan.ghi])
+    ref_l, _ = orc.preprocess_D(d_full, d_full, idx)
+    # reverse slots need the full map: evaluate the owned rows from the slab by the same formula
+    got = np.empty_like(ref_l[:, :, plan.lo:plan.hi])
+    for a in range(plan.lo, plan.hi):
+        for s in range(p.n_B):
+            b = int(idx[a, s])
+            r = int(np.nonzero(idx[b] == a)[0][0])
+            got[:, :, a - plan.lo, s] = (slab[:, :, b - plan.glo, 1 + r] - slab[:, :, b - plan.glo, 0]
+                                         - slab[:, :, a - plan.glo, 0] + slab[:, :, a - plan.glo, 1 + s])
+    ok_pre = np.array_equal(got, ref_l[:, :, plan.lo:plan.hi])
+    # Pi of the owned atoms returns to the (q, w) point owners
+    lo, hi = sdist.chunk(p.n_A, world, rank)
+    back = sdist.pi_to_points(torch.from_numpy(np.ascontiguousarray(pi_full[:, :, lo:hi])), p.n_A, p.n_qz, p.n_w)
+    ok_pi = np.array_equal(back.numpy(), pi_full.reshape(n_pts, *shape[2:])[ps:pe])
+    res = [None] * world
+    dist.all_gather_object(res, (ok_d, ok_pre, ok_pi))
+    if rank == 0:
+        result_q.put(res)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_phonon_points_to_slab_and_pi_return(world):
+    """SURVEY 8f-3, phonon side: raw D from the (q, w)-point layout -> halo'd slabs (preprocess_D
+    on them matches the full tensor bitwise), and Pi of the owned atoms back to the point owners."""
+    import multiprocessing as mp
+
+    p = SimParams(n_kz=2, n_qz=2, n_E=7, n_w=3, n_A=11, n_B=4, n_orb=2)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_phonon_a2a_worker, args=(r, world, port, p, 6, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(all(x) for x in res), res
