@@ -534,8 +534,14 @@ def run_gpu(args, p, grid, idx) -> None:
             peer_g.tensors[pol].copy_(sdist.atom_slab_to_points(prob.g[pol][own].contiguous(), idx, p.n_kz, p.n_E))
         peer_s = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
         token = torch.zeros(1, device=prob.device)
+        # raw D still comes from the phonon (q, w) points through the (small) NCCL all-to-all
+        d_pts = [sdist.columns_to_points(prob.d[pol][:, :, own].reshape(p.n_qz * p.n_w, prob.n_owned, -1),
+                                         sdist.owned_ranges(p.n_A, world), p.n_qz * p.n_w, p.n_A, False)
+                 .view(-1, p.n_A, p.n_B + 1, 3, 3) for pol in range(2)]
 
         def fused_step():
+            for pol in range(2):
+                prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
             prob.preprocess()
             prob.sigma_peer(peer_g, peer_s)
             dist.all_reduce(token)  # every rank's peer stores done before anyone reads its points
@@ -556,9 +562,10 @@ def run_gpu(args, p, grid, idx) -> None:
         fused_info = {"s_per_step": fused_ms / 1e3, "steps": args.gf_fused_steps, "vs_halo_step": fused_ms / step_ms,
                       "sigma_points_bitwise_equal_to_all_to_all": bool(same == 1.0),
                       "note": "G read from the GF (k,E)-point owners by TMA over NVLink and Sigma stored to them "
-                              "from the K3 epilogue (CUDA IPC peer memory); preprocess_D + K2 + K3 + one "
-                              "device-side all-reduce per step"}
+                              "from the K3 epilogue (CUDA IPC peer memory); raw D from the (q,w) points by NCCL "
+                              "all-to-all; preprocess_D + K2 + K3 + one device-side all-reduce per step"}
         barrier(world)
+        del d_pts
         peer_g.close()
         peer_s.close()
 
