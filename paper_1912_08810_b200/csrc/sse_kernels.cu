@@ -1787,16 +1787,22 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
 
   if (threadIdx.x == 0)
     for (int t = 0; t < kPi3Slots - 1 && t < n_ss; ++t) produce(t);
-  int k = 0, e = e_lo;
-  int kn = 0, en = e_lo + 1;
-  if (en == e_hi) {
-    en = e_lo;
-    ++kn;
-  }
+  // loop state kept minimal (v4 runs at 128 registers): slot, phase, sub-stage j and
+  // the quad index are functions of ss; (k, e) of the stage index ss / kPi3Sub
+  static_assert((kPi3Slots & (kPi3Slots - 1)) == 0, "ring slots: power of two");
+  auto stage_ke = [&](int st, int& k_, int& e_) {
+    k_ = st / ne_c;
+    e_ = e_lo + (st - k_ * ne_c);
+  };
+  {
+    int k0, e0, k1, e1;
+    stage_ke(0, k0, e0);
+    stage_ke(n_st > 1 ? 1 : 0, k1, e1);
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    cur[t] = row_of(t, k, e);
-    nxt[t] = n_st > 1 ? row_of(t, kn, en) : cur[t];
+    for (int t = 0; t < 2; ++t) {
+      cur[t] = row_of(t, k0, e0);
+      nxt[t] = row_of(t, k1, e1);
+    }
   }
   double2 a0[2], a1[2];
 #pragma unroll
@@ -1804,9 +1810,7 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
     a0[t] = load_a(t, 0);
     a1[t] = load_a(t, 1);
   }
-  int kq = 0, j = 0, slot = 0;
-  uint32_t phase = 0;
-  // one quad: B read once per n-tile, used by both m-tiles (T = tiles in use)
+  // one quad: B read once per n-tile, used by both m-tiles
   auto quad2 = [&](const double2 (&a)[2], const double* b) {
 #pragma unroll
     for (int u = 0; u < kPi3NT; ++u) {
@@ -1834,10 +1838,17 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
     for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[0][u], a[0].y, bi[u]);
   };
   for (int ss = 0; ss < n_ss; ++ss) {
-    const int t = ss + kPi3Slots - 1;
-    if (lane == 0 && t < n_ss && t % kPi4Warps == warp) produce(t);
+    const int slot = ss & (kPi3Slots - 1);
+    const int st = ss / kPi3Sub, j = ss - st * kPi3Sub;
+    const int kq = j * QS;
+    {
+      const int t = ss + kPi3Slots - 1;
+      if (lane == 0 && t < n_ss && t % kPi4Warps == warp) produce(t);
+    }
     __syncwarp();
-    mbar_wait(full + slot, phase);
+    mbar_wait(full + slot, (uint32_t)((ss / kPi3Slots) & 1));
+    int k, e;
+    stage_ke(st, k, e);
     const bool live = active && e + off_min < p.ne;
     const double* sb = reinterpret_cast<const double*>(ring + slot * SLOT) + pcol * 2 * NCOL + b_off;
     if (live && two) {
@@ -1868,26 +1879,15 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
         }
       }
     }
-    kq += QS;
     if (lane == 0) mbar_arrive(empty + slot);
-    if (++slot == kPi3Slots) {
-      slot = 0;
-      phase ^= 1u;
-    }
-    if (++j == kPi3Sub) {
-      j = 0;
-      kq -= KHP;
-      k = kn;
-      e = en;
+    if (j == kPi3Sub - 1) {  // stage done: the next stage's rows become current
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) cur[tt] = nxt[tt];
-      if (++en == e_hi) {
-        en = e_lo;
-        ++kn;
-      }
-      if (ss + 1 + kPi3Sub < n_ss) {
+      if (st + 2 < n_st) {
+        int k2, e2;
+        stage_ke(st + 2, k2, e2);
 #pragma unroll
-        for (int tt = 0; tt < 2; ++tt) nxt[tt] = row_of(tt, kn, en);
+        for (int tt = 0; tt < 2; ++tt) nxt[tt] = row_of(tt, k2, e2);
       }
     }
   }

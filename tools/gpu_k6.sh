@@ -1,3 +1,3 @@
 export PYTHONUNBUFFERED=1
 timeout 200 python -m pytest tests/test_gpu_pi.py -q -m gpu -x 2>&1 | tail -1
-for v in 3 4; do echo "SSE_PI_KERNEL=$v"; SSE_PI_KERNEL=$v timeout 120 python tools/profile_pi.py --atoms 96 --steps 2; done
+timeout 120 python tools/profile_pi.py --atoms 96 --steps 2
