@@ -172,6 +172,17 @@ int sse_sigma_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out,
                           int nranks, const int64_t* pt_lo, double* const* S_l,
                           double* const* S_g, void* stream, sse_timing* t);
 
+/* Pi of the owned atoms [out] with G read from the point owners' GF-layout
+ * buffers (as sse_sigma_device_peer): K5 reads G2 at f(a,s), K6 reads G1
+ * rows over NVLink.  Output Pi_* device [Nqz, Nw, out.natoms, NB+1, 3, 3]
+ * (return it to the (q,w) point owners with an all-to-all).  Needs the DMMA
+ * operand build and K6 v3/v4 (No in {4, 8, 12, 16}; else returns 1). */
+int sse_pi_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out,
+                       const double* const* G_l, const double* const* G_g, const double* dH,
+                       const int64_t* nmap, const int64_t* off, double energy_weight,
+                       int nranks, const int64_t* pt_lo, double* Pi_l, double* Pi_g,
+                       void* stream, sse_timing* t);
+
 /* Library-owned device memory that can be shared with peer processes, and CUDA
  * IPC export / import of it (handles are SSE_IPC_HANDLE_BYTES opaque bytes). */
 #define SSE_IPC_HANDLE_BYTES 64

@@ -28,6 +28,7 @@ EXPORTED = (
     "sse_sigma_device",
     "sse_sigma_device_scatter",
     "sse_sigma_device_peer",
+    "sse_pi_device_peer",
     "sse_dev_alloc",
     "sse_dev_free",
     "sse_ipc_handle",
@@ -129,6 +130,7 @@ def load() -> ctypes.CDLL:
         lib.sse_sigma_device.argtypes = [_P, pdims, pslab, pslab] + [_P] * 6 + [_P, _P, _P, _P, _P, ptim]
         lib.sse_sigma_device_scatter.argtypes = [_P, pdims, pslab, pslab] + [_P] * 8 + [i32, _P, _P, _P, _P, ptim]
         lib.sse_sigma_device_peer.argtypes = [_P, pdims, pslab, _P, _P] + [_P] * 6 + [i32, _P, _P, _P, _P, ptim]
+        lib.sse_pi_device_peer.argtypes = [_P, pdims, pslab, _P, _P, _P, _P, _P, dbl, i32, _P, _P, _P, _P, ptim]
         lib.sse_dev_alloc.argtypes = [_P, ctypes.c_size_t, ctypes.POINTER(_P)]
         lib.sse_dev_free.argtypes = [_P, _P]
         lib.sse_ipc_handle.argtypes = [_P, _P, ctypes.c_char_p]

@@ -387,7 +387,7 @@ int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const ss
 int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
                  const double2* G_l, const double2* G_g, const double2* dH, const int64_t* nmap,
                  const int64_t* off, double energy_weight, const unsigned char* mask, double2* Pi_l,
-                 double2* Pi_g, cudaStream_t st, int* launches) {
+                 double2* Pi_g, cudaStream_t st, int* launches, const sse::PeerGather* peer = nullptr) {
   CHECK(prepare_tables(ds, d, g, out, nmap, off, nullptr, st));
   const unsigned char* mask_dev = nullptr;
   if (mask) {
@@ -432,6 +432,7 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
     ba.g_sk = gs.sk;
     ba.g_se = gs.se;
     ba.swz = sse::pi_vt_swizzle(no, ncol);
+    if (peer) ba.peer = *peer;
     CHECK(profiled(ds, st, SSE_PROF_PI_BUILD, 0.0, [&] { return sse::launch_pi_build(ba, st); }));
     sse::PiArgs pa{};
     pa.G[0] = G_l;
@@ -456,6 +457,7 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
     pa.g_se = gs.se;
     pa.g_atom_of_chunk0 = out.atom0 + a0 - g.atom0;
     pa.swz = ba.swz;
+    if (peer) pa.peer = *peer;
     double flops = 0;  // 8 per complex MAC, both chain polarities, valid (E + off < NE) terms
     for (int64_t w = 0; w < d->nw; ++w) flops += (double)std::max<int64_t>(0, d->ne - off[w]);
     flops *= 16.0 * n * nqz * d->nkz * no2 * ncol;
@@ -915,6 +917,53 @@ int sse_sigma_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out, 
   const sse_slab all{0, d->na, 1, 0};
   return sigma_peer_impl(ctx, d, &all, out, nullptr, nullptr, G_l, G_g, Dc_l, Dc_g, dH, nmap, off, wt, nranks,
                          pt_lo, S_l, S_g, stream, t);
+}
+
+int sse_pi_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out, const double* const* G_l,
+                       const double* const* G_g, const double* dH, const int64_t* nmap, const int64_t* off,
+                       double energy_weight, int nranks, const int64_t* pt_lo, double* Pi_l, double* Pi_g,
+                       void* stream, sse_timing* t) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
+  CHECK(validate_dims(d));
+  CHECK(validate_slab(d, out, "output"));
+  if (!G_l || !G_g || !dH || !nmap || !off || !pt_lo || !Pi_l || !Pi_g) return fail(SSE_EINVAL, "NULL tensor pointer");
+  if (nranks < 1 || nranks > sse::kMaxScatter)
+    return fail(SSE_EINVAL, "peer gather needs 1..%d ranks (got %d)", sse::kMaxScatter, nranks);
+  if (pt_lo[0] != 0 || pt_lo[nranks] != d->nkz * d->ne) return fail(SSE_EINVAL, "point ranges must cover [0, Nkz*NE)");
+  sse::PeerGather pg{};
+  pg.ranks = nranks;
+  pg.na = d->na;
+  for (int r = 0; r <= nranks; ++r) {
+    if (r > 0 && pt_lo[r] < pt_lo[r - 1]) return fail(SSE_EINVAL, "point ranges must be non-decreasing");
+    pg.pt_lo[r] = pt_lo[r];
+  }
+  for (int r = 0; r < nranks; ++r) {
+    if ((!G_l[r] || !G_g[r]) && pt_lo[r + 1] > pt_lo[r]) return fail(SSE_EINVAL, "NULL gather source");
+    pg.G[0][r] = (const double2*)G_l[r];
+    pg.G[1][r] = (const double2*)G_g[r];
+  }
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->n_devices = 1;
+    CU(cudaEventRecord(ds.ev[0], st));
+  }
+  int launches = 0;
+  const sse_slab all{0, d->na, 1, 0};
+  const int rc = pi_on_device(ds, d, all, *out, nullptr, nullptr, (const double2*)dH, nmap, off, energy_weight, nullptr,
+                              (double2*)Pi_l, (double2*)Pi_g, st, &launches, &pg);
+  if (rc == SSE_ECUDA && std::string(g_last_error).find("not supported") != std::string::npos)
+    return fail(SSE_EINVAL, "Pi peer gather needs the DMMA operand build and K6 v3/v4 (No in {4,8,12,16})");
+  CHECK(rc);
+  if (t) {
+    CU(cudaEventRecord(ds.ev[1], st));
+    CU(cudaEventSynchronize(ds.ev[1]));
+    t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
+    t->kernel_launches = launches;
+  }
+  return SSE_OK;
 }
 
 int sse_dev_alloc(sse_ctx* ctx, size_t bytes, void** out) {

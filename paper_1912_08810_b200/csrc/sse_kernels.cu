@@ -162,6 +162,14 @@ __device__ __forceinline__ double2* sigma_block(const SigmaArgs& p, int pol, int
   return p.S_rank[pol][r] + ((pt - p.pt_lo[r]) * p.scatter_na + p.scatter_atom0 + la) * (long long)(p.no * p.no);
 }
 
+// G block (k, E, atom) of a point-layout owner (PeerGather, Pi kernels)
+__device__ __forceinline__ const double2* peer_block(const PeerGather& pg, int pol, long long pt, long long atom,
+                                                     int no2) {
+  int r = 0;
+  while (r + 1 < pg.ranks && pt >= pg.pt_lo[r + 1]) ++r;
+  return pg.G[pol][r] + ((pt - pg.pt_lo[r]) * pg.na + atom) * no2;
+}
+
 // same without `volatile`: lets the scheduler interleave the shared-memory
 // operand loads with the DMMAs (the per-accumulator order is data-dependent)
 __device__ __forceinline__ void dmma884_nv(double (&c)[2], double a, double b) {
@@ -812,9 +820,11 @@ pi_build_dmma_kernel(PiBuildArgs p) {
   constexpr int kPB2Prefetch = 2;
   auto g2_elem = [&](int e_, int pol_, int x) -> double2 {
     if (p.mask && !p.mask[k * p.ne + e_]) return make_double2(0.0, 0.0);
-    const double2* G2 = pol_ ? p.G[0] : p.G[1];  // chain pol 0 (lesser): G2 = G>; pol 1: G2 = G<
     const int ss = x / NO2, rr = x % NO2;
     const long long lb = p.nbr[la * nb + ss];
+    if (p.peer.ranks > 0)  // G2 of chain pol 0 is G>, of pol 1 G<
+      return peer_block(p.peer, pol_ ? 0 : 1, (long long)k * p.ne + e_, lb, NO2)[rr];
+    const double2* G2 = pol_ ? p.G[0] : p.G[1];  // chain pol 0 (lesser): G2 = G>; pol 1: G2 = G<
     return G2[lb * p.g_sa + (long long)k * p.g_sk + (long long)e_ * p.g_se + rr];
   };
   double2 pf[kPB2Prefetch];
@@ -1554,9 +1564,10 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   auto row_of = [&](int k, int e) -> const double2* {
     int kp = k + q;
     if (kp >= p.nkz) kp -= p.nkz;
-    return (row_ok && e + off < p.ne)
-               ? g_atom + (long long)kp * p.g_sk + (long long)(e + off) * p.g_se + pcol
-               : kPiZeroRow + pcol;
+    if (!(row_ok && e + off < p.ne)) return kPiZeroRow + pcol;
+    if (p.peer.ranks > 0)
+      return peer_block(p.peer, pol, (long long)kp * p.ne + e + off, p.g_atom_of_chunk0 + la, no2) + pcol;
+    return g_atom + (long long)kp * p.g_sk + (long long)(e + off) * p.g_se + pcol;
   };
   // ragged last quad (No^2 % 4 != 0): lanes past No^2 read zeros, because the
   // slot rows they meet may hold another sub-stage's (stale, finite) B
@@ -1774,9 +1785,10 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   auto row_of = [&](int t, int k, int e) -> const double2* {
     int kp = k + q;
     if (kp >= p.nkz) kp -= p.nkz;
-    return (row_ok[t] && e + off[t] < p.ne)
-               ? g_atom + (long long)kp * p.g_sk + (long long)(e + off[t]) * p.g_se + pcol
-               : kPiZeroRow + pcol;
+    if (!(row_ok[t] && e + off[t] < p.ne)) return kPiZeroRow + pcol;
+    if (p.peer.ranks > 0)
+      return peer_block(p.peer, pol, (long long)kp * p.ne + e + off[t], p.g_atom_of_chunk0 + la, NO2) + pcol;
+    return g_atom + (long long)kp * p.g_sk + (long long)(e + off[t]) * p.g_se + pcol;
   };
   const double2 *cur[2] = {nullptr, nullptr}, *nxt[2] = {nullptr, nullptr};
   auto load_a = [&](int t, int kq) -> double2 {
@@ -2189,6 +2201,7 @@ static bool pi_build_dmma_ok(const PiBuildArgs& a) {
 
 cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
   if (a.no > kPiMaxNo) return cudaErrorInvalidValue;
+  if (a.peer.ranks > 0 && !pi_build_dmma_ok(a)) return cudaErrorNotSupported;  // peer gather: DMMA build only
   if (pi_build_dmma_ok(a)) {
     switch (a.no) {
       case 4: return launch_pi_build_dmma<4>(a, st);
@@ -2239,6 +2252,7 @@ int pi_vt_swizzle(int no, int ncol) { return (pi_kernel_choice(no, ncol) >= 3 &&
 
 cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
   const int v = pi_kernel_choice(a.no, a.ncol);
+  if (a.peer.ranks > 0 && v < 3) return cudaErrorNotSupported;  // peer gather: K6 v3 / v4 only
   if (a.swz != (v >= 3 && a.ncol % 4 == 0 ? 2 : 0)) return cudaErrorInvalidValue;  // K5 / K6 disagree
   const size_t smem = pi_smem(v, a.no, a.ncol);
   const unsigned gy = (unsigned)((a.warp_groups + kPiWarps - 1) / kPiWarps);

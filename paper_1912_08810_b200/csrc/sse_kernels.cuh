@@ -87,6 +87,16 @@ struct SigmaArgs {
 //              partial sums per E-chunk to a scratch.
 // K7 pi_assemble: sum the E-chunks in order, Pi[q,w,a,1+s] = i w_E chain,
 //              Pi[q,w,a,0] = -i sum_s w_E chain (sse.py:393-406).
+// Pi from the GF point layout: when ranks > 0, G block
+// (k, E, atom) is read from G[pol][r] + ((k*NE + E - pt_lo[r]) * na + atom) * No^2
+// of the point owner r (CUDA-IPC peer memory); atom ids are global.
+struct PeerGather {
+  int ranks;
+  long long na;
+  long long pt_lo[kMaxScatter + 1];
+  const double2* G[2][kMaxScatter];
+};
+
 struct PiBuildArgs {
   const double2* G[2];        // G slab per polarity (layout by strides)
   const double2* dH;          // [out atoms][NB][3][No][No]
@@ -97,6 +107,7 @@ struct PiBuildArgs {
   int atom_begin, chunk_atoms;  // chunk within the output slab (dH rows, nbr rows)
   long long g_sa, g_sk, g_se;
   int swz;                      // V column swizzle (pi_vt_swizzle)
+  PeerGather peer;              // ranks > 0: G2 from the point owners (DMMA build only)
 };
 struct PiArgs {
   const double2* G[2];      // G slab per polarity
@@ -110,6 +121,7 @@ struct PiArgs {
   long long g_sa, g_sk, g_se;
   long long g_atom_of_chunk0;  // G-slab index of the chunk's first output atom
   int swz;                     // V column swizzle (must match K5's)
+  PeerGather peer;             // ranks > 0: G1 from the point owners (K6 v3 / v4 only)
 };
 struct PiAssembleArgs {
   const double2* partial;

@@ -134,6 +134,18 @@ class ShardProblem:
             atom_major=True, stream=stream,
         )
 
+    def pi_peer(self, peer_g, stream=None) -> None:
+        """Pi of the owned atoms with G read from the GF point owners (dist.PeerPointBuffers)."""
+        t, p = self.torch, self.p
+        if self.pi_out is None:
+            shape = (p.n_qz, p.n_w, self.n_owned, p.n_B + 1, 3, 3)
+            self.pi_out = [t.zeros(shape, dtype=t.complex128, device=self.device) for _ in range(2)]
+        dev.pi_device_peer(
+            peer_g.remote[0], peer_g.remote[1], self.dh, self.idx[self.lo:self.hi], self.offsets,
+            self.grid.energy_weight, self.pi_out[0], self.pi_out[1], peer_g.pt_lo, n_kz=p.n_kz, n_qz=p.n_qz,
+            n_e=p.n_E, n_a=p.n_A, n_o=p.n_orb, out_atom0=self.lo, stream=stream,
+        )
+
     def step(self, exchange=None, stream=None, with_pi: bool = False) -> None:
         """One SSE evaluation: halo exchange (if any) + preprocess_D + Sigma (+ Pi)."""
         if exchange is not None:

@@ -498,6 +498,36 @@ def sigma_device_peer(
     return tim.as_dict() if sync_timing else None
 
 
+def pi_device_peer(
+    sources_l, sources_g, dh, nmap_rows: Array, offsets, energy_weight: float, out_l, out_g, pt_lo, *,
+    n_kz: int, n_qz: int, n_e: int, n_a: int, n_o: int, out_atom0: int, stream=None, sync_timing: bool = False,
+) -> dict | None:
+    """Pi of owned atoms with G read from the GF point-layout buffers of the owner ranks
+    (``sse_pi_device_peer``); out_*: device [Nqz, Nw, oA, NB+1, 3, 3]."""
+    o_atoms, n_b = dh.shape[0], dh.shape[1]
+    idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    if idx.shape != (o_atoms, n_b):
+        raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    nranks = len(sources_l)
+    if len(sources_g) != nranks or len(pt_lo) != nranks + 1:
+        raise ValueError("one source per rank and nranks + 1 point bounds")
+    n_w = out_l.shape[1]
+    offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    bounds = np.ascontiguousarray(pt_lo, dtype=np.int64)
+    arr = lambda xs: (ctypes.c_void_p * nranks)(*[int(x) for x in xs])  # noqa: E731
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, 1, 0)
+    tim = _lib.SseTiming()
+    ctx = _device_ctx(out_l)
+    rc = _lib.load().sse_pi_device_peer(
+        ctx.handle, ctypes.byref(dims), ctypes.byref(os_), arr(sources_l), arr(sources_g), _dptr(dh), _ptr(idx),
+        _ptr(offs), float(energy_weight), nranks, _ptr(bounds), _dptr(out_l), _dptr(out_g),
+        _stream_ptr(stream), ctypes.byref(tim) if sync_timing else None,
+    )
+    _lib.check(rc)
+    return tim.as_dict() if sync_timing else None
+
+
 def pi_device(
     g_l, g_g, dh, nmap_rows: Array, offsets, energy_weight: float, pi_l, pi_g, *, n_a: int, n_qz: int,
     g_atom0: int = 0, out_atom0: int = 0, atom_major: bool = False, point_mask=None, stream=None,

@@ -3,7 +3,7 @@
 Two NCCL ranks (spawned processes, one GPU each): the peer-scatter epilogue
 (``sse_sigma_device_scatter`` into CUDA-IPC-mapped buffers) and the fully fused
 variant that also reads G from the owners' point buffers with TMA
-(``sse_sigma_device_peer``) must equal, bitwise, Sigma computed into atom slabs
+(``sse_sigma_device_peer``), and Pi with G read the same way (``sse_pi_device_peer``), must equal, bitwise, Sigma computed into atom slabs
 and returned with the NCCL all-to-all (``dist.atom_slab_to_points``).
 """
 
@@ -66,6 +66,15 @@ def _worker(rank, world, port, q):
         torch.cuda.synchronize()
         dist.barrier()
         ok_fused = all(torch.equal(peer.tensors[pol], ref[pol]) for pol in range(2))
+        # Pi from the point layout too (K5 reads G2, K6 reads G1 over NVLink) == Pi from the slabs
+        prob.pi()
+        pi_ref = [t.clone() for t in prob.pi_out]
+        for t in prob.pi_out:
+            t.fill_(float("nan"))
+        prob.pi_peer(peer_g)
+        torch.cuda.synchronize()
+        ok_pi = all(torch.equal(prob.pi_out[pol], pi_ref[pol]) for pol in range(2))
+        ok_fused = ok_fused and ok_pi
         dist.barrier()
         peer_g.close()
         peer.close()
