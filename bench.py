@@ -564,6 +564,23 @@ def run_gpu(args, p, grid, idx) -> None:
                       "note": "G read from the GF (k,E)-point owners by TMA over NVLink and Sigma stored to them "
                               "from the K3 epilogue (CUDA IPC peer memory); raw D from the (q,w) points by NCCL "
                               "all-to-all; preprocess_D + K2 + K3 + one device-side all-reduce per step"}
+        if args.pi_steps > 0:
+            # Pi from the point layout too (K5 / K6 read G over NVLink), returned to the (q, w) owners
+            def fused_pi():
+                prob.pi_peer(peer_g)
+                return [sdist.pi_to_points(prob.pi_out[pol], p.n_A, p.n_qz, p.n_w) for pol in range(2)]
+
+            fused_pi()
+            torch.cuda.synchronize()
+            barrier(world)
+            start.record(stream)
+            for _ in range(args.pi_steps):
+                fused_pi()
+            end.record(stream)
+            torch.cuda.synchronize()
+            fused_info["pi_s_per_eval"] = allreduce_max(start.elapsed_time(end) / args.pi_steps, world) / 1e3
+            fused_info["pi_note"] = ("Pi with G read from the point owners (K5 G2, K6 G1 rows over NVLink) + "
+                                     "Pi to the (q,w) point owners (NCCL all-to-all)")
         barrier(world)
         del d_pts
         peer_g.close()
