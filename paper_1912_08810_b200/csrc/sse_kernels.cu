@@ -837,11 +837,19 @@ pi_build_dmma_kernel(PiBuildArgs p) {
   };
   if (e0 < e1) fetch(e0, 0);
   int step = 0;  // (point, polarity) counter: buffer = step & 1
+  auto store_v = [&](int st_, int e_, int pol_) {  // thread 0: V image of step st_ -> HBM (TMA)
+    double2* out = p.VT[pol_] + (((long long)la * p.nkz + k) * p.ne + e_) * vt_vec;
+    bulk_s2g(out, vt + (st_ & 1) * vt_vec, (uint32_t)vt_vec * 16);
+    bulk_commit();
+  };
   for (int e = e0; e < e1; ++e) {
     for (int pol = 0; pol < 2; ++pol, ++step) {
       double2* buf = vt + (step & 1) * vt_vec;
-      __syncthreads();  // sg2 / buf readers of the previous steps are done
-      if (threadIdx.x == 0 && step >= 2) bulk_wait_read<1>();  // buf's store (two steps ago) has read it
+      __syncthreads();  // step-1's products are in its buffer; sg2 is free
+      if (threadIdx.x == 0) {
+        if (step >= 1) store_v(step - 1, pol ? e : e - 1, pol ? 0 : 1);  // previous (point, polarity)
+        if (step >= 2) bulk_wait_read<1>();  // buf's store (two steps ago) has read it
+      }
 #pragma unroll
       for (int i = 0; i < kPB2Prefetch; ++i) {
         const int x = threadIdx.x + i * blockDim.x;
@@ -898,15 +906,13 @@ pi_build_dmma_kernel(PiBuildArgs p) {
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS visible to the bulk copy
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double2* out = p.VT[pol] + (((long long)la * p.nkz + k) * p.ne + e) * vt_vec;
-        bulk_s2g(out, buf, (uint32_t)vt_vec * 16);
-        bulk_commit();
-      }
     }
   }
-  if (threadIdx.x == 0) bulk_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (step >= 1) store_v(step - 1, e1 - 1, 1);
+    bulk_wait_all();
+  }
 }
 
 // --------------------------------------------------------------------------
