@@ -792,12 +792,14 @@ pi_build_dmma_kernel(PiBuildArgs p) {
   constexpr int KH = NO / 4;         // k-steps per real/imaginary half
   constexpr int NT1 = NO / 4;        // n-tiles of U (2No real columns)
   constexpr int NT2 = 3 * NO / 4;    // n-tiles of W (6No real columns)
+  constexpr int NOP = NO + 1;        // padded smem row of dH / G2 blocks: the B reads (4 rows
+                                     // of a quarter warp) hit distinct banks
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int nb = p.nb, ncol = nb * 9;
   const int vt_vec = NO2 * ncol;  // double2 per point and polarity
   double2* vt = reinterpret_cast<double2*>(smem_raw);          // [2][No2][ncol]
-  double2* sdh = vt + 2 * vt_vec;                               // [nb][3][No][No]
-  double2* sg2 = sdh + nb * 3 * NO2;                            // [nb][No][No]
+  double2* sdh = vt + 2 * vt_vec;                               // [nb][3][No][NOP]
+  double2* sg2 = sdh + nb * 3 * NO * NOP;                       // [nb][No][NOP]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e_groups = (p.ne + kPB2Energies - 1) / kPB2Energies;
   int bx = blockIdx.x;
@@ -808,7 +810,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
   const int e0 = eg * kPB2Energies, e1 = min(p.ne, e0 + kPB2Energies);
 
   const double2* dH = p.dH + (long long)(p.atom_begin + la) * nb * 3 * NO2;
-  for (int x = threadIdx.x; x < nb * 3 * NO2; x += blockDim.x) sdh[x] = dH[x];
+  for (int x = threadIdx.x; x < nb * 3 * NO2; x += blockDim.x) sdh[(x / NO) * NOP + x % NO] = dH[x];
 
   const int im = (lane >> 2) & 1;                  // this lane's B column is an imaginary part
   const unsigned neg = im ? 0u : 0x80000000u;      // the im-row of a real column is -Im
@@ -853,10 +855,10 @@ pi_build_dmma_kernel(PiBuildArgs p) {
 #pragma unroll
       for (int i = 0; i < kPB2Prefetch; ++i) {
         const int x = threadIdx.x + i * blockDim.x;
-        if (x < nb * NO2) sg2[x] = pf[i];
+        if (x < nb * NO2) sg2[(x / NO) * NOP + x % NO] = pf[i];
       }
       for (int x = threadIdx.x + kPB2Prefetch * blockDim.x; x < nb * NO2; x += blockDim.x)
-        sg2[x] = g2_elem(e, pol, x);
+        sg2[(x / NO) * NOP + x % NO] = g2_elem(e, pol, x);
       __syncthreads();
       if (pol == 0) fetch(e, 1);
       else if (e + 1 < e1) fetch(e + 1, 0);
@@ -865,8 +867,8 @@ pi_build_dmma_kernel(PiBuildArgs p) {
         const int m = mt * 8 + (lane >> 2);
         const bool m_ok = m < MROWS;
         const int mj = m_ok ? m / NO : 0, mp = m_ok ? m % NO : 0;
-        const double2* dsr = sdh + ((ss * 3 + mj) * NO + mp) * NO;  // row (j, p) of D_s
-        const double2* g2 = sg2 + ss * NO2;
+        const double2* dsr = sdh + ((ss * 3 + mj) * NO + mp) * NOP;  // row (j, p) of D_s
+        const double2* g2 = sg2 + ss * NO * NOP;
         double u[NT1][2];
 #pragma unroll
         for (int nt = 0; nt < NT1; ++nt) u[nt][0] = u[nt][1] = 0.0;
@@ -876,7 +878,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
           const double2 a = m_ok ? dsr[r] : make_double2(0.0, 0.0);
 #pragma unroll
           for (int nt = 0; nt < NT1; ++nt) {
-            const double2 g = g2[r * NO + ((nt * 8 + (lane >> 2)) >> 1)];
+            const double2 g = g2[r * NOP + ((nt * 8 + (lane >> 2)) >> 1)];
             dmma884_nv(u[nt], a.x, im ? g.y : g.x);
             dmma884_nv(u[nt], a.y, xor_sign(im ? g.x : g.y, neg));
           }
@@ -890,7 +892,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
 #pragma unroll
           for (int nt = 0; nt < NT2; ++nt) {
             const int cc = (nt * 8 + (lane >> 2)) >> 1, i = cc / NO, n = cc % NO;
-            const double2 h = sdh[((ss * 3 + i) * NO + t) * NO + n];
+            const double2 h = sdh[((ss * 3 + i) * NO + t) * NOP + n];
             dmma884_nv(w[nt], u[kh][0], im ? h.y : h.x);
             dmma884_nv(w[nt], u[kh][1], xor_sign(im ? h.x : h.y, neg));
           }
@@ -2187,7 +2189,7 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
 
 template <int NO>
 static cudaError_t launch_pi_build_dmma(const PiBuildArgs& a, cudaStream_t st) {
-  const size_t smem = ((size_t)2 * NO * NO * a.nb * 9 + (size_t)a.nb * 3 * NO * NO + (size_t)a.nb * NO * NO) * 16;
+  const size_t smem = ((size_t)2 * NO * NO * a.nb * 9 + (size_t)a.nb * 4 * NO * (NO + 1)) * 16;
   cudaError_t e = cudaFuncSetAttribute(pi_build_dmma_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPB2Energies - 1) / kPB2Energies);
@@ -2201,7 +2203,7 @@ static bool pi_build_dmma_ok(const PiBuildArgs& a) {
   const char* env = getenv("SSE_PI_BUILD");
   if (env && env[0] == '0') return false;
   if (a.no % 4 || a.no > 16) return false;
-  const size_t smem = ((size_t)2 * a.no * a.no * a.nb * 9 + (size_t)a.nb * 4 * a.no * a.no) * 16;
+  const size_t smem = ((size_t)2 * a.no * a.no * a.nb * 9 + (size_t)a.nb * 4 * a.no * (a.no + 1)) * 16;
   return smem <= 220 * 1024;
 }
 
