@@ -643,6 +643,9 @@ def run_gpu(args, p, grid, idx) -> None:
             line["parity_check_max_rel_dev"] = check
         if pi_info is not None:
             line["pi"] = pi_info
+            # the whole SSE phase of a Born iteration (sse.py:532-534): Sigma (`value`, SURVEY 8d's
+            # unit of work) + Pi, both device-resident
+            line["sse_phase_device_s"] = step_ms / 1e3 + pi_info["s_per_eval"]
         if gf_info is not None:
             line["gf_layout"] = gf_info
         if fused_info is not None:
