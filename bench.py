@@ -372,6 +372,198 @@ def load_traffic():
         return None
 
 
+def pi_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream):
+    """Pi (the other half of the SSE phase, sse.py:534) on the same resident G."""
+    import torch
+
+    from paper_1912_08810_b200.sse import Profile
+
+    if args.pi_steps <= 0:
+        return None
+    prob.pi()
+    torch.cuda.synchronize()
+    barrier(world)
+    with Profile(device=local_rank) as pprof:
+        start.record(stream)
+        for _ in range(args.pi_steps):
+            prob.pi()
+        end.record(stream)
+        torch.cuda.synchronize()
+    pi_ms = allreduce_max(start.elapsed_time(end) / args.pi_steps, world)
+    k6 = pprof.result["pi"]
+    k6_tflops = allreduce_sum(k6["flops"] / (k6["ms"] * 1e-3) / 1e12 if k6["ms"] > 0 else 0.0, world) / world
+    terms = sum(max(0, p.n_E - int(o)) for o in grid.offsets)
+    pi_flops = 16 * p.n_A * p.n_B * p.n_qz * p.n_kz * 9 * p.n_orb**2 * terms
+    pi_info = {
+        "s_per_eval": pi_ms / 1e3, "steps": args.pi_steps, "tflops": pi_flops / (pi_ms * 1e-3) / 1e12,
+        "flops_alg": pi_flops,
+        "roofline": {"bound": "tensor", "kernel": k6_kernel_name(),
+                     "achieved": k6_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": k6_tflops / FP64_PEAK_TFLOPS},
+        "kernels": {k: pprof.result[k] for k in ("pi_build", "pi", "pi_assemble")},
+        "note": "phonon self-energy Pi (sse_pi) per Born iteration, V form: chain = w_E sum <G1(E+off)^T, "
+                "dH_j G2 dH_i>; not part of `value` (north_star's path is Sigma)",
+    }
+    return pi_info
+
+
+def gf_layout_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream):
+    """the step as it follows a distributed GF phase: G from the (k, E)-point layout and raw D
+    from the (q, w) points by NCCL all-to-all into the atom slabs (halos included), Sigma back to the point
+    owners by a second all-to-all."""
+    import torch
+
+    from paper_1912_08810_b200 import dist as sdist
+
+    if args.gf_layout_steps <= 0 or world <= 1:
+        return None
+    # the GF phase's layout of the same G: rank r holds every atom of its (k, E) points;
+    # built from the owned atoms with the return collective itself
+    g_pts = [sdist.atom_slab_to_points(prob.g[pol][prob.lo - prob.glo:prob.hi - prob.glo], idx, p.n_kz, p.n_E)
+             for pol in range(2)]
+    # raw D from the phonon GF phase's (q, w) points
+    d_own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
+    d_pts = [sdist.columns_to_points(prob.d[pol][:, :, d_own].reshape(p.n_qz * p.n_w, prob.n_owned, -1),
+                                     sdist.owned_ranges(p.n_A, world), p.n_qz * p.n_w, p.n_A, False)
+             .view(-1, p.n_A, p.n_B + 1, 3, 3) for pol in range(2)]
+
+    def digest(ts):  # bit-pattern checksum (int64 wrap-around sum): equal inputs <=> equal digests
+        return [int(torch.view_as_real(t).view(torch.int64).sum()) for t in ts]
+
+    want = digest(prob.g) + digest(prob.d)
+
+    def gf_step():
+        for pol in range(2):
+            prob.g[pol].copy_(sdist.points_to_atom_slab(g_pts[pol], idx, p.n_kz, p.n_E))
+            prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
+        prob.preprocess()
+        prob.sigma()
+        return [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
+
+    gf_step()
+    torch.cuda.synchronize()
+    same = float(digest(prob.g) + digest(prob.d) == want)
+    same = -allreduce_max(-same, world)  # min over ranks
+    barrier(world)
+    start.record(stream)
+    for _ in range(args.gf_layout_steps):
+        gf_step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    gf_ms = allreduce_max(start.elapsed_time(end) / args.gf_layout_steps, world)
+    blk = p.n_orb * p.n_orb * 16
+    pts_r = p.n_kz * p.n_E / world
+    gf_info = {"s_per_step": gf_ms / 1e3, "steps": args.gf_layout_steps,
+               "vs_halo_step": gf_ms / step_ms,
+               "slab_digest_equal_to_halo_exchange": bool(same == 1.0),
+               "a2a_bytes_per_rank_approx": int(2 * pts_r * (prob.n_slab + p.n_A) * blk),
+               "note": "G from the GF (k,E)-point layout and raw D from the phonon (q,w)-point layout -> "
+                       "atom slabs (NCCL all_to_all_single, halos included) + preprocess_D + K2 + K3 + Sigma "
+                       "back to points (all_to_all_single)"}
+    del g_pts, d_pts
+    torch.cuda.empty_cache()
+    return gf_info
+
+
+def gf_fused_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream):
+    """SURVEY 8f-3 fused: G read from the GF point owners and Sigma written back to them inside the Sigma
+    kernel (NVLink peer memory via CUDA IPC): no slab assembly, halo or return collective; one device-side
+    all-reduce per step orders the peers' stores."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1912_08810_b200 import dist as sdist
+
+    if args.gf_fused_steps <= 0 or world <= 1:
+        return None
+
+    own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
+    peer_g = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
+    for pol in range(2):
+        peer_g.tensors[pol].copy_(sdist.atom_slab_to_points(prob.g[pol][own].contiguous(), idx, p.n_kz, p.n_E))
+    peer_s = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
+    token = torch.zeros(1, device=prob.device)
+    # raw D still comes from the phonon (q, w) points through the (small) NCCL all-to-all
+    d_pts = [sdist.columns_to_points(prob.d[pol][:, :, own].reshape(p.n_qz * p.n_w, prob.n_owned, -1),
+                                     sdist.owned_ranges(p.n_A, world), p.n_qz * p.n_w, p.n_A, False)
+             .view(-1, p.n_A, p.n_B + 1, 3, 3) for pol in range(2)]
+
+    def fused_step():
+        for pol in range(2):
+            prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
+        prob.preprocess()
+        prob.sigma_peer(peer_g, peer_s)
+        dist.all_reduce(token)  # every rank's peer stores done before anyone reads its points
+
+    fused_step()
+    ref_pts = [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
+    torch.cuda.synchronize()
+    same = float(all(torch.equal(peer_s.tensors[pol], ref_pts[pol]) for pol in range(2)))
+    same = -allreduce_max(-same, world)
+    del ref_pts
+    barrier(world)
+    start.record(stream)
+    for _ in range(args.gf_fused_steps):
+        fused_step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    fused_ms = allreduce_max(start.elapsed_time(end) / args.gf_fused_steps, world)
+    fused_info = {"s_per_step": fused_ms / 1e3, "steps": args.gf_fused_steps, "vs_halo_step": fused_ms / step_ms,
+                  "sigma_points_bitwise_equal_to_all_to_all": bool(same == 1.0),
+                  "note": "G read from the GF (k,E)-point owners by TMA over NVLink and Sigma stored to them "
+                          "from the K3 epilogue (CUDA IPC peer memory); raw D from the (q,w) points by NCCL "
+                          "all-to-all; preprocess_D + K2 + K3 + one device-side all-reduce per step"}
+    if args.pi_steps > 0:
+        # Pi from the point layout too (K5 / K6 read G over NVLink), returned to the (q, w) owners
+        def fused_pi():
+            prob.pi_peer(peer_g)
+            return [sdist.pi_to_points(prob.pi_out[pol], p.n_A, p.n_qz, p.n_w) for pol in range(2)]
+
+        fused_pi()
+        torch.cuda.synchronize()
+        barrier(world)
+        start.record(stream)
+        for _ in range(args.pi_steps):
+            fused_pi()
+        end.record(stream)
+        torch.cuda.synchronize()
+        fused_info["pi_s_per_eval"] = allreduce_max(start.elapsed_time(end) / args.pi_steps, world) / 1e3
+        fused_info["pi_note"] = ("Pi with G read from the point owners (K5 G2, K6 G1 rows over NVLink) + "
+                                 "Pi to the (q,w) point owners (NCCL all-to-all)")
+    barrier(world)
+    del d_pts
+    peer_g.close()
+    peer_s.close()
+    return fused_info
+
+
+def cpu_baseline_leg(args, p, grid, idx, prob):
+    """The bench's CPU leg: parity of a few Sigma blocks of this run against the oracle
+    (pointwise, host regeneration of the atom-keyed inputs) and the reference algorithm
+    (oracle port of BATCHED_FUSED) timed on a bounded sample."""
+    check = None
+    if args.check:
+        sys.path.insert(0, os.path.join(REPO, "tests"))
+        from tests.scale_helpers import host_point
+
+        worst = 0.0
+        for a in (prob.lo, prob.lo + 1, prob.hi - 1):
+            for (k, e) in ((0, p.n_E - 1), (p.n_kz - 1, p.n_E // 2)):
+                for pol in (0, 1):
+                    got = prob.sigma_block(pol, k, e, a)
+                    ref = host_point(prob, pol, k, e, a)
+                    worst = max(worst, float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)))
+        check = worst
+    cpu = None
+    if args.cpu_pairs > 0:
+        s = cpu_sample(p, grid, idx, args.cpu_pairs)
+        cpu = {"value": s["extrapolated_s"], "unit": "s", "cores": blas_threads(), "kind": "port",
+               "sample": (f"{s['pairs']} (atom, neighbour) pairs of the reference BATCHED_FUSED algorithm "
+                          f"(oracle port of sse.py:265-302) at the real per-pair shapes in {s['seconds']:.1f} s, "
+                          f"x NA*NB={p.n_A * p.n_B}; {os.cpu_count()} host cores, ~1 busy")}
+    return check, cpu
+
+
 def run_gpu(args, p, grid, idx) -> None:
     import torch
 
@@ -426,165 +618,16 @@ def run_gpu(args, p, grid, idx) -> None:
     k3_share = sig["ms"] / (step_ms * args.steps) if step_ms > 0 else None
     clk = clocks.summary() if rank == 0 else {}
 
-    # verify a few output blocks of this run (cheap host regeneration) unless disabled
-    check = None
-    if args.check and rank == 0:
-        sys.path.insert(0, os.path.join(REPO, "tests"))
-        from tests.scale_helpers import host_point
+    # cpu_baseline leg (rank 0, N = 1): the reference algorithm timed on the host cores, and the
+    # oracle as the checker of a few output blocks of this run (the only oracle use in the bench)
+    check, cpu = None, None
+    if rank == 0 and world == 1:
+        check, cpu = cpu_baseline_leg(args, p, grid, idx, prob)
 
-        worst = 0.0
-        for a in (prob.lo, prob.lo + 1, prob.hi - 1):
-            for (k, e) in ((0, p.n_E - 1), (p.n_kz - 1, p.n_E // 2)):
-                for pol in (0, 1):
-                    got = prob.sigma_block(pol, k, e, a)
-                    ref = host_point(prob, pol, k, e, a)
-                    worst = max(worst, float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)))
-        check = worst
-
-    # Pi (the other half of the SSE phase, sse.py:534) on the same resident G
-    pi_info = None
-    if args.pi_steps > 0:
-        prob.pi()
-        torch.cuda.synchronize()
-        barrier(world)
-        with Profile(device=local_rank) as pprof:
-            start.record(stream)
-            for _ in range(args.pi_steps):
-                prob.pi()
-            end.record(stream)
-            torch.cuda.synchronize()
-        pi_ms = allreduce_max(start.elapsed_time(end) / args.pi_steps, world)
-        k6 = pprof.result["pi"]
-        k6_tflops = allreduce_sum(k6["flops"] / (k6["ms"] * 1e-3) / 1e12 if k6["ms"] > 0 else 0.0, world) / world
-        terms = sum(max(0, p.n_E - int(o)) for o in grid.offsets)
-        pi_flops = 16 * p.n_A * p.n_B * p.n_qz * p.n_kz * 9 * p.n_orb**2 * terms
-        pi_info = {
-            "s_per_eval": pi_ms / 1e3, "steps": args.pi_steps, "tflops": pi_flops / (pi_ms * 1e-3) / 1e12,
-            "flops_alg": pi_flops,
-            "roofline": {"bound": "tensor", "kernel": k6_kernel_name(),
-                         "achieved": k6_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": k6_tflops / FP64_PEAK_TFLOPS},
-            "kernels": {k: pprof.result[k] for k in ("pi_build", "pi", "pi_assemble")},
-            "note": "phonon self-energy Pi (sse_pi) per Born iteration, V form: chain = w_E sum <G1(E+off)^T, "
-                    "dH_j G2 dH_i>; not part of `value` (north_star's path is Sigma)",
-        }
-
-    # the step as it follows a distributed GF phase: G arrives in the GF
-    # (k, E)-point layout, one NCCL all-to-all builds the atom slabs (halo included),
-    # Sigma returns to the point owners with a second all-to-all
-    gf_info = None
-    if args.gf_layout_steps > 0 and world > 1:
-        import torch.distributed as dist
-
-        # the GF phase's layout of the same G: rank r holds every atom of its (k, E) points;
-        # built from the owned atoms with the return collective itself
-        g_pts = [sdist.atom_slab_to_points(prob.g[pol][prob.lo - prob.glo:prob.hi - prob.glo], idx, p.n_kz, p.n_E)
-                 for pol in range(2)]
-        # raw D from the phonon GF phase's (q, w) points
-        d_own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
-        d_pts = [sdist.columns_to_points(prob.d[pol][:, :, d_own].reshape(p.n_qz * p.n_w, prob.n_owned, -1),
-                                         sdist.owned_ranges(p.n_A, world), p.n_qz * p.n_w, p.n_A, False)
-                 .view(-1, p.n_A, p.n_B + 1, 3, 3) for pol in range(2)]
-        def digest(ts):  # bit-pattern checksum (int64 wrap-around sum): equal inputs <=> equal digests
-            return [int(torch.view_as_real(t).view(torch.int64).sum()) for t in ts]
-
-        want = digest(prob.g) + digest(prob.d)
-
-        def gf_step():
-            for pol in range(2):
-                prob.g[pol].copy_(sdist.points_to_atom_slab(g_pts[pol], idx, p.n_kz, p.n_E))
-                prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
-            prob.preprocess()
-            prob.sigma()
-            return [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
-
-        gf_step()
-        torch.cuda.synchronize()
-        same = float(digest(prob.g) + digest(prob.d) == want)
-        same = -allreduce_max(-same, world)  # min over ranks
-        barrier(world)
-        start.record(stream)
-        for _ in range(args.gf_layout_steps):
-            gf_step()
-        end.record(stream)
-        torch.cuda.synchronize()
-        gf_ms = allreduce_max(start.elapsed_time(end) / args.gf_layout_steps, world)
-        blk = p.n_orb * p.n_orb * 16
-        pts_r = p.n_kz * p.n_E / world
-        gf_info = {"s_per_step": gf_ms / 1e3, "steps": args.gf_layout_steps,
-                   "vs_halo_step": gf_ms / step_ms,
-                   "slab_digest_equal_to_halo_exchange": bool(same == 1.0),
-                   "a2a_bytes_per_rank_approx": int(2 * pts_r * (prob.n_slab + p.n_A) * blk),
-                   "note": "G from the GF (k,E)-point layout and raw D from the phonon (q,w)-point layout -> "
-                           "atom slabs (NCCL all_to_all_single, halos included) + preprocess_D + K2 + K3 + Sigma "
-                           "back to points (all_to_all_single)"}
-        del g_pts, d_pts
-        torch.cuda.empty_cache()
-
-    # SURVEY 8f-3 fused: G read from the GF point owners and Sigma written back to them inside
-    # the Sigma kernel (NVLink peer memory via CUDA IPC): no slab assembly, halo or return
-    # collective; one device-side all-reduce per step orders the peers' stores
-    fused_info = None
-    if args.gf_fused_steps > 0 and world > 1:
-        import torch.distributed as dist
-
-        own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
-        peer_g = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
-        for pol in range(2):
-            peer_g.tensors[pol].copy_(sdist.atom_slab_to_points(prob.g[pol][own].contiguous(), idx, p.n_kz, p.n_E))
-        peer_s = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=local_rank)
-        token = torch.zeros(1, device=prob.device)
-        # raw D still comes from the phonon (q, w) points through the (small) NCCL all-to-all
-        d_pts = [sdist.columns_to_points(prob.d[pol][:, :, own].reshape(p.n_qz * p.n_w, prob.n_owned, -1),
-                                         sdist.owned_ranges(p.n_A, world), p.n_qz * p.n_w, p.n_A, False)
-                 .view(-1, p.n_A, p.n_B + 1, 3, 3) for pol in range(2)]
-
-        def fused_step():
-            for pol in range(2):
-                prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
-            prob.preprocess()
-            prob.sigma_peer(peer_g, peer_s)
-            dist.all_reduce(token)  # every rank's peer stores done before anyone reads its points
-
-        fused_step()
-        ref_pts = [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
-        torch.cuda.synchronize()
-        same = float(all(torch.equal(peer_s.tensors[pol], ref_pts[pol]) for pol in range(2)))
-        same = -allreduce_max(-same, world)
-        del ref_pts
-        barrier(world)
-        start.record(stream)
-        for _ in range(args.gf_fused_steps):
-            fused_step()
-        end.record(stream)
-        torch.cuda.synchronize()
-        fused_ms = allreduce_max(start.elapsed_time(end) / args.gf_fused_steps, world)
-        fused_info = {"s_per_step": fused_ms / 1e3, "steps": args.gf_fused_steps, "vs_halo_step": fused_ms / step_ms,
-                      "sigma_points_bitwise_equal_to_all_to_all": bool(same == 1.0),
-                      "note": "G read from the GF (k,E)-point owners by TMA over NVLink and Sigma stored to them "
-                              "from the K3 epilogue (CUDA IPC peer memory); raw D from the (q,w) points by NCCL "
-                              "all-to-all; preprocess_D + K2 + K3 + one device-side all-reduce per step"}
-        if args.pi_steps > 0:
-            # Pi from the point layout too (K5 / K6 read G over NVLink), returned to the (q, w) owners
-            def fused_pi():
-                prob.pi_peer(peer_g)
-                return [sdist.pi_to_points(prob.pi_out[pol], p.n_A, p.n_qz, p.n_w) for pol in range(2)]
-
-            fused_pi()
-            torch.cuda.synchronize()
-            barrier(world)
-            start.record(stream)
-            for _ in range(args.pi_steps):
-                fused_pi()
-            end.record(stream)
-            torch.cuda.synchronize()
-            fused_info["pi_s_per_eval"] = allreduce_max(start.elapsed_time(end) / args.pi_steps, world) / 1e3
-            fused_info["pi_note"] = ("Pi with G read from the point owners (K5 G2, K6 G1 rows over NVLink) + "
-                                     "Pi to the (q,w) point owners (NCCL all-to-all)")
-        barrier(world)
-        del d_pts
-        peer_g.close()
-        peer_s.close()
+    common = (args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream)
+    pi_info = pi_phase(*common)
+    gf_info = gf_layout_phase(*common)
+    fused_info = gf_fused_phase(*common)
 
     prob.free()
     del prob
@@ -600,13 +643,6 @@ def run_gpu(args, p, grid, idx) -> None:
     if args.phase_steps > 0 and world == 1:
         phase = phase_e2e(args, p, grid, idx, local_rank)
 
-    cpu = None
-    if rank == 0 and world == 1 and args.cpu_pairs > 0:
-        s = cpu_sample(p, grid, idx, args.cpu_pairs)
-        cpu = {"value": s["extrapolated_s"], "unit": "s", "cores": blas_threads(), "kind": "port",
-               "sample": (f"{s['pairs']} (atom, neighbour) pairs of the reference BATCHED_FUSED algorithm "
-                          f"(oracle port of sse.py:265-302) at the real per-pair shapes in {s['seconds']:.1f} s, "
-                          f"x NA*NB={p.n_A * p.n_B}; {os.cpu_count()} host cores, ~1 busy")}
 
     if rank == 0:
         traffic = load_traffic()
