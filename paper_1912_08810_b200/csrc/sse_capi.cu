@@ -591,13 +591,26 @@ int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi,
     CU(cudaEventRecord(ds.ev[2], st));
     CU(cudaStreamWaitEvent(ds.s_h2d, ds.ev[2], 0));
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(op_chunk_atoms(d), (on + 7) / 8));
+    // chunk boundaries: a small first chunk (its H2D is not hidden) and a small last chunk
+    // (its D2H is not hidden), regular chunks in between
+    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(32, chunk / 4));
+    std::vector<int64_t> bounds{0};
+    if (on > 2 * edge + chunk) {
+      bounds.push_back(edge);
+      while (bounds.back() + chunk < on - edge) bounds.push_back(bounds.back() + chunk);
+      bounds.push_back(on - edge);
+    } else {
+      while (bounds.back() + chunk < on) bounds.push_back(bounds.back() + chunk);
+    }
+    bounds.push_back(on);
     const DevPtrs ptr{ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dc[0].as<double2>(),
                       ds.dc[1].as<double2>(), ds.dh.as<double2>(), ds.s[0].as<double2>(),
                       ds.s[1].as<double2>()};
     int64_t copied = glo;  // G columns [glo, copied) are on their way
     size_t ei = 0;
-    for (int64_t a0 = 0; a0 < on; a0 += chunk) {
-      const int64_t n = std::min<int64_t>(chunk, on - a0);
+    for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
+      const int64_t a0 = bounds[ci], n = bounds[ci + 1] - bounds[ci];
+      if (n <= 0) continue;
       int64_t need = copied;
       for (int64_t i = a0 * d->nb; i < (a0 + n) * d->nb; ++i) need = std::max(need, rows_nmap[i] + 1);
       need = std::max(need, lo + a0 + n);
