@@ -18,6 +18,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -387,7 +388,8 @@ int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const ss
 int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
                  const double2* G_l, const double2* G_g, const double2* dH, const int64_t* nmap,
                  const int64_t* off, double energy_weight, const unsigned char* mask, double2* Pi_l,
-                 double2* Pi_g, cudaStream_t st, int* launches, const sse::PeerGather* peer = nullptr) {
+                 double2* Pi_g, cudaStream_t st, int* launches, const sse::PeerGather* peer = nullptr,
+                 const std::function<int(int64_t, int64_t)>& before_chunk = nullptr) {
   CHECK(prepare_tables(ds, d, g, out, nmap, off, nullptr, st));
   const unsigned char* mask_dev = nullptr;
   if (mask) {
@@ -414,6 +416,7 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
   const SlabStrides gs = strides_of(d, g);
   for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk) {
     const int n = (int)std::min<int64_t>(chunk, out.natoms - a0);
+    if (before_chunk) CHECK(before_chunk(a0, n));  // e.g. the host call's progressive G upload
     sse::PiBuildArgs ba{};
     ba.G[0] = G_l;
     ba.G[1] = G_g;
@@ -1090,15 +1093,33 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
     CHECK(ds.dh.ensure(on * dh_atom));
     CU(cudaEventRecord(ds.ev[0], st));
     const char* Gh[2] = {(const char*)G_l, (const char*)G_g};
-    for (int p = 0; p < 2; ++p)
-      CU(cudaMemcpy2DAsync(ds.g[p].ptr, gn * blk, Gh[p] + glo * blk, d->na * blk, gn * blk, rows,
-                           cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(ds.dh.ptr, (const char*)dH + lo * dh_atom, on * dh_atom, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(ds.ev[2], st));
+    CU(cudaStreamWaitEvent(ds.s_h2d, ds.ev[2], 0));
+    // G columns are uploaded progressively on the copy stream: atom chunk [a0, a0 + n) waits only
+    // for the columns it reads (its atoms and their neighbours), the rest streams under the kernels
+    int64_t copied = glo;
+    size_t ei = 0;
+    auto before_chunk = [&](int64_t a0, int64_t n) -> int {
+      int64_t need = std::max<int64_t>(copied, lo + a0 + n);
+      for (int64_t i = (lo + a0) * d->nb; i < (lo + a0 + n) * d->nb; ++i) need = std::max(need, nmap[i] + 1);
+      if (need > copied) {
+        for (int p = 0; p < 2; ++p)
+          CU(cudaMemcpy2DAsync((char*)ds.g[p].ptr + (copied - glo) * blk, gn * blk, Gh[p] + copied * blk,
+                               d->na * blk, (need - copied) * blk, rows, cudaMemcpyHostToDevice, ds.s_h2d));
+        copied = need;
+      }
+      cudaEvent_t in = pipe_event(ds, ei++);
+      if (!in) return fail(SSE_ECUDA, "event creation failed");
+      CU(cudaEventRecord(in, ds.s_h2d));
+      CU(cudaStreamWaitEvent(st, in, 0));
+      return SSE_OK;
+    };
     int launches = 0;
     const sse_slab gs{glo, gn, 0, 0}, os{lo, on, 0, 0};
     CHECK(pi_on_device(ds, d, gs, os, ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dh.as<double2>(),
                        nmap + lo * d->nb, off, energy_weight, mask, ds.pi_out[0].as<double2>(),
-                       ds.pi_out[1].as<double2>(), st, &launches));
+                       ds.pi_out[1].as<double2>(), st, &launches, nullptr, before_chunk));
     double* Ph[2] = {Pi_l, Pi_g};
     for (int p = 0; p < 2; ++p)
       CU(cudaMemcpy2DAsync((char*)Ph[p] + lo * pi_row, d->na * pi_row, ds.pi_out[p].ptr, on * pi_row,
