@@ -476,7 +476,7 @@ struct SlideGeom {
   static constexpr int kRing = kNeed <= 32 ? 32 : (kNeed <= 64 ? 64 : 128);
   static constexpr int kBVec = frag_geom(NO).fv * 32;            // double2 per M stage
   static constexpr size_t kSmem = (size_t)kSlideStages * kBVec * 16 + (size_t)kRing * NO * NO * 16 +
-                                  2 * kSlideStages * 8 + kMaxSlideNw * 4;
+                                  2 * kSlideStages * 8 + kMaxSlideNw * 4 + (size_t)NO * NO * 16;
   static constexpr bool kFits = kSmem <= 225 * 1024;
 };
 
@@ -533,6 +533,9 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 
   int* s_off = reinterpret_cast<int*>(empty + SB);  // frequency offsets (p.nw <= kMaxSlideNw)
   for (int w = threadIdx.x; w < p.nw; w += blockDim.x) s_off[w] = offs[w];
+  // a zero block: rows outside the matrix or with E - off < 0 read it (no per-element predicates)
+  double2* zero_blk = reinterpret_cast<double2*>(s_off + kMaxSlideNw);
+  for (int x = threadIdx.x; x < BLK; x += blockDim.x) zero_blk[x] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < SB; ++s) {
       mbar_init(full + s, 1);
@@ -602,11 +605,15 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 #pragma unroll
       for (int tt = 0; tt < MT; ++tt) {
         const bool ok = v_row[tt] && e_row[tt] >= off;
-        const double2* src = ring_a + ((fbase - e_row[tt]) & (R - 1)) * BLK + m_off[tt];
+        const double2* src = ok ? ring_a + ((fbase - e_row[tt]) & (R - 1)) * BLK + m_off[tt] : zero_blk + pcol;
 #pragma unroll
         for (int kk = 0; kk < KH; ++kk) {
-          st.a[tt][kk] = make_double2(0.0, 0.0);
-          if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO)) st.a[tt][kk] = src[4 * kk];
+          if (NO % 4 == 0) {
+            st.a[tt][kk] = src[4 * kk];
+          } else {
+            st.a[tt][kk] = make_double2(0.0, 0.0);
+            if (ok && pcol + 4 * kk < NO) st.a[tt][kk] = src[4 * kk];
+          }
         }
       }
     }
