@@ -557,7 +557,10 @@ def pi_device(
 
 
 def layout_transform(src, dst, to_atom_major: bool, stream=None) -> None:
-    """K1 (sse.py:48-55): [Nkz,NE,NA,No,No] <-> [NA,Nkz,NE,No,No] on the GPU."""
+    """K1 (sse.py:48-55): [Nkz,NE,NA,No,No] <-> [NA,Nkz,NE,No,No] on the GPU.
+
+    Any trailing block works: the phonon tensors [Nqz,Nw,NA,NB+1,3,3] <-> [NA,Nqz,Nw,NB+1,3,3] too.
+    """
     if to_atom_major:
         n_kz, n_e, n_a = src.shape[:3]
     else:

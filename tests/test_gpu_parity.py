@@ -259,6 +259,15 @@ def test_layout_transform_kernel_bitwise():
     torch.cuda.synchronize()
     assert np.array_equal(am.cpu().numpy(), np.moveaxis(c.g_l, 2, 0))
     assert np.array_equal(back.cpu().numpy(), c.g_l)
+    # the phonon tensor D[qz, w, atom, neighbour, 3, 3] -> atom-major (north_star item 1)
+    d = torch.from_numpy(c.d_l).cuda()
+    dam = torch.empty((c.p.n_A, c.p.n_qz, c.p.n_w, c.p.n_B + 1, 3, 3), dtype=torch.complex128, device="cuda")
+    dback = torch.empty_like(d)
+    dev.layout_transform(d, dam, to_atom_major=True)
+    dev.layout_transform(dam, dback, to_atom_major=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(dam.cpu().numpy(), np.moveaxis(c.d_l, 2, 0))
+    assert np.array_equal(dback.cpu().numpy(), c.d_l)
 
 
 def test_preprocess_D_device_bitwise():
