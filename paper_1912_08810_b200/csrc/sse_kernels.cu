@@ -1716,8 +1716,11 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
 // --------------------------------------------------------------------------
 constexpr int kPi4Warps = 5;
 
-template <int NOT, int NBT>
-__global__ void __launch_bounds__(kPi4Warps * 32, 3)
+// TAIL: the CTA is (atom, chain polarity, E-chunk) and warp w computes the LAST lag
+// tile for momentum q = w (all Nqz warps share the V stages); the main launch then
+// covers the first 2*NW tiles per q (paper: 8 + 1 lag tiles, 4 warps per SMSP).
+template <int NOT, int NBT, int NW = kPi4Warps, int SL = kPi3Slots, int MINB = 3, bool TAIL = false>
+__global__ void __launch_bounds__(NW * 32, MINB)
 pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   constexpr int NO2 = NOT * NOT, NCOL = 9 * NBT;
   constexpr int KHP = (NO2 + 3) / 4;
@@ -1727,28 +1730,28 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   constexpr int SLOT = QS * 4 * NCOL;  // double2 per slot
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* ring = reinterpret_cast<double2*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kPi3Slots * SLOT + kPi2Pad);
-  uint64_t* empty = full + kPi3Slots;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + SL * SLOT + kPi2Pad);
+  uint64_t* empty = full + SL;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx = blockIdx.x;
-  const int q = bx % p.nqz;
-  bx /= p.nqz;
+  const int q = TAIL ? warp : bx % p.nqz;
+  if (!TAIL) bx /= p.nqz;
   const int ec = bx % p.echunks;
   bx /= p.echunks;
   const int pol = bx % 2;
   const int la = bx / 2;
   const int m_tiles = (p.nw + 7) / 8;
-  const int wg = blockIdx.y * kPi4Warps + warp;
-  const int mt0 = 2 * wg;
-  const bool active = mt0 < m_tiles;
-  const bool two = mt0 + 1 < m_tiles;  // warp-uniform
+  const int wg = blockIdx.y * NW + warp;
+  const int mt0 = TAIL ? m_tiles - 1 : 2 * wg;
+  const bool active = TAIL ? warp < p.nqz : mt0 < m_tiles;
+  const bool two = !TAIL && mt0 + 1 < m_tiles;  // warp-uniform
   const int pcol = lane & 3;
 
-  for (int i = threadIdx.x; i < kPi3Slots * SLOT + kPi2Pad; i += blockDim.x) ring[i] = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < SL * SLOT + kPi2Pad; i += blockDim.x) ring[i] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kPi3Slots; ++s) {
+    for (int s = 0; s < SL; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kPi4Warps);
+      mbar_init(empty + s, NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1789,8 +1792,8 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   const int n_ss = kPi3Sub * n_st;
 
   auto produce = [&](int t) {
-    const int slot = t % kPi3Slots;
-    if (t >= kPi3Slots) mbar_wait(empty + slot, (uint32_t)(((t - kPi3Slots) / kPi3Slots) & 1));
+    const int slot = t % SL;
+    if (t >= SL) mbar_wait(empty + slot, (uint32_t)(((t - SL) / SL) & 1));
     const int st = t / kPi3Sub, j = t % kPi3Sub;
     const int k = st / ne_c, e = e_lo + st % ne_c;
     constexpr uint32_t bytes = (uint32_t)SLOT * 16;
@@ -1813,10 +1816,9 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   };
 
   if (threadIdx.x == 0)
-    for (int t = 0; t < kPi3Slots - 1 && t < n_ss; ++t) produce(t);
+    for (int t = 0; t < SL - 1 && t < n_ss; ++t) produce(t);
   // loop state kept minimal (v4 runs at 128 registers): slot, phase, sub-stage j and
   // the quad index are functions of ss; (k, e) of the stage index ss / kPi3Sub
-  static_assert((kPi3Slots & (kPi3Slots - 1)) == 0, "ring slots: power of two");
   auto stage_ke = [&](int st, int& k_, int& e_) {
     k_ = st / ne_c;
     e_ = e_lo + (st - k_ * ne_c);
@@ -1865,15 +1867,15 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
     for (int u = 0; u < kPi3NT; ++u) dmma884_nv(acc[0][u], a[0].y, bi[u]);
   };
   for (int ss = 0; ss < n_ss; ++ss) {
-    const int slot = ss & (kPi3Slots - 1);
+    const int slot = ss % SL;
     const int st = ss / kPi3Sub, j = ss - st * kPi3Sub;
     const int kq = j * QS;
     {
-      const int t = ss + kPi3Slots - 1;
-      if (lane == 0 && t < n_ss && t % kPi4Warps == warp) produce(t);
+      const int t = ss + SL - 1;
+      if (lane == 0 && t < n_ss && t % NW == warp) produce(t);
     }
     __syncwarp();
-    mbar_wait(full + slot, (uint32_t)((ss / kPi3Slots) & 1));
+    mbar_wait(full + slot, (uint32_t)((ss / SL) & 1));
     int k, e;
     stage_ke(st, k, e);
     const bool live = active && e + off_min < p.ne;
@@ -2280,6 +2282,28 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(pi_dmma4_kernel<12, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
       const int pairs = ((a.nw + 7) / 8 + 1) / 2;
+      const char* w4 = getenv("SSE_PI_V4_WARPS");
+      const int m_tiles = (a.nw + 7) / 8;
+      const bool split = !(w4 && w4[0] == '5') && m_tiles == 9 && a.nqz >= 1 && a.nqz <= 4;
+      if (split || (w4 && w4[0] == '4')) {
+        // 4 warps x 2 lag tiles per CTA (4 CTAs, 16 warps per SM: 4 per SMSP) for tiles 0..7,
+        // then (split) the 9th tile of every q in one tail CTA per (atom, polarity, E-chunk)
+        auto kern = pi_dmma4_kernel<12, 4, 4, 3, 4>;
+        const size_t slot = (size_t)2 * ((((a.no * a.no + 3) / 4) + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) * 4 * a.ncol * 16;
+        const size_t smem4 = smem - (size_t)(kPi3Slots - 3) * slot;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        kern<<<dim3(gx, split ? 1u : (unsigned)((pairs + 3) / 4)), 4 * 32, smem4, st>>>(a, chunk_atoms);
+        if (split) {
+          auto tail = pi_dmma4_kernel<12, 4, 4, 3, 4, true>;
+          e = cudaFuncSetAttribute(tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+          if (e == cudaSuccess) e = cudaFuncSetAttribute(tail, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          if (e != cudaSuccess) return e;
+          tail<<<dim3((unsigned)((long long)chunk_atoms * 2 * a.echunks)), 4 * 32, smem4, st>>>(a, chunk_atoms);
+        }
+        break;
+      }
       pi_dmma4_kernel<12, 4><<<dim3(gx, (unsigned)((pairs + kPi4Warps - 1) / kPi4Warps)), kPi4Warps * 32, smem, st>>>(
           a, chunk_atoms);
       break;

@@ -190,3 +190,23 @@ def test_pi_device_api_slab_bitwise():
     torch.cuda.synchronize()
     assert np.array_equal(pl.cpu().numpy(), full.lesser[:, :, lo:hi])
     assert np.array_equal(pg.cpu().numpy(), full.greater[:, :, lo:hi])
+
+
+def test_pi_split_lag_tiles_bitwise(monkeypatch):
+    """Paper shapes with 9 lag tiles (Nw in 65..72): K6 v4 runs tiles 0..7 with 4 warps per CTA plus a
+    tail CTA computing the 9th tile of every q; bitwise equal to the unsplit v4 and to v3."""
+    p = SimParams(n_kz=2, n_qz=2, n_E=72, n_w=66, n_A=5, n_B=4, n_orb=12)
+    g_l, g_g, _, _, dh = inputs.stream_instance(8, p, dh_scale=0.05)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    outs = []
+    for kernel, warps in (("4", None), ("4", "5"), ("3", None)):
+        monkeypatch.setenv("SSE_PI_KERNEL", kernel)
+        if warps:
+            monkeypatch.setenv("SSE_PI_V4_WARPS", warps)
+        else:
+            monkeypatch.delenv("SSE_PI_V4_WARPS", raising=False)
+        outs.append(sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, p.n_qz))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
+    assert np.abs(outs[0].lesser).max() > 0

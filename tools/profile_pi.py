@@ -18,8 +18,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="paper")
 ap.add_argument("--atoms", type=int, default=64)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--nw", type=int, default=0, help="override the number of phonon frequencies")
 args = ap.parse_args()
 p, grid, nmap = config(args.config)
+if args.nw:
+    import dataclasses
+
+    from paper_1912_08810_b200.types import default_grid
+
+    p = dataclasses.replace(p, n_w=args.nw)
+    grid = default_grid(p)
 world = max(1, p.n_A // args.atoms)
 prob = ShardProblem(p, rank=world // 2, world=world, seed=0, grid=grid, idx=nmap.idx)
 prob.allocate()
