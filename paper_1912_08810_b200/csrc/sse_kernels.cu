@@ -1719,7 +1719,7 @@ constexpr int kPi4Warps = 5;
 // TAIL: the CTA is (atom, chain polarity, E-chunk) and warp w computes the LAST lag
 // tile for momentum q = w (all Nqz warps share the V stages); the main launch then
 // covers the first 2*NW tiles per q (paper: 8 + 1 lag tiles, 4 warps per SMSP).
-template <int NOT, int NBT, int NW = kPi4Warps, int SL = kPi3Slots, int MINB = 3, bool TAIL = false>
+template <int NOT, int NBT, int NW = kPi4Warps, int SL = kPi3Slots, int MINB = 3, bool TAIL_CTAS = false>
 __global__ void __launch_bounds__(NW * 32, MINB)
 pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   constexpr int NO2 = NOT * NOT, NCOL = 9 * NBT;
@@ -1734,6 +1734,11 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   uint64_t* empty = full + SL;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx = blockIdx.x;
+  // TAIL_CTAS: CTAs past the main grid (chunk x 2 x echunks x Nqz) are tail CTAs, one per
+  // (atom, polarity, E-chunk); they run after the main CTAs in the same launch
+  const int main_ctas = chunk_atoms * 2 * p.echunks * p.nqz;
+  const bool TAIL = TAIL_CTAS && bx >= main_ctas;
+  if (TAIL) bx -= main_ctas;
   const int q = TAIL ? warp : bx % p.nqz;
   if (!TAIL) bx /= p.nqz;
   const int ec = bx % p.echunks;
@@ -2294,13 +2299,14 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
-        kern<<<dim3(gx, split ? 1u : (unsigned)((pairs + 3) / 4)), 4 * 32, smem4, st>>>(a, chunk_atoms);
-        if (split) {
-          auto tail = pi_dmma4_kernel<12, 4, 4, 3, 4, true>;
-          e = cudaFuncSetAttribute(tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
-          if (e == cudaSuccess) e = cudaFuncSetAttribute(tail, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (split) {  // main and tail CTAs in one launch (the tail CTAs fill the last wave)
+          auto both = pi_dmma4_kernel<12, 4, 4, 3, 4, true>;
+          e = cudaFuncSetAttribute(both, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+          if (e == cudaSuccess) e = cudaFuncSetAttribute(both, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
           if (e != cudaSuccess) return e;
-          tail<<<dim3((unsigned)((long long)chunk_atoms * 2 * a.echunks)), 4 * 32, smem4, st>>>(a, chunk_atoms);
+          both<<<dim3(gx + (unsigned)((long long)chunk_atoms * 2 * a.echunks), 1u), 4 * 32, smem4, st>>>(a, chunk_atoms);
+        } else {
+          kern<<<dim3(gx, (unsigned)((pairs + 3) / 4)), 4 * 32, smem4, st>>>(a, chunk_atoms);
         }
         break;
       }
