@@ -53,7 +53,8 @@ def k6_kernel_name() -> str:
         "2": "pi_dmma2_kernel (K6 v2, half stages)",
         "3": "pi_dmma3_kernel (K6 v3: one m-tile x 9 n-tiles per warp, TMA ring of V, 3 CTAs/SM)",
     }.get(os.environ.get("SSE_PI_KERNEL", "4"),
-          "pi_dmma4_kernel<12,4> (K6 v4: two m-tiles x 9 n-tiles per warp, TMA ring of V, 3 CTAs/SM)")
+          "pi_dmma4_kernel<12,4,4,3,4,true> (K6 v4: 2 lag tiles x 9 n-tiles per warp, 4-warp CTAs for lag "
+          "tiles 0-7 + tail CTAs for the 9th tile of every q in the same launch, TMA ring of V)")
 
 
 def env_rank():
