@@ -189,6 +189,16 @@ __device__ __forceinline__ double xor_sign(double x, unsigned mask) {
   return r;
 }
 
+// Column swizzle of the V rows (kappa = n*No + p): mode 2 flips column bit 1 with kappa bit 1
+// (K6 v3 reads rows kappa..kappa+3 conflict-free); mode 3 also XORs (n & 3), so K5's scatter
+// (whose lanes differ in n) spreads over the banks while K6 v4's quads (one n each) stay conflict-free
+__device__ __forceinline__ int vt_swz(int kap, int no, int swz) {
+  if (swz == 0) return 0;
+  int x = ((kap >> 1) & 1) ? 2 : 0;
+  if (swz == 3) x ^= (kap / no) & 3;
+  return x;
+}
+
 template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32)
 sigma_dmma_kernel(SigmaArgs p) {
@@ -755,7 +765,7 @@ pi_build_kernel(PiBuildArgs p) {
             }
           }
           const int kap = n * no + pp;
-          out[(long long)kap * ncol + (c ^ (((kap >> 1) & 1) ? p.swz : 0))] =
+          out[(long long)kap * ncol + (c ^ vt_swz(kap, no, p.swz))] =
               masked ? make_double2(0.0, 0.0) : make_double2(re, im);
         }
       }
@@ -910,7 +920,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
             const int cc = nt * 4 + kl, i = cc / NO, n = cc % NO;
             const int kap = n * NO + mp;
             const int c = ss * 9 + i * 3 + mj;
-            buf[kap * ncol + (c ^ (((kap >> 1) & 1) ? p.swz : 0))] = make_double2(w[nt][0], w[nt][1]);
+            buf[kap * ncol + (c ^ vt_swz(kap, NO, p.swz))] = make_double2(w[nt][0], w[nt][1]);
           }
         }
       }
@@ -1781,7 +1791,10 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
   const int nc0 = lane >> 2;
   const int im = nc0 & 1;
-  const int b_off = 2 * ((nc0 >> 1) ^ (((pcol >> 1) & 1) ? p.swz : 0)) + im;
+  const int c1 = (nc0 >> 1) ^ (((pcol >> 1) & 1) ? 2 : 0);  // column of tile 0 after the kappa-bit-1 flip
+  const int b_off = 2 * (p.swz ? c1 : (nc0 >> 1)) + im;
+  // swizzle mode 3: quad kq (rows n = kq / 3) also XORs the column with (n & 3): offset in doubles
+  auto n_delta = [&](int n) -> int { return p.swz == 3 ? 2 * ((c1 ^ (n & 3)) - c1) : 0; };
   const int b_dim = im ? -1 : 1;
   const unsigned b_mask = im ? 0u : 0x80000000u;
 
@@ -1885,22 +1898,26 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
     stage_ke(st, k, e);
     const bool live = active && e + off_min < p.ne;
     const double* sb = reinterpret_cast<const double*>(ring + slot * SLOT) + pcol * 2 * NCOL + b_off;
+    // the sub-stage's quads kq .. kq+5 span rows n = kq/3 (quads 0-2) and kq/3 + 1 (quads 3-5)
+    static_assert(QS == 6, "mode-3 swizzle deltas assume 6 quads per sub-stage");
+    const int dn0 = n_delta(kq / 3), dn1 = n_delta(kq / 3 + 1);
+    auto dq = [&](int qd) { return qd < 3 ? dn0 : dn1; };
     if (live && two) {
 #pragma unroll
       for (int pr = 0; pr < QS / 2; ++pr) {
-        quad2(a0, sb + 16 * pr * NCOL);
+        quad2(a0, sb + 16 * pr * NCOL + dq(2 * pr));
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) a0[tt] = load_a(tt, kq + 2 * pr + 2);
-        quad2(a1, sb + (16 * pr + 8) * NCOL);
+        quad2(a1, sb + (16 * pr + 8) * NCOL + dq(2 * pr + 1));
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) a1[tt] = load_a(tt, kq + 2 * pr + 3);
       }
     } else if (live) {
 #pragma unroll
       for (int pr = 0; pr < QS / 2; ++pr) {
-        quad1(a0, sb + 16 * pr * NCOL);
+        quad1(a0, sb + 16 * pr * NCOL + dq(2 * pr));
         a0[0] = load_a(0, kq + 2 * pr + 2);
-        quad1(a1, sb + (16 * pr + 8) * NCOL);
+        quad1(a1, sb + (16 * pr + 8) * NCOL + dq(2 * pr + 1));
         a1[0] = load_a(0, kq + 2 * pr + 3);
       }
     } else {
@@ -2270,12 +2287,16 @@ static int pi_kernel_choice(int no, int ncol) {
 }
 // column swizzle of V rows for K6 v3 (conflict-free B reads): column c of
 // kappa row r is stored at c ^ (2 * ((r >> 1) & 1)); needs ncol % 4 == 0
-int pi_vt_swizzle(int no, int ncol) { return (pi_kernel_choice(no, ncol) >= 3 && ncol % 4 == 0) ? 2 : 0; }
+int pi_vt_swizzle(int no, int ncol) {
+  const int v = pi_kernel_choice(no, ncol);
+  if (ncol % 4 || v < 3) return 0;
+  return v == 4 ? 3 : 2;  // v4 (paper shapes): the mode-3 swizzle; v3: mode 2
+}
 
 cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
   const int v = pi_kernel_choice(a.no, a.ncol);
   if (a.peer.ranks > 0 && v < 3) return cudaErrorNotSupported;  // peer gather: K6 v3 / v4 only
-  if (a.swz != (v >= 3 && a.ncol % 4 == 0 ? 2 : 0)) return cudaErrorInvalidValue;  // K5 / K6 disagree
+  if (a.swz != (a.ncol % 4 || v < 3 ? 0 : (v == 4 ? 3 : 2))) return cudaErrorInvalidValue;  // K5 / K6 disagree
   const size_t smem = pi_smem(v, a.no, a.ncol);
   const unsigned gy = (unsigned)((a.warp_groups + kPiWarps - 1) / kPiWarps);
   const unsigned gx = (unsigned)((long long)chunk_atoms * 2 * a.echunks * a.nqz);
