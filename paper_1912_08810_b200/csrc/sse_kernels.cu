@@ -1749,8 +1749,15 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   const int main_ctas = chunk_atoms * 2 * p.echunks * p.nqz;
   const bool TAIL = TAIL_CTAS && bx >= main_ctas;
   if (TAIL) bx -= main_ctas;
-  const int q = TAIL ? warp : bx % p.nqz;
-  if (!TAIL) bx /= p.nqz;
+  const int qgroups = (p.nqz + NW - 1) / NW;  // tail CTAs: NW momenta each
+  int q;
+  if (TAIL) {
+    q = (bx % qgroups) * NW + warp;
+    bx /= qgroups;
+  } else {
+    q = bx % p.nqz;
+    bx /= p.nqz;
+  }
   const int ec = bx % p.echunks;
   bx /= p.echunks;
   const int pol = bx % 2;
@@ -1758,7 +1765,7 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   const int m_tiles = (p.nw + 7) / 8;
   const int wg = blockIdx.y * NW + warp;
   const int mt0 = TAIL ? m_tiles - 1 : 2 * wg;
-  const bool active = TAIL ? warp < p.nqz : mt0 < m_tiles;
+  const bool active = TAIL ? q < p.nqz : mt0 < m_tiles;
   const bool two = !TAIL && mt0 + 1 < m_tiles;  // warp-uniform
   const int pcol = lane & 3;
 
@@ -2310,7 +2317,7 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
       const int pairs = ((a.nw + 7) / 8 + 1) / 2;
       const char* w4 = getenv("SSE_PI_V4_WARPS");
       const int m_tiles = (a.nw + 7) / 8;
-      const bool split = !(w4 && w4[0] == '5') && m_tiles == 9 && a.nqz >= 1 && a.nqz <= 4;
+      const bool split = !(w4 && w4[0] == '5') && m_tiles == 9;
       if (split || (w4 && w4[0] == '4')) {
         // 4 warps x 2 lag tiles per CTA (4 CTAs, 16 warps per SM: 4 per SMSP) for tiles 0..7,
         // then (split) the 9th tile of every q in one tail CTA per (atom, polarity, E-chunk)
@@ -2325,7 +2332,8 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
           e = cudaFuncSetAttribute(both, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
           if (e == cudaSuccess) e = cudaFuncSetAttribute(both, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
           if (e != cudaSuccess) return e;
-          both<<<dim3(gx + (unsigned)((long long)chunk_atoms * 2 * a.echunks), 1u), 4 * 32, smem4, st>>>(a, chunk_atoms);
+          const long long tails = (long long)chunk_atoms * 2 * a.echunks * ((a.nqz + 3) / 4);
+          both<<<dim3(gx + (unsigned)tails, 1u), 4 * 32, smem4, st>>>(a, chunk_atoms);
         } else {
           kern<<<dim3(gx, (unsigned)((pairs + 3) / 4)), 4 * 32, smem4, st>>>(a, chunk_atoms);
         }

@@ -195,7 +195,7 @@ def test_pi_device_api_slab_bitwise():
 def test_pi_split_lag_tiles_bitwise(monkeypatch):
     """Paper shapes with 9 lag tiles (Nw in 65..72): K6 v4 runs tiles 0..7 with 4 warps per CTA plus a
     tail CTA computing the 9th tile of every q; bitwise equal to the unsplit v4 and to v3."""
-    p = SimParams(n_kz=2, n_qz=2, n_E=72, n_w=66, n_A=5, n_B=4, n_orb=12)
+    p = SimParams(n_kz=5, n_qz=5, n_E=72, n_w=66, n_A=5, n_B=4, n_orb=12)  # Nqz = 5: two tail q-groups
     g_l, g_g, _, _, dh = inputs.stream_instance(8, p, dh_scale=0.05)
     nmap = build_neighbor_map(p.n_A, p.n_B)
     grid = default_grid(p)
