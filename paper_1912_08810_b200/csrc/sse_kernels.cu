@@ -646,7 +646,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
         for (int nt = 0; nt < NT; ++nt) {
           const int f = kk * NT + nt;
           const double b = (f & 1) ? st.b[f >> 1].y : st.b[f >> 1].x;
-          dmma884(acc[t][nt], a, b);
+          dmma884_nv(acc[t][nt], a, b);
         }
       }
     }
