@@ -594,11 +594,23 @@ int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi,
     CU(cudaEventRecord(ds.ev[2], st));
     CU(cudaStreamWaitEvent(ds.s_h2d, ds.ev[2], 0));
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(op_chunk_atoms(d), (on + 7) / 8));
-    // chunk boundaries: a small first chunk (its H2D is not hidden) and a small last chunk
-    // (its D2H is not hidden), regular chunks in between
-    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(32, chunk / 4));
+    // chunk boundaries: a geometric ramp of small chunks at the start (the first chunk's H2D is
+    // not hidden; each chunk's compute then covers the next one's H2D, ~3.5x faster per atom on
+    // one B200) and the mirrored ramp at the end (the last chunk's D2H is not hidden)
+    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(8, chunk / 4));
+    std::vector<int64_t> ramp;
+    for (int64_t s = edge; s < chunk; s *= 3) ramp.push_back(s);
+    int64_t ramp_atoms = 0;
+    for (int64_t s : ramp) ramp_atoms += s;
     std::vector<int64_t> bounds{0};
-    if (on > 2 * edge + chunk) {
+    if (on >= 2 * ramp_atoms + chunk) {
+      for (int64_t s : ramp) bounds.push_back(bounds.back() + s);
+      const int64_t tail = on - ramp_atoms;
+      while (bounds.back() + chunk < tail) bounds.push_back(bounds.back() + chunk);
+      if (tail > bounds.back()) bounds.push_back(tail);
+      int64_t b = tail;
+      for (size_t i = ramp.size(); i-- > 1;) bounds.push_back(b += ramp[i]);
+    } else if (on > 2 * edge + chunk) {
       bounds.push_back(edge);
       while (bounds.back() + chunk < on - edge) bounds.push_back(bounds.back() + chunk);
       bounds.push_back(on - edge);
