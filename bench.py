@@ -514,6 +514,50 @@ def gf_fused_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, 
                   "note": "G read from the GF (k,E)-point owners by TMA over NVLink and Sigma stored to them "
                           "from the K3 epilogue (CUDA IPC peer memory); raw D from the (q,w) points by NCCL "
                           "all-to-all; preprocess_D + K2 + K3 + one device-side all-reduce per step"}
+    # pull variant: the G slab (owned + halo) pulled from the point owners by one kernel per polarity
+    # (NVLink loads), then the slab kernels; Sigma still stored to the owners from the K3 epilogue
+    def g_digest():  # bit-pattern digest (no second copy of the slab in HBM)
+        return [int(torch.view_as_real(t).view(torch.int64).sum()) for t in prob.g]
+
+    g_keep = g_digest()
+
+    def pull_step():
+        for pol in range(2):
+            prob.d[pol].copy_(sdist.phonon_points_to_slab(d_pts[pol], idx, p.n_qz, p.n_w))
+        prob.pull_g(peer_g)
+        prob.preprocess()
+        prob.sigma_scatter(peer_s)
+        dist.all_reduce(token)
+
+    for t in prob.g:
+        t.fill_(float("nan"))
+    pull_step()
+    torch.cuda.synchronize()
+    same_g = float(g_digest() == g_keep)
+    same_g = -allreduce_max(-same_g, world)
+    del g_keep
+    barrier(world)
+    start.record(stream)
+    for _ in range(args.gf_fused_steps):
+        prob.pull_g(peer_g)
+    end.record(stream)
+    torch.cuda.synchronize()
+    pull_ms = allreduce_max(start.elapsed_time(end) / args.gf_fused_steps, world)
+    barrier(world)
+    start.record(stream)
+    for _ in range(args.gf_fused_steps):
+        pull_step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    pull_step_ms = allreduce_max(start.elapsed_time(end) / args.gf_fused_steps, world)
+    slab_bytes = 2 * prob.n_slab * p.n_kz * p.n_E * p.n_orb ** 2 * 16
+    fused_info["pull"] = {
+        "s_per_step": pull_step_ms / 1e3, "vs_halo_step": pull_step_ms / step_ms,
+        "pull_ms": pull_ms, "pull_GB_per_s": slab_bytes / (pull_ms * 1e-3) / 1e9,
+        "slab_bitwise_equal": bool(same_g == 1.0),
+        "note": "G slab (owned + halo atoms, both polarities) pulled from the point owners by sse_slab_from_points "
+                "(NVLink loads), then preprocess_D + K2 + K3 with Sigma stored to the owners from the epilogue",
+    }
     if args.pi_steps > 0:
         # Pi from the point layout too (K5 / K6 read G over NVLink), returned to the (q, w) owners
         def fused_pi():
@@ -531,6 +575,20 @@ def gf_fused_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, 
         fused_info["pi_s_per_eval"] = allreduce_max(start.elapsed_time(end) / args.pi_steps, world) / 1e3
         fused_info["pi_note"] = ("Pi with G read from the point owners (K5 G2, K6 G1 rows over NVLink) + "
                                  "Pi to the (q,w) point owners (NCCL all-to-all)")
+
+        def pull_pi():  # the slab is already pulled by pull_step
+            prob.pi()
+            return [sdist.pi_to_points(prob.pi_out[pol], p.n_A, p.n_qz, p.n_w) for pol in range(2)]
+
+        pull_pi()
+        torch.cuda.synchronize()
+        barrier(world)
+        start.record(stream)
+        for _ in range(args.pi_steps):
+            pull_pi()
+        end.record(stream)
+        torch.cuda.synchronize()
+        fused_info["pull"]["pi_s_per_eval"] = allreduce_max(start.elapsed_time(end) / args.pi_steps, world) / 1e3
     barrier(world)
     del d_pts
     peer_g.close()

@@ -183,6 +183,18 @@ int sse_pi_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out,
                        int nranks, const int64_t* pt_lo, double* Pi_l, double* Pi_g,
                        void* stream, sse_timing* t);
 
+/* Assemble the G slab g (atoms [g.atom0, g.atom0+g.natoms), layout g.atom_major)
+ * from the GF (k,E)-point layout: src[r] = rank r's [pts_r, NA, No, No] buffer
+ * (device pointer valid in this process: local, or a CUDA-IPC-mapped peer read
+ * over NVLink), pt_lo[0..nranks] the point ranges (dist.point_chunks), self_rank
+ * the caller's rank (points are read starting from its own range, so concurrent
+ * pulls spread over the owners; -1: from point 0).  One kernel; the slab then
+ * feeds sse_sigma_device / sse_pi_device.  Replaces the
+ * G-forward round of the tiled scheme's all-to-all (distsim.py:300-315). */
+int sse_slab_from_points(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, int nranks,
+                         const int64_t* pt_lo, const double* const* src, int self_rank, double* dst,
+                         void* stream);
+
 /* Library-owned device memory that can be shared with peer processes, and CUDA
  * IPC export / import of it (handles are SSE_IPC_HANDLE_BYTES opaque bytes). */
 #define SSE_IPC_HANDLE_BYTES 64

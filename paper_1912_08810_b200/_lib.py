@@ -29,6 +29,7 @@ EXPORTED = (
     "sse_sigma_device_scatter",
     "sse_sigma_device_peer",
     "sse_pi_device_peer",
+    "sse_slab_from_points",
     "sse_dev_alloc",
     "sse_dev_free",
     "sse_ipc_handle",
@@ -131,6 +132,7 @@ def load() -> ctypes.CDLL:
         lib.sse_sigma_device_scatter.argtypes = [_P, pdims, pslab, pslab] + [_P] * 8 + [i32, _P, _P, _P, _P, ptim]
         lib.sse_sigma_device_peer.argtypes = [_P, pdims, pslab, _P, _P] + [_P] * 6 + [i32, _P, _P, _P, _P, ptim]
         lib.sse_pi_device_peer.argtypes = [_P, pdims, pslab, _P, _P, _P, _P, _P, dbl, i32, _P, _P, _P, _P, ptim]
+        lib.sse_slab_from_points.argtypes = [_P, pdims, pslab, i32, _P, _P, i32, _P, _P]
         lib.sse_dev_alloc.argtypes = [_P, ctypes.c_size_t, ctypes.POINTER(_P)]
         lib.sse_dev_free.argtypes = [_P, _P]
         lib.sse_ipc_handle.argtypes = [_P, _P, ctypes.c_char_p]

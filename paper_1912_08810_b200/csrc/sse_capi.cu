@@ -994,6 +994,45 @@ int sse_pi_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out, con
   return SSE_OK;
 }
 
+int sse_slab_from_points(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, int nranks, const int64_t* pt_lo,
+                         const double* const* src, int self_rank, double* dst, void* stream) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
+  CHECK(validate_dims(d));
+  CHECK(validate_slab(d, g, "G"));
+  if (!src || !pt_lo || !dst) return fail(SSE_EINVAL, "NULL tensor pointer");
+  if (nranks < 1 || nranks > sse::kMaxScatter)
+    return fail(SSE_EINVAL, "slab pull needs 1..%d ranks (got %d)", sse::kMaxScatter, nranks);
+  const int64_t npts = d->nkz * d->ne;
+  if (pt_lo[0] != 0 || pt_lo[nranks] != npts) return fail(SSE_EINVAL, "point ranges must cover [0, Nkz*NE)");
+  if (npts > 65535) return fail(SSE_EINVAL, "slab pull supports at most 65535 (k,E) points");
+  if (g->natoms * d->norb * d->norb >= (1ll << 32)) return fail(SSE_EINVAL, "slab too wide for the pull kernel");
+  sse::SlabPullArgs a{};
+  a.ranks = nranks;
+  for (int r = 0; r <= nranks; ++r) {
+    if (r > 0 && pt_lo[r] < pt_lo[r - 1]) return fail(SSE_EINVAL, "point ranges must be non-decreasing");
+    a.pt_lo[r] = pt_lo[r];
+  }
+  for (int r = 0; r < nranks; ++r) {
+    if (!src[r] && pt_lo[r + 1] > pt_lo[r]) return fail(SSE_EINVAL, "NULL point source for rank %d", r);
+    a.src[r] = (const double2*)src[r];
+  }
+  const SlabStrides gs = strides_of(d, *g);
+  a.dst = (double2*)dst;
+  a.na = d->na;
+  a.atom0 = g->atom0;
+  a.natoms = g->natoms;
+  a.no2 = d->norb * d->norb;
+  a.dst_sa = gs.sa;
+  a.dst_sp = gs.se;  // point k*NE+e: k*sk + e*se == (k*NE+e)*se in both layouts
+  if (self_rank >= nranks) return fail(SSE_EINVAL, "self_rank %d outside [0, %d)", self_rank, nranks);
+  a.pt_shift = self_rank >= 0 ? pt_lo[self_rank] : 0;
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  CU(sse::launch_slab_pull(a, npts, st));
+  return SSE_OK;
+}
+
 int sse_dev_alloc(sse_ctx* ctx, size_t bytes, void** out) {
   if (!ctx || ctx->devs.size() != 1 || !out) return fail(SSE_EINVAL, "device allocation needs a 1-device context");
   CU(cudaSetDevice(ctx->devs[0].device));

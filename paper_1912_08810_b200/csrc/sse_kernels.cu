@@ -43,6 +43,43 @@ __global__ void layout_transform_kernel(long long nkz, long long ne, long long n
 }
 
 // --------------------------------------------------------------------------
+// Slab pull: assemble an electron-tensor atom slab from the GF
+// (k,E)-point layout.  Point pt lives on rank r (pt_lo[r] <= pt < pt_lo[r+1])
+// as src[r][pt - pt_lo[r]][NA][No*No]; the slab's atoms [atom0, atom0+natoms)
+// of one point are one contiguous source run, read here over NVLink when r is
+// a peer (CUDA IPC mapping).  grid.y = point, grid.x = pieces of the run; each
+// thread keeps kPullUnroll 16-byte loads in flight.  Points are visited from
+// pt_shift on (the caller's own first point), so while every rank pulls at once
+// each owner serves one reader at a time instead of all of them reading rank 0.
+// --------------------------------------------------------------------------
+constexpr int kPullUnroll = 8;
+
+__global__ void __launch_bounds__(256) slab_pull_kernel(SlabPullArgs p) {
+  long long pt = blockIdx.y + p.pt_shift;
+  if (pt >= p.pt_lo[p.ranks]) pt -= p.pt_lo[p.ranks];
+  int r = 0;
+  while (r + 1 < p.ranks && pt >= p.pt_lo[r + 1]) ++r;
+  const double2* __restrict__ src = p.src[r] + ((pt - p.pt_lo[r]) * p.na + p.atom0) * p.no2;
+  double2* __restrict__ dst = p.dst + pt * p.dst_sp;
+  const unsigned run = (unsigned)(p.natoms * p.no2), no2 = (unsigned)p.no2;
+  const unsigned base = blockIdx.x * (blockDim.x * kPullUnroll) + threadIdx.x;
+  double2 v[kPullUnroll];
+#pragma unroll
+  for (int u = 0; u < kPullUnroll; ++u) {
+    const unsigned e = base + u * blockDim.x;
+    if (e < run) v[u] = __ldcs(src + e);
+  }
+#pragma unroll
+  for (int u = 0; u < kPullUnroll; ++u) {
+    const unsigned e = base + u * blockDim.x;
+    if (e < run) {
+      const unsigned a = e / no2;
+      dst[a * p.dst_sa + (e - a * no2)] = v[u];
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // K2: operator build.  One CTA per (atom, neighbour slot) of the chunk:
 //   stage dH[a,s,0..2] and P_ij = dH_i @ dH_j (9 blocks) in shared memory,
 //   then every thread produces output doubles of
@@ -2401,6 +2438,16 @@ cudaError_t launch_fill_synthetic(uint64_t seed, uint32_t tensor_id, long long a
   const long long total = natoms * outer * inner;
   fill_synthetic_kernel<<<grid_for(total, 256), 256, 0, st>>>(
       seed, tensor_id, atom0, natoms, outer, inner, atom_stride, outer_stride, scale, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slab_pull(const SlabPullArgs& a, long long npts, cudaStream_t st) {
+  const long long run = a.natoms * a.no2;
+  if (npts <= 0 || run <= 0) return cudaSuccess;
+  if (npts > 65535 || run >= (1ll << 32) || a.ranks < 1 || a.ranks > kMaxScatter)
+    return cudaErrorInvalidValue;
+  const dim3 grid((unsigned)((run + 256 * kPullUnroll - 1) / (256 * kPullUnroll)), (unsigned)npts);
+  slab_pull_kernel<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

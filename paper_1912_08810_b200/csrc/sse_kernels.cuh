@@ -97,6 +97,15 @@ struct PeerGather {
   const double2* G[2][kMaxScatter];
 };
 
+struct SlabPullArgs {
+  int ranks;
+  long long pt_lo[kMaxScatter + 1];
+  const double2* src[kMaxScatter];  // per rank: [pts_r][NA][No*No] (peer pointers valid here)
+  double2* dst;                     // slab block (atom i, point pt) at dst + i*dst_sa + pt*dst_sp
+  long long na, atom0, natoms, no2, dst_sa, dst_sp;
+  long long pt_shift;               // first point visited (the caller's own range)
+};
+
 struct PiBuildArgs {
   const double2* G[2];        // G slab per polarity (layout by strides)
   const double2* dH;          // [out atoms][NB][3][No][No]
@@ -143,6 +152,7 @@ cudaError_t launch_preprocess_D(long long nqz, long long nw, long long d_natoms,
                                 long long out_atom0, long long out_natoms, long long nb,
                                 const int* nbr, const int* rev, const double2* D, double2* Dc,
                                 cudaStream_t st);
+cudaError_t launch_slab_pull(const SlabPullArgs& a, long long npts, cudaStream_t st);
 cudaError_t launch_fill_synthetic(uint64_t seed, uint32_t tensor_id, long long atom0,
                                   long long natoms, long long outer, long long inner,
                                   long long atom_stride, long long outer_stride, double scale,

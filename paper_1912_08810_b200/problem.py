@@ -122,6 +122,14 @@ class ShardProblem:
             n_a=p.n_A, n_o=p.n_orb, out_atom0=self.lo, device=self.device.index or 0, stream=stream,
         )
 
+    def pull_g(self, peer_g, stream=None) -> None:
+        """The G slab (owned atoms + halo) from the GF point owners' buffers (dist.PeerPointBuffers):
+        one kernel per polarity reading the peers over NVLink; replaces slab assembly + halo exchange."""
+        p = self.p
+        for pol in range(2):
+            dev.slab_from_points(peer_g.remote[pol], peer_g.pt_lo, self.g[pol], n_kz=p.n_kz, n_e=p.n_E, n_a=p.n_A,
+                                 g_atom0=self.glo, atom_major=True, self_rank=peer_g.rank, stream=stream)
+
     def pi(self, stream=None) -> None:
         """Phonon self-energy Pi of the owned atoms (sse.py:409-428), [Nqz, Nw, oA, NB+1, 3, 3]."""
         t, p = self.torch, self.p

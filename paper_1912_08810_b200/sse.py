@@ -498,6 +498,37 @@ def sigma_device_peer(
     return tim.as_dict() if sync_timing else None
 
 
+def slab_from_points(sources, pt_lo, out, *, n_kz: int, n_e: int, n_a: int, g_atom0: int,
+                     atom_major: bool = True, self_rank: int = -1, stream=None) -> None:
+    """Fill the device G slab ``out`` (atoms [g_atom0, g_atom0 + natoms), layout
+    [natoms, Nkz, NE, No, No] or grid-major [Nkz, NE, natoms, No, No]) from the GF
+    (k,E)-point layout: ``sources[r]`` is rank r's [pts_r, NA, No, No] buffer (device
+    pointer valid in this process, a CUDA-IPC-mapped peer read over NVLink),
+    ``pt_lo`` the point bounds, ``self_rank`` this rank (reads start at its own points so
+    concurrent pulls spread over the owners) (``sse_slab_from_points``)."""
+    import torch
+
+    if out.dtype != torch.complex128:
+        raise ValueError("out must be complex128")
+    shape = tuple(out.shape)
+    if len(shape) != 5 or shape[3] != shape[4]:
+        raise ValueError("out must be a 5-d slab of square blocks")
+    natoms = shape[0] if atom_major else shape[2]
+    grid = shape[1:3] if atom_major else shape[0:2]
+    if tuple(grid) != (n_kz, n_e):
+        raise ValueError(f"slab grid {tuple(grid)} != (Nkz, NE) = {(n_kz, n_e)}")
+    nranks = len(sources)
+    if len(pt_lo) != nranks + 1:
+        raise ValueError("nranks + 1 point bounds")
+    bounds = np.ascontiguousarray(pt_lo, dtype=np.int64)
+    srcs = (ctypes.c_void_p * nranks)(*[int(x) for x in sources])
+    dims = _lib.SseDims(n_kz, 1, n_e, 1, n_a, 1, shape[3])
+    slab = _lib.SseSlab(g_atom0, natoms, 1 if atom_major else 0, 0)
+    ctx = _lib.context(device=out.device.index or 0)
+    _lib.check(_lib.load().sse_slab_from_points(ctx.handle, ctypes.byref(dims), ctypes.byref(slab), nranks,
+                                                _ptr(bounds), srcs, self_rank, _dptr(out), _stream_ptr(stream)))
+
+
 def pi_device_peer(
     sources_l, sources_g, dh, nmap_rows: Array, offsets, energy_weight: float, out_l, out_g, pt_lo, *,
     n_kz: int, n_qz: int, n_e: int, n_a: int, n_o: int, out_atom0: int, stream=None, sync_timing: bool = False,

@@ -4,7 +4,8 @@ Two NCCL ranks (spawned processes, one GPU each): the peer-scatter epilogue
 (``sse_sigma_device_scatter`` into CUDA-IPC-mapped buffers) and the fully fused
 variant that also reads G from the owners' point buffers with TMA
 (``sse_sigma_device_peer``), and Pi with G read the same way (``sse_pi_device_peer``), must equal, bitwise, Sigma computed into atom slabs
-and returned with the NCCL all-to-all (``dist.atom_slab_to_points``).
+and returned with the NCCL all-to-all (``dist.atom_slab_to_points``); the G slab pulled from the
+point owners (``sse_slab_from_points``) must equal the slab filled directly.
 """
 
 import os
@@ -75,6 +76,15 @@ def _worker(rank, world, port, q):
         torch.cuda.synchronize()
         ok_pi = all(torch.equal(prob.pi_out[pol], pi_ref[pol]) for pol in range(2))
         ok_fused = ok_fused and ok_pi
+        # the whole G slab (owned + halo) pulled from the point owners == the slab filled directly
+        g_ref = [t.clone() for t in prob.g]
+        for t in prob.g:
+            t.fill_(float("nan"))
+        torch.cuda.synchronize()
+        dist.barrier()
+        prob.pull_g(peer_g)
+        torch.cuda.synchronize()
+        ok_fused = ok_fused and all(torch.equal(prob.g[pol], g_ref[pol]) for pol in range(2))
         dist.barrier()
         peer_g.close()
         peer.close()
