@@ -116,3 +116,32 @@ def test_peer_scatter_and_gather_equal_all_to_all_bitwise():
         assert pr.exitcode == 0
     assert all(ok and fin for ok, fin, _ in res), res
     assert all(fused for _, _, fused in res), res
+
+
+@pytest.mark.parametrize("world,self_rank,atom_major", [(3, 1, True), (3, -1, False), (1, 0, True)])
+def test_slab_from_points_single_process(world, self_rank, atom_major):
+    """``sse_slab_from_points`` with every "rank's" point buffer on this GPU: the slab equals the
+    tensor sliced directly, for ragged point ranges, a rotated start and both slab layouts."""
+    import torch
+
+    from paper_1912_08810_b200 import dist as sdist
+    from paper_1912_08810_b200 import sse as dev
+
+    n_kz, n_e, n_a, n_o = 2, 13, 11, 3
+    g = torch.randn(n_kz, n_e, n_a, n_o, n_o, dtype=torch.complex128, device="cuda")
+    pts = sdist.point_chunks(n_kz, n_e, world)
+    flat = g.reshape(n_kz * n_e, n_a, n_o, n_o)
+    bufs = [flat[a:b].contiguous() for a, b in pts]
+    pt_lo = [a for a, _ in pts] + [pts[-1][1]]
+    glo, ghi = 3, 9
+    want = g[:, :, glo:ghi]
+    if atom_major:
+        want = want.permute(2, 0, 1, 3, 4)
+    out = torch.full_like(want.contiguous(), float("nan"))
+    dev.slab_from_points([b.data_ptr() for b in bufs], pt_lo, out, n_kz=n_kz, n_e=n_e, n_a=n_a, g_atom0=glo,
+                         atom_major=atom_major, self_rank=self_rank)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want.contiguous())
+    with pytest.raises(ValueError, match="self_rank"):
+        dev.slab_from_points([b.data_ptr() for b in bufs], pt_lo, out, n_kz=n_kz, n_e=n_e, n_a=n_a,
+                             g_atom0=glo, atom_major=atom_major, self_rank=world)
