@@ -389,7 +389,8 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
                  const double2* G_l, const double2* G_g, const double2* dH, const int64_t* nmap,
                  const int64_t* off, double energy_weight, const unsigned char* mask, double2* Pi_l,
                  double2* Pi_g, cudaStream_t st, int* launches, const sse::PeerGather* peer = nullptr,
-                 const std::function<int(int64_t, int64_t)>& before_chunk = nullptr) {
+                 const std::function<int(int64_t, int64_t)>& before_chunk = nullptr,
+                 const std::function<int(int64_t, int64_t)>& after_chunk = nullptr) {
   CHECK(prepare_tables(ds, d, g, out, nmap, off, nullptr, st));
   const unsigned char* mask_dev = nullptr;
   if (mask) {
@@ -400,6 +401,8 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
   const int no = (int)d->norb, no2 = no * no, nb = (int)d->nb, ncol = nb * 9;
   const size_t vt_atom = (size_t)d->nkz * d->ne * no2 * ncol * 16;  // per chain polarity
   int64_t chunk = std::max<int64_t>(1, (int64_t)((12ull << 30) / std::max<size_t>(vt_atom, 1)));
+  if (const char* env = getenv("SSE_PI_CHUNK_ATOMS"))  // override, for tests and experiments
+    if (atoll(env) > 0) chunk = atoll(env);
   chunk = std::min<int64_t>(chunk, out.natoms);
   const int64_t n_chunks = (out.natoms + chunk - 1) / chunk;
   chunk = (out.natoms + n_chunks - 1) / n_chunks;  // balanced chunks (no tiny tail launch)
@@ -479,7 +482,35 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
     aa.out_natoms = (int)out.natoms;
     CHECK(profiled(ds, st, SSE_PROF_PI_ASSEMBLE, 0.0, [&] { return sse::launch_pi_assemble(aa, st); }));
     if (launches) *launches += 3;
+    if (after_chunk) CHECK(after_chunk(a0, n));  // e.g. the chunk's Pi to the host
   }
+  return SSE_OK;
+}
+
+cudaEvent_t pipe_event(DevState& ds, size_t i);
+
+// Host-call helper: Pi of owned-atom chunk [a0, a0 + n) (device [rows][on][pi_row]) to the host
+// tensors Ph (global atom lo + a0 of [rows][na][pi_row]) on the D2H stream once K7 wrote it.
+int pi_chunk_to_host(DevState& ds, const sse_dims* d, int64_t lo, int64_t on, int64_t a0, int64_t n,
+                     double* const* Ph, cudaStream_t st, size_t* ei) {
+  const size_t pi_row = (size_t)(d->nb + 1) * 9 * 16;
+  const size_t pi_rows = (size_t)(d->nqz * d->nw);
+  cudaEvent_t done = pipe_event(ds, (*ei)++);
+  if (!done) return fail(SSE_ECUDA, "event creation failed");
+  CU(cudaEventRecord(done, st));
+  CU(cudaStreamWaitEvent(ds.s_d2h, done, 0));
+  for (int p = 0; p < 2; ++p)
+    CU(cudaMemcpy2DAsync((char*)Ph[p] + (lo + a0) * pi_row, d->na * pi_row, (char*)ds.pi_out[p].ptr + a0 * pi_row,
+                         on * pi_row, n * pi_row, pi_rows, cudaMemcpyDeviceToHost, ds.s_d2h));
+  return SSE_OK;
+}
+
+// Join the D2H stream back into st (after the last pi_chunk_to_host).
+int join_d2h(DevState& ds, cudaStream_t st, size_t* ei) {
+  cudaEvent_t e = pipe_event(ds, (*ei)++);
+  if (!e) return fail(SSE_ECUDA, "event creation failed");
+  CU(cudaEventRecord(e, ds.s_d2h));
+  CU(cudaStreamWaitEvent(st, e, 0));
   return SSE_OK;
 }
 
@@ -1168,13 +1199,12 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
     };
     int launches = 0;
     const sse_slab gs{glo, gn, 0, 0}, os{lo, on, 0, 0};
+    double* const Ph[2] = {Pi_l, Pi_g};
+    auto after_chunk = [&](int64_t a0, int64_t n) { return pi_chunk_to_host(ds, d, lo, on, a0, n, Ph, st, &ei); };
     CHECK(pi_on_device(ds, d, gs, os, ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dh.as<double2>(),
                        nmap + lo * d->nb, off, energy_weight, mask, ds.pi_out[0].as<double2>(),
-                       ds.pi_out[1].as<double2>(), st, &launches, nullptr, before_chunk));
-    double* Ph[2] = {Pi_l, Pi_g};
-    for (int p = 0; p < 2; ++p)
-      CU(cudaMemcpy2DAsync((char*)Ph[p] + lo * pi_row, d->na * pi_row, ds.pi_out[p].ptr, on * pi_row,
-                           on * pi_row, pi_rows, cudaMemcpyDeviceToHost, st));
+                       ds.pi_out[1].as<double2>(), st, &launches, nullptr, before_chunk, after_chunk));
+    CHECK(join_d2h(ds, st, &ei));
     CU(cudaEventRecord(ds.ev[1], st));
     CU(cudaEventSynchronize(ds.ev[1]));
     if (tt) {
@@ -1279,13 +1309,13 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
     int launches = ts.kernel_launches + 2;
     for (int p = 0; p < 2; ++p) CHECK(ds.pi_out[p].ensure(pi_rows * on * pi_row));
     const sse_slab gs{glo, gn, 0, 0}, os{lo, on, 0, 0};
+    double* const Ph[2] = {Pi_l, Pi_g};
+    size_t ei = 0;
+    auto after_chunk = [&](int64_t a0, int64_t n) { return pi_chunk_to_host(ds, d, lo, on, a0, n, Ph, st, &ei); };
     CHECK(pi_on_device(ds, d, gs, os, ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dh.as<double2>(),
                        nmap + lo * d->nb, off, energy_weight, nullptr, ds.pi_out[0].as<double2>(),
-                       ds.pi_out[1].as<double2>(), st, &launches));
-    double* Ph[2] = {Pi_l, Pi_g};
-    for (int p = 0; p < 2; ++p)
-      CU(cudaMemcpy2DAsync((char*)Ph[p] + lo * pi_row, d->na * pi_row, ds.pi_out[p].ptr, on * pi_row,
-                           on * pi_row, pi_rows, cudaMemcpyDeviceToHost, st));
+                       ds.pi_out[1].as<double2>(), st, &launches, nullptr, nullptr, after_chunk));
+    CHECK(join_d2h(ds, st, &ei));
     CU(cudaEventRecord(e1, st));
     CU(cudaEventSynchronize(e1));
     if (tt) {

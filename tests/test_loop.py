@@ -156,3 +156,26 @@ def test_sse_phase_multi_gpu_bitwise():
     s2, p2 = sse_phase(*args, n_gpus=2)
     for a, b in ((s1, s2), (p1, p2)):
         assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["orb12_s5", "baseline_tiny_s0", "cli_small_s2"])
+def test_sse_phase_chunked_pipelines_bitwise(name, monkeypatch):
+    """Small Sigma and Pi atom chunks (SSE_OP_CHUNK_ATOMS / SSE_PI_CHUNK_ATOMS): the host pipelines'
+    chunk ramps and per-chunk Pi downloads give the same bits as one chunk."""
+    from paper_1912_08810_b200.sse import sse_phase, sse_pi
+    from tests.golden_cases import load_case
+
+    c = load_case(name)
+    grid = EnergyGrid(values=tuple(np.linspace(-1, 1, c.p.n_E)),
+                      frequency_map=tuple(zip(c.offsets.tolist(), c.weights.tolist())), energy_weight=0.01)
+    args = (GreensTensor(c.g_l, c.g_g), GreensTensor(c.d_l, c.d_g), c.dh, NeighborMap(c.idx), grid, c.p.n_qz)
+    s1, p1 = sse_phase(*args)
+    q1 = sse_pi(args[0], c.dh, args[3], grid, c.p.n_qz)
+    monkeypatch.setenv("SSE_OP_CHUNK_ATOMS", "16")  # Sigma chunks of min(16, NA/8): ramps at both ends
+    monkeypatch.setenv("SSE_PI_CHUNK_ATOMS", "5")
+    s2, p2 = sse_phase(*args)
+    q2 = sse_pi(args[0], c.dh, args[3], grid, c.p.n_qz)
+    for a, b in ((s1, s2), (p1, p2), (q1, q2)):
+        assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
+    assert np.array_equal(p1.lesser, q1.lesser) and np.array_equal(p1.greater, q1.greater)
