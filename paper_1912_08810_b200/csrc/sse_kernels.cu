@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(256) slab_pull_kernel(SlabPullArgs p) {
 //   M[q,w] = wt_w * sum_ij Dc[q,w,a,s,i,j] * P_ij
 // for both polarities, either in DMMA B-fragment order or compact [p][n].
 // --------------------------------------------------------------------------
+constexpr int kOpBlocks = 8;  // (q,w) operator blocks per K2 iteration (fragment order)
+
 __global__ void build_operator_kernel(OperatorArgs p) {
   extern __shared__ double2 smem[];
   const int no = p.no, no2 = no * no;
@@ -114,20 +116,16 @@ __global__ void build_operator_kernel(OperatorArgs p) {
   }
   __syncthreads();
 
-  const FragGeom fg = frag_geom(no);
-  const int per_qw_vec = p.fragment_order ? fg.fv * 32 : no2;  // double2 per (q,w)
   const long long qw_total = (long long)p.nqz * p.nw;
-  const long long out_base = (long long)blockIdx.x * qw_total * per_qw_vec;  // (la*nb+s)
-  for (int pol = 0; pol < p.npol; ++pol) {
-    const double2* dc_base = p.Dc[pol];
-    double2* out = p.M[pol] + out_base;
-    for (long long x = threadIdx.x; x < qw_total * per_qw_vec; x += blockDim.x) {
-      const int qw = (int)(x / per_qw_vec);
-      const int v = (int)(x % per_qw_vec);
-      const int q = qw / p.nw, w = qw % p.nw;
-      const double2* dc = dc_base + (((long long)(q * p.nw + w) * p.dc_natoms + a_slab) * p.nb + s) * 9;
-      const double wt = p.wt[w];
-      if (!p.fragment_order) {
+  if (!p.fragment_order) {
+    const long long out_base = (long long)blockIdx.x * qw_total * no2;  // (la*nb+s)
+    for (int pol = 0; pol < p.npol; ++pol) {
+      const double2* dc_base = p.Dc[pol];
+      double2* out = p.M[pol] + out_base;
+      for (long long x = threadIdx.x; x < qw_total * no2; x += blockDim.x) {
+        const int qw = (int)(x / no2), v = (int)(x % no2);
+        const double2* dc = dc_base + (((long long)qw * p.dc_natoms + a_slab) * p.nb + s) * 9;
+        const double wt = p.wt[qw % p.nw];
         double re = 0.0, im = 0.0;
         for (int ij = 0; ij < 9; ++ij) {
           const double2 c = dc[ij], m = s_p[ij * no2 + v];
@@ -137,38 +135,65 @@ __global__ void build_operator_kernel(OperatorArgs p) {
           im = fma(c.y, m.x, im);
         }
         out[x] = make_double2(wt * re, wt * im);
-        continue;
       }
-      // fragment order: v = j * 32 + lane, vector j holds fragments 2j, 2j+1,
-      // fragment f = kk * NT + nt; lane holds B'[4kk + (lane&3)][8nt + (lane>>2)].
-      const int j = v >> 5, lane = v & 31;
-      double vals[2];
-      for (int h = 0; h < 2; ++h) {
-        const int f = 2 * j + h;
-        const int kk = f / fg.nt, nt = f % fg.nt;
-        const int kr = 4 * kk + (lane & 3), nc = 8 * nt + (lane >> 2);
-        const bool im_row = kr >= fg.nop;
-        const int pr = im_row ? kr - fg.nop : kr;
-        const int n = nc >> 1, part = nc & 1;
-        double val = 0.0;
-        if (pr < no && n < no) {
-          double re = 0.0, im = 0.0;
-          for (int ij = 0; ij < 9; ++ij) {
-            const double2 c = dc[ij], m = s_p[ij * no2 + pr * no + n];
-            re = fma(c.x, m.x, re);
-            re = fma(-c.y, m.y, re);
-            im = fma(c.x, m.y, im);
-            im = fma(c.y, m.x, im);
-          }
-          re *= wt;
-          im *= wt;
-          // B'[re-row p][2n] = Re M, B'[re-row p][2n+1] = Im M,
-          // B'[im-row p][2n] = -Im M, B'[im-row p][2n+1] = Re M.
-          val = !im_row ? (part == 0 ? re : im) : (part == 0 ? -im : re);
+    }
+    return;
+  }
+  // DMMA fragment order, kOpBlocks (q,w) blocks at a time: phase 1 computes each complex
+  // M element once into shared memory (wt-scaled), phase 2 writes the real embedding
+  //   B'[re-row p][2n] = Re M, B'[re-row p][2n+1] = Im M,
+  //   B'[im-row p][2n] = -Im M, B'[im-row p][2n+1] = Re M
+  // in fragment order (v = j * 32 + lane, vector j holds fragments 2j, 2j+1, fragment
+  // f = kk * NT + nt; lane holds B'[4kk + (lane&3)][8nt + (lane>>2)]) with coalesced stores.
+  double2* s_m = s_p + 9 * no2;  // [kOpBlocks][no][no]
+  const FragGeom fg = frag_geom(no);
+  const int per_qw_vec = fg.fv * 32;  // double2 per (q,w)
+  const long long out_base = (long long)blockIdx.x * qw_total * per_qw_vec;  // (la*nb+s)
+  for (int pol = 0; pol < p.npol; ++pol) {
+    const double2* dc_base = p.Dc[pol];
+    double2* out = p.M[pol] + out_base;
+    for (int qw0 = 0; qw0 < qw_total; qw0 += kOpBlocks) {
+      const int nblk = min(kOpBlocks, (int)qw_total - qw0);
+      for (int x = threadIdx.x; x < nblk * no2; x += blockDim.x) {
+        const int b = x / no2, v = x - b * no2, qw = qw0 + b;
+        const double2* dc = dc_base + (((long long)qw * p.dc_natoms + a_slab) * p.nb + s) * 9;
+        const double wt = p.wt[qw % p.nw];
+        double re = 0.0, im = 0.0;
+        for (int ij = 0; ij < 9; ++ij) {
+          const double2 c = dc[ij], m = s_p[ij * no2 + v];
+          re = fma(c.x, m.x, re);
+          re = fma(-c.y, m.y, re);
+          im = fma(c.x, m.y, im);
+          im = fma(c.y, m.x, im);
         }
-        vals[h] = val;
+        re *= wt;
+        im *= wt;
+        s_m[x] = make_double2(re, im);
       }
-      out[x] = make_double2(vals[0], vals[1]);
+      __syncthreads();
+      double2* o = out + (long long)qw0 * per_qw_vec;
+      for (int x = threadIdx.x; x < nblk * per_qw_vec; x += blockDim.x) {
+        const int b = x / per_qw_vec, v = x - b * per_qw_vec;
+        const int j = v >> 5, lane = v & 31;
+        double vals[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int f = 2 * j + h;
+          const int kk = f / fg.nt, nt = f % fg.nt;
+          const int kr = 4 * kk + (lane & 3), nc = 8 * nt + (lane >> 2);
+          const bool im_row = kr >= fg.nop;
+          const int pr = im_row ? kr - fg.nop : kr;
+          const int n = nc >> 1, part = nc & 1;
+          double val = 0.0;
+          if (pr < no && n < no) {
+            const double2 m = s_m[b * no2 + pr * no + n];
+            val = !im_row ? (part == 0 ? m.x : m.y) : (part == 0 ? -m.y : m.x);
+          }
+          vals[h] = val;
+        }
+        o[x] = make_double2(vals[0], vals[1]);
+      }
+      __syncthreads();
     }
   }
 }
@@ -2175,7 +2200,7 @@ cudaError_t launch_layout_transform(long long nkz, long long ne, long long na, l
 }
 
 cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)12 * a.no * a.no * sizeof(double2);
+  const size_t smem = (size_t)(12 + (a.fragment_order ? kOpBlocks : 0)) * a.no * a.no * sizeof(double2);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(build_operator_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
