@@ -349,6 +349,7 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   sa.npol = npol;
   sa.off_slide = 1;
   sa.lookahead = getenv("SSE_SLIDE_LOOKAHEAD") ? atoi(getenv("SSE_SLIDE_LOOKAHEAD")) : 0;
+  sa.k3_opts = getenv("SSE_K3_OPTS") ? atoi(getenv("SSE_K3_OPTS")) : 3;
   for (int64_t w = 1; w < d->nw; ++w)
     if (off[w] < off[w - 1] || off[w] > off[w - 1] + 1) sa.off_slide = 0;
   if (sc && sc->nranks > 0) {

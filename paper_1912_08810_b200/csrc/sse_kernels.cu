@@ -15,6 +15,7 @@
 #include "sse_kernels.cuh"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace sse {
 
@@ -573,7 +574,13 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   const int la = bx / p.nkz;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cta_r0 = rc * SG::kRows;
-  const int rbase = cta_r0 + warp * (MT * 8);
+  // The last CTA of an (atom, k) row range is usually partial (paper: 120 of 288
+  // rows).  There the row tiles are interleaved over the warps (tile t of warp w
+  // = CTA tile t * NW + w), so the valid tiles spread over all four SMSPs, and
+  // each warp runs the DMMAs of its valid tiles only (a prefix of its MT).
+  // Each output row keeps its accumulation order: bitwise equal either way.
+  const bool tail = (p.k3_opts & 1) && cta_r0 + SG::kRows > p.rows;
+  auto tile_row0 = [&](int t) { return tail ? cta_r0 + (t * NW + warp) * 8 : cta_r0 + warp * (MT * 8) + t * 8; };
   const int pcol = lane & 3;
   const double2* __restrict__ G = p.G[pol];
   const double2* __restrict__ Mf = p.M[pol];
@@ -589,13 +596,17 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   bool v_row[MT];
 #pragma unroll
   for (int t = 0; t < MT; ++t) {
-    const int row = rbase + t * 8 + (lane >> 2);
+    const int row = tile_row0(t) + (lane >> 2);
     v_row[t] = row < p.rows;
     e_row[t] = row / NO;
     m_off[t] = (row - e_row[t] * NO) * NO + pcol;
   }
-  const int warp_rows = min(MT * 8, p.rows - rbase);
-  const int warp_emax = warp_rows > 0 ? (rbase + warp_rows - 1) / NO : -1;
+  // valid tiles (first row inside the matrix) form a prefix in both mappings;
+  // warp_emax = energy of the warp's last valid row (rows ascend with t)
+  int n_valid = 0;
+#pragma unroll
+  for (int t = 0; t < MT; ++t) n_valid += tile_row0(t) < p.rows ? 1 : 0;
+  const int warp_emax = n_valid > 0 ? (min(tile_row0(n_valid - 1) + 8, p.rows) - 1) / NO : -1;
 
   double acc[MT][NT][2];
 #pragma unroll
@@ -617,7 +628,14 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   }
   __syncthreads();
 
-  const int n_it = p.nqz * p.nb * p.nw;
+  // Stages whose offset exceeds the CTA's top energy (E - off < 0 for every row:
+  // a suffix of each segment, offsets being non-decreasing) contribute nothing;
+  // they are dropped, keeping >= kSlideStages stages per segment so that the
+  // stages in flight still span at most one segment boundary (ring bound).
+  int nw_eff = p.nw;
+  if (p.k3_opts & 2)
+    while (nw_eff > SB && s_off[nw_eff - 1] > e_hi) --nw_eff;
+  const int n_it = p.nqz * p.nb * nw_eff;
 
   // Window bookkeeping in closed form.  Segment sg = (q, s) covers stages
   // [sg*nw, (sg+1)*nw); its window at stage w is [max(0, e_lo - off_w),
@@ -628,12 +646,12 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   // index sg * seg_blocks + (top0 - e).
   const int top0 = e_hi - s_off[0];
   const bool seg_empty = top0 < 0;
-  const int seg_blocks = seg_empty ? 0 : top0 + 1 - max(0, e_lo - s_off[p.nw - 1]);
+  const int seg_blocks = seg_empty ? 0 : top0 + 1 - max(0, e_lo - s_off[nw_eff - 1]);
   auto win_low = [&](int w) { return w < 0 ? top0 + 1 : max(0, e_lo - s_off[w]); };
 
   auto produce = [&](int t) {  // lane 0 of the owning warp
     const int slot = t % SB;
-    const int sg = t / p.nw, w = t - sg * p.nw;
+    const int sg = t / nw_eff, w = t - sg * nw_eff;
     const int q = sg / p.nb, s = sg - q * p.nb;
     int kp = (k - q) % p.nkz;
     if (kp < 0) kp += p.nkz;
@@ -690,19 +708,18 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
       }
     }
     ++c_it;
-    if (++c_w == p.nw) {
+    if (++c_w == nw_eff) {
       c_w = 0;
       ++c_sg;
     }
   };
   // k-steps [k0, k1) of one stage's DMMAs
-  auto compute_part = [&](const OperandStageT<NO, MT>& st, int k0, int k1) {
-    if (warp_emax < st.off) return;
+  auto compute_tiles = [&](const OperandStageT<NO, MT>& st, auto nv) {
+    constexpr int NV = decltype(nv)::value;
 #pragma unroll
     for (int kk = 0; kk < KSTEPS; ++kk) {
-      if (kk < k0 || kk >= k1) continue;
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
+      for (int t = 0; t < NV; ++t) {
         const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -721,16 +738,22 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   const int L = p.lookahead > 0 ? min(p.lookahead, SB - 1) : kSlideLookahead;
   if (lane == 0)
     for (int i = warp; i < L && i < n_it; i += NW) produce(i);
-  {
+  // the stage loop, instantiated per count of valid tiles (warp-uniform; the
+  // branch is outside the loop, so the full-tile loop is the only hot code)
+  auto run = [&](auto nv) {
     // single buffer: the LDS latency is hidden by the other warps of the SMSP
     OperandStageT<NO, MT> s0;
     for (int it = 0; it < n_it; ++it) {
       if (lane == 0 && it + L < n_it && (it + L) % NW == warp) produce(it + L);
       lds(s0);
-      compute_part(s0, 0, KSTEPS);
+      if (warp_emax >= s0.off) compute_tiles(s0, nv);
       release(it);
     }
-  }
+  };
+  if (n_valid == MT) run(std::integral_constant<int, MT>{});
+  else if (MT > 2 && n_valid == 2) run(std::integral_constant<int, (MT > 2 ? 2 : 0)>{});
+  else if (MT > 1 && n_valid == 1) run(std::integral_constant<int, (MT > 1 ? 1 : 0)>{});
+  else run(std::integral_constant<int, 0>{});
 
 #pragma unroll
   for (int t = 0; t < MT; ++t) {

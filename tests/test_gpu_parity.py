@@ -136,6 +136,8 @@ def test_all_sigma_kernels_bitwise(monkeypatch, name):
     (24, 6, 12, 10, 4),    # the smoke shape: 6 offsets < 12 ring stages (pipelined fallback)
     (48, 12, 12, 6, 4),    # sliding-window kernel, one CTA tile, segments of exactly 12 stages
     (64, 20, 12, 5, 4),    # sliding-window kernel, two CTA tiles, window clipped at E = 0
+    (25, 12, 12, 5, 4),    # sliding-window tail CTA: 12 rows, interleaved tiles, a partial tile
+    (41, 14, 12, 5, 4),    # sliding-window tail CTA: 204 rows (warps with 3 / 2 valid tiles, partial tile)
     (40, 13, 10, 6, 4),    # No = 10 (padded DMMA embedding; ring too large: pipelined kernel)
     (31, 16, 4, 7, 4),     # No = 4, ragged last tile
     (30, 14, 12, 9, 6),    # NB = 6 neighbour slots

@@ -20,7 +20,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="paper")
 ap.add_argument("--atoms", type=int, default=64)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--lib", default=None, help="libsse.so to load instead of the in-tree build (A/B runs)")
 args = ap.parse_args()
+if args.lib:
+    from paper_1912_08810_b200 import _lib
+    _lib.LIB_PATH = os.path.abspath(args.lib)
 p, grid, nmap = config(args.config)
 world = max(1, p.n_A // args.atoms)
 prob = ShardProblem(p, rank=world // 2, world=world, seed=0, grid=grid, idx=nmap.idx)
