@@ -19,7 +19,11 @@ ap.add_argument("--config", default="paper")
 ap.add_argument("--atoms", type=int, default=64)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--nw", type=int, default=0, help="override the number of phonon frequencies")
+ap.add_argument("--lib", default=None, help="libsse.so to load instead of the in-tree build (A/B runs)")
 args = ap.parse_args()
+if args.lib:
+    from paper_1912_08810_b200 import _lib
+    _lib.LIB_PATH = os.path.abspath(args.lib)
 p, grid, nmap = config(args.config)
 if args.nw:
     import dataclasses
