@@ -16,6 +16,10 @@ new = ("  auto run = [&](auto two_c) {\n    constexpr bool TWO = decltype(two_c)
        "  if (two) run(std::true_type{});\n  else run(std::false_type{});\n")
 s = s[:i] + new + s[j:]
 s = s.replace("#include <cstdlib>", "#include <cstdlib>\n#include <type_traits>")
+if os.environ.get("K6_SYNCWARP"):  # lane 0 releases the slot only after the whole warp is done with it
+    k = s.index("pi_dmma4_kernel(PiArgs p")
+    a = s.index("    if (lane == 0) mbar_arrive(empty + slot);\n", k)
+    s = s[:a] + "    __syncwarp();\n" + s[a:]
 open(os.path.join(dst, "sse_kernels.cu"), "w").write(s)
 cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
        "-shared", "-o", "/tmp/k6h/libsse.so", os.path.join(dst, "sse_kernels.cu"), os.path.join(dst, "sse_capi.cu"),
