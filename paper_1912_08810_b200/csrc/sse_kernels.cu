@@ -1759,6 +1759,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
       a1 = load_a(kq + 2);
       ++kq;
     }
+    __syncwarp();  // the warp is done with the slot before lane 0 releases it
     if (LAST_PRODUCES) {
       if (lane == 0) {
         unsigned old;
