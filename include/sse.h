@@ -282,6 +282,11 @@ typedef struct sse_profile {
 int sse_profile_begin(sse_ctx* ctx);
 int sse_profile_end(sse_ctx* ctx, sse_profile* out);
 
+/* Name (with template arguments) of the kernel of kind SSE_PROF_* the library
+ * launched last in this process, e.g. "sigma_dmma_slide_kernel<12,12,3>";
+ * "" before the first launch of that kind or for an unknown kind. */
+const char* sse_kernel_name(int kind);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,7 @@ EXPORTED = (
     "sse_fill_synthetic",
     "sse_profile_begin",
     "sse_profile_end",
+    "sse_kernel_name",
 )
 
 PROF_KINDS = ("operator", "sigma", "layout", "preprocess", "pi_build", "pi", "pi_assemble")
@@ -143,11 +144,18 @@ def load() -> ctypes.CDLL:
         lib.sse_fill_synthetic.argtypes = [
             _P, ctypes.c_uint64, ctypes.c_uint32, i64, i64, i64, i64, i64, i64, dbl, _P, _P,
         ]
+        lib.sse_kernel_name.argtypes = [i32]
+        lib.sse_kernel_name.restype = ctypes.c_char_p
         for name in EXPORTED:
-            if name not in ("sse_ctx_destroy", "sse_last_error"):
+            if name not in ("sse_ctx_destroy", "sse_last_error", "sse_kernel_name"):
                 getattr(lib, name).restype = i32
         _lib = lib
         return lib
+
+
+def kernel_name(kind: str) -> str:
+    """Name of the kernel of ``kind`` (one of PROF_KINDS) libsse launched last in this process."""
+    return load().sse_kernel_name(PROF_KINDS.index(kind)).decode()
 
 
 def check(rc: int) -> None:

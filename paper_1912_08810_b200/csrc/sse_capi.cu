@@ -108,6 +108,12 @@ struct DevState {
   std::vector<ProfRec> recs;
   // pipeline events (grow-only pool)
   std::vector<cudaEvent_t> pipe;
+  // The cached scratch (op, nbr, off, wt, pi_vt, pi_part, pp_*) is shared by
+  // every call on this device; a call on another stream than the previous
+  // one first waits for the previous call's last use of it (scratch_done).
+  cudaEvent_t scratch_done = nullptr;
+  cudaStream_t scratch_stream = nullptr;
+  bool scratch_pending = false;
 
   cudaEvent_t prof_event() {
     if (pool_used == pool.size()) {
@@ -168,7 +174,29 @@ int init_dev(DevState& d, int device) {
   CU(cudaStreamCreateWithFlags(&d.s_h2d, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&d.s_d2h, cudaStreamNonBlocking));
   for (auto& e : d.ev) CU(cudaEventCreate(&e));
+  CU(cudaEventCreateWithFlags(&d.scratch_done, cudaEventDisableTiming));
   return SSE_OK;
+}
+
+// Order a call on stream st after the previous call's use of the shared scratch.
+int scratch_enter(DevState& ds, cudaStream_t st) {
+  if (ds.scratch_pending && ds.scratch_stream != st) CU(cudaStreamWaitEvent(st, ds.scratch_done, 0));
+  return SSE_OK;
+}
+// Mark the end of this call's use of the scratch (its last kernel is queued on st).
+int scratch_leave(DevState& ds, cudaStream_t st) {
+  CU(cudaEventRecord(ds.scratch_done, st));
+  ds.scratch_stream = st;
+  ds.scratch_pending = true;
+  return SSE_OK;
+}
+
+// Error paths of the host calls: earlier chunks' copies may still be in flight into
+// (or out of) the caller's host buffers; wait for them before reporting the error.
+void drain(DevState& ds) {
+  for (cudaStream_t s : {ds.stream, ds.s_h2d, ds.s_d2h})
+    if (s) cudaStreamSynchronize(s);
+  cudaGetLastError();
 }
 
 void destroy_dev(DevState& d) {
@@ -182,6 +210,7 @@ void destroy_dev(DevState& d) {
     if (e) cudaEventDestroy(e);
   for (auto& e : d.pool) cudaEventDestroy(e);
   for (auto& e : d.pipe) cudaEventDestroy(e);
+  if (d.scratch_done) cudaEventDestroy(d.scratch_done);
   for (cudaStream_t s : {d.stream, d.s_h2d, d.s_d2h})
     if (s) cudaStreamDestroy(s);
 }
@@ -208,6 +237,17 @@ int validate_grid(const sse_dims* d, const int64_t* off, const double* wt) {
     if (!std::isfinite(wt[w]))
       return fail(SSE_EINVAL, "frequency weight %g (index %lld) is not finite", wt[w], (long long)w);
   }
+  return SSE_OK;
+}
+
+// Pi entry points: offsets in [0, NE) and a finite energy weight (params.py:158-162)
+int validate_offsets(const sse_dims* d, const int64_t* off, double energy_weight) {
+  if (!off) return fail(SSE_EINVAL, "frequency map is NULL");
+  for (int64_t w = 0; w < d->nw; ++w)
+    if (off[w] < 0 || off[w] >= d->ne)
+      return fail(SSE_EINVAL, "frequency offset %lld (index %lld) outside [0, %lld)", (long long)off[w],
+                  (long long)w, (long long)d->ne);
+  if (!std::isfinite(energy_weight)) return fail(SSE_EINVAL, "energy weight is not finite");
   return SSE_OK;
 }
 
@@ -539,7 +579,7 @@ cudaEvent_t pipe_event(DevState& ds, size_t i) {
 }
 
 // One device's share of a host-memory call: owned atoms [lo, hi) (global ids).
-int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi, sse_timing* t) {
+int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_t hi, sse_timing* t) {
   const sse_dims* d = c.d;
   CU(cudaSetDevice(ds.device));
   const int64_t on = hi - lo;
@@ -699,6 +739,26 @@ int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi,
     t->kernel_launches += launches;
   }
   return SSE_OK;
+}
+
+// Run `body` for one device of a host call: ordered after the previous call's use of the
+// shared scratch; on error the in-flight host copies are drained before returning.
+template <class F>
+int guarded(DevState& ds, F&& body) {
+  CU(cudaSetDevice(ds.device));
+  CHECK(scratch_enter(ds, ds.stream));
+  const int rc = body();
+  if (rc != SSE_OK) {
+    const std::string err = g_last_error;
+    drain(ds);
+    g_last_error = err;
+    return rc;
+  }
+  return scratch_leave(ds, ds.stream);
+}
+
+int host_call_on_device(DevState& ds, const HostCall& c, int64_t lo, int64_t hi, sse_timing* t) {
+  return guarded(ds, [&] { return host_call_on_device_body(ds, c, lo, hi, t); });
 }
 
 // Reverse-slot table of the owned edges (device.py:53-66): for owned atom a and
@@ -879,7 +939,9 @@ int sse_sigma_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const s
   int launches = 0;
   const DevPtrs p{(const double2*)G_l, (const double2*)G_g, (const double2*)Dc_l,
                   (const double2*)Dc_g, (const double2*)dH, (double2*)Sig_l, (double2*)Sig_g};
+  CHECK(scratch_enter(ds, st));
   CHECK(sigma_on_device(ds, d, *g, *out, p, nmap, off, wt, st, &launches));
+  CHECK(scratch_leave(ds, st));
   if (t) {
     CU(cudaEventRecord(ds.ev[1], st));
     CU(cudaEventSynchronize(ds.ev[1]));
@@ -942,7 +1004,9 @@ int sigma_peer_impl(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const ss
   int launches = 0;
   const DevPtrs p{(const double2*)G_l, (const double2*)G_g, (const double2*)Dc_l,
                   (const double2*)Dc_g, (const double2*)dH, nullptr, nullptr};
+  CHECK(scratch_enter(ds, st));
   const int rc = sigma_on_device(ds, d, *g, *out, p, nmap, off, wt, st, &launches, 2, &sc);
+  if (rc == SSE_OK) CHECK(scratch_leave(ds, st));
   if (rc == SSE_ECUDA && gather && std::string(g_last_error).find("not supported") != std::string::npos)
     return fail(SSE_EINVAL, "peer gather needs the sliding-window K3 (sliding offsets, Nw >= 12, No <= 16)");
   CHECK(rc);
@@ -987,6 +1051,7 @@ int sse_pi_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out, con
   CHECK(validate_dims(d));
   CHECK(validate_slab(d, out, "output"));
   if (!G_l || !G_g || !dH || !nmap || !off || !pt_lo || !Pi_l || !Pi_g) return fail(SSE_EINVAL, "NULL tensor pointer");
+  CHECK(validate_offsets(d, off, energy_weight));
   if (nranks < 1 || nranks > sse::kMaxScatter)
     return fail(SSE_EINVAL, "peer gather needs 1..%d ranks (got %d)", sse::kMaxScatter, nranks);
   if (pt_lo[0] != 0 || pt_lo[nranks] != d->nkz * d->ne) return fail(SSE_EINVAL, "point ranges must cover [0, Nkz*NE)");
@@ -1012,8 +1077,10 @@ int sse_pi_device_peer(sse_ctx* ctx, const sse_dims* d, const sse_slab* out, con
   }
   int launches = 0;
   const sse_slab all{0, d->na, 1, 0};
+  CHECK(scratch_enter(ds, st));
   const int rc = pi_on_device(ds, d, all, *out, nullptr, nullptr, (const double2*)dH, nmap, off, energy_weight, nullptr,
                               (double2*)Pi_l, (double2*)Pi_g, st, &launches, &pg);
+  if (rc == SSE_OK) CHECK(scratch_leave(ds, st));
   if (rc == SSE_ECUDA && std::string(g_last_error).find("not supported") != std::string::npos)
     return fail(SSE_EINVAL, "Pi peer gather needs the DMMA operand build and K6 v3/v4 (No in {4,8,12,16})");
   CHECK(rc);
@@ -1113,12 +1180,7 @@ int sse_pi_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_
                   double* Pi_g, void* stream, sse_timing* t) {
   if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
   CHECK(validate_dims(d));
-  if (!off) return fail(SSE_EINVAL, "frequency map is NULL");
-  for (int64_t w = 0; w < d->nw; ++w)
-    if (off[w] < 0 || off[w] >= d->ne)
-      return fail(SSE_EINVAL, "frequency offset %lld (index %lld) outside [0, %lld)", (long long)off[w],
-                  (long long)w, (long long)d->ne);
-  if (!std::isfinite(energy_weight)) return fail(SSE_EINVAL, "energy weight is not finite");
+  CHECK(validate_offsets(d, off, energy_weight));
   CHECK(validate_slab(d, g, "G"));
   CHECK(validate_slab(d, out, "output"));
   if (!G_l || !G_g || !dH || !nmap || !Pi_l || !Pi_g) return fail(SSE_EINVAL, "NULL tensor pointer");
@@ -1131,8 +1193,10 @@ int sse_pi_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_
     CU(cudaEventRecord(ds.ev[0], st));
   }
   int launches = 0;
+  CHECK(scratch_enter(ds, st));
   CHECK(pi_on_device(ds, d, *g, *out, (const double2*)G_l, (const double2*)G_g, (const double2*)dH, nmap,
                      off, energy_weight, mask, (double2*)Pi_l, (double2*)Pi_g, st, &launches));
+  CHECK(scratch_leave(ds, st));
   if (t) {
     CU(cudaEventRecord(ds.ev[1], st));
     CU(cudaEventSynchronize(ds.ev[1]));
@@ -1149,6 +1213,7 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
   CHECK(validate_dims(d));
   if (atom_lo < 0 || atom_hi > d->na || atom_lo > atom_hi) return fail(SSE_EINVAL, "invalid atom range");
   if (!G_l || !G_g || !dH || !nmap || !Pi_l || !Pi_g || !off) return fail(SSE_EINVAL, "NULL tensor pointer");
+  CHECK(validate_offsets(d, off, energy_weight));
   if (t) std::memset(t, 0, sizeof(*t));
   if (atom_lo == atom_hi) return SSE_OK;
   const int nd = (int)ctx->devs.size();
@@ -1216,7 +1281,10 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
     }
     return SSE_OK;
   };
-  if (nd == 1) return on_device(ctx->devs[0], atom_lo, atom_hi, t);
+  auto run_dev = [&](DevState& ds, int64_t lo, int64_t hi, sse_timing* tt) {
+    return guarded(ds, [&] { return on_device(ds, lo, hi, tt); });
+  };
+  if (nd == 1) return run_dev(ctx->devs[0], atom_lo, atom_hi, t);
   std::vector<int> rcs(nd, SSE_OK);
   std::vector<sse_timing> ts(nd);
   std::vector<std::string> errs(nd);
@@ -1225,7 +1293,7 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
     th.emplace_back([&, i] {
       std::memset(&ts[i], 0, sizeof(sse_timing));
       const int64_t lo = atom_lo + std::min<int64_t>(i * per, span), hi = atom_lo + std::min<int64_t>((i + 1) * per, span);
-      rcs[i] = on_device(ctx->devs[i], lo, hi, &ts[i]);
+      rcs[i] = run_dev(ctx->devs[i], lo, hi, &ts[i]);
       if (rcs[i] != SSE_OK) errs[i] = g_last_error;
     });
   for (auto& x : th) x.join();
@@ -1327,7 +1395,10 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
     }
     return SSE_OK;
   };
-  if (nd == 1) return on_device(ctx->devs[0], 0, d->na, t);
+  auto run_dev = [&](DevState& ds, int64_t lo, int64_t hi, sse_timing* tt) {
+    return guarded(ds, [&] { return on_device(ds, lo, hi, tt); });
+  };
+  if (nd == 1) return run_dev(ctx->devs[0], 0, d->na, t);
   std::vector<int> rcs(nd, SSE_OK);
   std::vector<sse_timing> ts(nd);
   std::vector<std::string> errs(nd);
@@ -1336,7 +1407,7 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
     th.emplace_back([&, i] {
       std::memset(&ts[i], 0, sizeof(sse_timing));
       const int64_t lo = std::min<int64_t>(i * per, d->na), hi = std::min<int64_t>((i + 1) * per, d->na);
-      rcs[i] = on_device(ctx->devs[i], lo, hi, &ts[i]);
+      rcs[i] = run_dev(ctx->devs[i], lo, hi, &ts[i]);
       if (rcs[i] != SSE_OK) errs[i] = g_last_error;
     });
   for (auto& x : th) x.join();
@@ -1385,6 +1456,7 @@ int sse_preprocess_D(sse_ctx* ctx, int64_t nqz, int64_t nw, int64_t na, int64_t 
   DevState& ds = ctx->devs[0];
   CU(cudaSetDevice(ds.device));
   cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  CHECK(scratch_enter(ds, st));
   CHECK(upload_cached(ds.pp_nbr, ds.pp_nbr_host, nbr, st));
   CHECK(upload_cached(ds.pp_rev, ds.pp_rev_host, rev, st));
   CHECK(profiled(ds, st, SSE_PROF_PREPROCESS, 0.0, [&] {
@@ -1392,6 +1464,7 @@ int sse_preprocess_D(sse_ctx* ctx, int64_t nqz, int64_t nw, int64_t na, int64_t 
                                     ds.pp_nbr.as<int>(), ds.pp_rev.as<int>(), (const double2*)D,
                                     (double2*)Dc, st);
   }));
+  CHECK(scratch_leave(ds, st));
   if (!stream) CU(cudaStreamSynchronize(st));
   return SSE_OK;
 }
@@ -1411,6 +1484,8 @@ int sse_fill_synthetic(sse_ctx* ctx, uint64_t seed, uint32_t tensor_id, int64_t 
   if (!stream) CU(cudaStreamSynchronize(st));
   return SSE_OK;
 }
+
+const char* sse_kernel_name(int kind) { return sse::last_kernel_name(kind); }
 
 int sse_profile_begin(sse_ctx* ctx) {
   if (!ctx) return fail(SSE_EINVAL, "context is NULL");

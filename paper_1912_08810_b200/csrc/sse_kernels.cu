@@ -14,10 +14,22 @@
 // algebra; results agree with the reference to rounding (tests/).
 #include "sse_kernels.cuh"
 
+#include <cstdarg>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
 namespace sse {
+
+// last launched kernel per kind (bench / smoke evidence of which variant ran)
+static char g_kernel_name[7][192];
+static void note_kernel(int kind, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_kernel_name[kind], sizeof(g_kernel_name[kind]), fmt, ap);
+  va_end(ap);
+}
+const char* last_kernel_name(int kind) { return kind >= 0 && kind < 7 ? g_kernel_name[kind] : ""; }
 
 // --------------------------------------------------------------------------
 // K1: layout transform.  One warp per (k, E, a) block of blk_vec 16-byte
@@ -2226,6 +2238,7 @@ cudaError_t launch_layout_transform(long long nkz, long long ne, long long na, l
                                     int to_atom_major, const double2* src, double2* dst,
                                     cudaStream_t st) {
   const long long warps = nkz * ne * na;
+  note_kernel(2, "layout_transform_kernel");
   layout_transform_kernel<<<grid_for(warps * 32, 256), 256, 0, st>>>(nkz, ne, na, blk_vec,
                                                                      to_atom_major, src, dst);
   return cudaGetLastError();
@@ -2238,6 +2251,7 @@ cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  note_kernel(0, "build_operator_kernel");
   build_operator_kernel<<<a.chunk_atoms * a.nb, 256, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -2265,6 +2279,7 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
   if (a.gather_ranks > 0 && !slide_ok) return cudaErrorNotSupported;  // peer gather: sliding-window K3 only
   if (choice == 0 && a.gather_ranks == 0) {
     const dim3 grid = grid_for_rows(kRowsPerCta);
+    note_kernel(1, "sigma_dmma_kernel<%d>", NO);
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
   } else if ((choice == 3 || a.gather_ranks > 0) && a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw) {
     // nw >= kSlideStages: the kSlideStages stages in flight span at most one
@@ -2276,13 +2291,16 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
       const size_t smem = SlideGeom<NO, 12, 3>::kSmem;
       cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
+      note_kernel(1, "sigma_dmma_slide_kernel<%d,12,3>", NO);
       sigma_dmma_slide_kernel<NO, 12, 3><<<grid, 12 * 32, smem, st>>>(a);
       return cudaSuccess;
     }
     const dim3 grid = grid_for_rows(kRowsPerCta);
+    note_kernel(1, "sigma_dmma_pipe_kernel<%d>", NO);
     sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
   } else {
     const dim3 grid = grid_for_rows(kRowsPerCta);
+    note_kernel(1, "sigma_dmma_pipe_kernel<%d>", NO);
     sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
   }
   return cudaSuccess;
@@ -2314,6 +2332,7 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
     if (a.gather_ranks > 0) return cudaErrorNotSupported;
     const long long total = (long long)a.nkz * a.ne * a.no * a.no * chunk_atoms;
     dim3 grid(grid_for(total, 256), a.npol);
+    note_kernel(1, "sigma_generic_kernel");
     sigma_generic_kernel<<<grid, 256, 0, st>>>(a, chunk_atoms);
   }
   return cudaGetLastError();
@@ -2325,6 +2344,7 @@ static cudaError_t launch_pi_build_dmma(const PiBuildArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(pi_build_dmma_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPB2Energies - 1) / kPB2Energies);
+  note_kernel(4, "pi_build_dmma_kernel<%d>", NO);
   pi_build_dmma_kernel<NO><<<(unsigned)blocks, kPB2Warps * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -2359,6 +2379,7 @@ cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPiBuildEnergies - 1) / kPiBuildEnergies);
+  note_kernel(4, "pi_build_kernel");
   pi_build_kernel<<<(unsigned)blocks, kPiBuildThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -2427,12 +2448,15 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
           if (e == cudaSuccess) e = cudaFuncSetAttribute(both, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
           if (e != cudaSuccess) return e;
           const long long tails = (long long)chunk_atoms * 2 * a.echunks * ((a.nqz + 3) / 4);
+          note_kernel(5, "pi_dmma4_kernel<12,4,4,3,4,true>");
           both<<<dim3(gx + (unsigned)tails, 1u), 4 * 32, smem4, st>>>(a, chunk_atoms);
         } else {
+          note_kernel(5, "pi_dmma4_kernel<12,4,4,3,4>");
           kern<<<dim3(gx, (unsigned)((pairs + 3) / 4)), 4 * 32, smem4, st>>>(a, chunk_atoms);
         }
         break;
       }
+      note_kernel(5, "pi_dmma4_kernel<12,4>");
       pi_dmma4_kernel<12, 4><<<dim3(gx, (unsigned)((pairs + kPi4Warps - 1) / kPi4Warps)), kPi4Warps * 32, smem, st>>>(
           a, chunk_atoms);
       break;
@@ -2448,6 +2472,7 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
       const int groups = ((a.nw + 7) / 8) * (((2 * a.ncol + 7) / 8 + kPi3NT - 1) / kPi3NT);
+      note_kernel(5, fixed ? "pi_dmma3_kernel<%d,12,4>" : "pi_dmma3_kernel<%d,0,0>", (int)last);
       kern<<<dim3(gx, (unsigned)((groups + kPiWarps - 1) / kPiWarps)), kPiWarps * 32, smem, st>>>(a, chunk_atoms);
       break;
     }
@@ -2456,6 +2481,7 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(pi_dmma2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
+      note_kernel(5, "pi_dmma2_kernel");
       pi_dmma2_kernel<<<dim3(gx, gy), kPiWarps * 32, smem, st>>>(a, chunk_atoms);
       break;
     case 1: {
@@ -2463,10 +2489,12 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       const int qblocks = (a.nqz + kPiQB - 1) / kPiQB;
       dim3 grid((unsigned)((long long)chunk_atoms * 2 * qblocks * a.echunks), gy);
+      note_kernel(5, "pi_dmma_kernel");
       pi_dmma_kernel<<<grid, kPiWarps * 32, smem, st>>>(a, chunk_atoms);
       break;
     }
     default:
+      note_kernel(5, "pi_dmma_direct_kernel");
       pi_dmma_direct_kernel<<<dim3(gx, gy), kPiWarps * 32, 0, st>>>(a, chunk_atoms);
   }
   return cudaGetLastError();
@@ -2474,6 +2502,7 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
 
 cudaError_t launch_pi_assemble(const PiAssembleArgs& a, cudaStream_t st) {
   const long long total = (long long)a.chunk_atoms * 2 * a.nqz * a.nw * 9;
+  note_kernel(6, "pi_assemble_kernel");
   pi_assemble_kernel<<<grid_for(total, 256), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
@@ -2483,6 +2512,7 @@ cudaError_t launch_preprocess_D(long long nqz, long long nw, long long d_natoms,
                                 const int* nbr, const int* rev, const double2* D, double2* Dc,
                                 cudaStream_t st) {
   const long long total = nqz * nw * out_natoms * nb * 9;
+  note_kernel(3, "preprocess_D_kernel");
   preprocess_D_kernel<<<grid_for(total, 256), 256, 0, st>>>(nqz * nw, d_natoms, d_atom0, out_atom0,
                                                             out_natoms, nb, nbr, rev, D, Dc);
   return cudaGetLastError();

@@ -159,6 +159,11 @@ cudaError_t launch_fill_synthetic(uint64_t seed, uint32_t tensor_id, long long a
                                   long long atom_stride, long long outer_stride, double scale,
                                   double2* dst, cudaStream_t st);
 
+// Name of the kernel (with its template arguments) last launched per kind, in
+// the SSE_PROF_* order of include/sse.h (0 operator build, 1 Sigma, 2 layout,
+// 3 preprocess_D, 4 Pi operand build, 5 Pi chains, 6 Pi assembly); "" if none.
+const char* last_kernel_name(int kind);
+
 // Bytes of the per-chunk operator buffer (one polarity).
 inline size_t operator_bytes(int no, int nb, int nqz, int nw, int chunk_atoms) {
   size_t per = (no <= kMaxDmmaOrb) ? (size_t)frag_geom(no).fv * 32 : (size_t)no * no;

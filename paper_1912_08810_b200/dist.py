@@ -360,10 +360,14 @@ class PeerPointBuffers:
     def close(self) -> None:
         from . import _lib
 
+        import torch.distributed as dist
+
         for ptr in self._opened:
             _lib.check(self._lib.sse_ipc_close(self._ctx.handle, ctypes.c_void_p(ptr)))
         self._opened = []
         self.tensors = []
+        # every peer has unmapped this rank's buffers before they are freed
+        dist.barrier(group=self.group)
         for ptr in self.local:
             _lib.check(self._lib.sse_dev_free(self._ctx.handle, ctypes.c_void_p(ptr)))
         self.local = []

@@ -345,6 +345,23 @@ def _dptr(t):
 _CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 
+def _check_dev(t, shape, name: str, device=None) -> None:
+    """A contiguous complex128 CUDA tensor of exactly ``shape`` (on ``device`` if given):
+    the C side only sees raw pointers, so a mismatch would be an out-of-bounds access."""
+    import torch
+
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.complex128:
+        raise ValueError(f"{name} must be complex128, got {t.dtype}")
+    if tuple(t.shape) != tuple(int(x) for x in shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+
+
 def _stream_ptr(stream):
     """cudaStream_t of a torch stream (default: torch's current stream).
 
@@ -360,6 +377,29 @@ def _stream_ptr(stream):
 
 def _device_ctx(t):
     return _lib.context(device=t.device.index if t.device.index is not None else 0)
+
+
+def _electron_shape(n_kz, n_e, atoms, n_o, atom_major):
+    return (atoms, n_kz, n_e, n_o, n_o) if atom_major else (n_kz, n_e, atoms, n_o, n_o)
+
+
+def _check_slab_args(g_l, g_g, dc_l, dc_g, dh, out_l, out_g, atom_major) -> None:
+    """Shapes of a device Sigma call: G slab pair, Dc pair / dH of the owned atoms, Sigma pair."""
+    if atom_major:
+        g_atoms, n_kz, n_e, n_o = (int(x) for x in g_l.shape[:4])
+        o_atoms = int(out_l.shape[0])
+    else:
+        n_kz, n_e, g_atoms, n_o = (int(x) for x in g_l.shape[:4])
+        o_atoms = int(out_l.shape[2])
+    dev = g_l.device
+    _check_dev(g_l, _electron_shape(n_kz, n_e, g_atoms, n_o, atom_major), "g_l", dev)
+    _check_dev(g_g, g_l.shape, "g_g", dev)
+    _check_dev(out_l, _electron_shape(n_kz, n_e, o_atoms, n_o, atom_major), "out_l", dev)
+    _check_dev(out_g, out_l.shape, "out_g", dev)
+    n_qz, n_w, _, n_b = (int(x) for x in dc_l.shape[:4])
+    _check_dev(dc_l, (n_qz, n_w, o_atoms, n_b, 3, 3), "dc_l", dev)
+    _check_dev(dc_g, dc_l.shape, "dc_g", dev)
+    _check_dev(dh, (o_atoms, n_b, 3, n_o, n_o), "dh", dev)
 
 
 def sigma_device(
@@ -403,6 +443,7 @@ def sigma_device(
     idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
     if idx.shape != (o_atoms, n_b):
         raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    _check_slab_args(g_l, g_g, dc_l, dc_g, dh, out_l, out_g, atom_major)
     offs = np.ascontiguousarray(offsets, dtype=np.int64)
     wts = np.ascontiguousarray(weights, dtype=np.float64)
     dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
@@ -441,6 +482,12 @@ def sigma_device_scatter(
     idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
     if idx.shape != (o_atoms, n_b):
         raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    dev = g_l.device
+    _check_dev(g_l, _electron_shape(n_kz, n_e, g_atoms, n_o, atom_major), "g_l", dev)
+    _check_dev(g_g, g_l.shape, "g_g", dev)
+    _check_dev(dc_l, (n_qz, n_w, o_atoms, n_b, 3, 3), "dc_l", dev)
+    _check_dev(dc_g, dc_l.shape, "dc_g", dev)
+    _check_dev(dh, (o_atoms, n_b, 3, n_o, n_o), "dh", dev)
     nranks = len(targets_l)
     if len(targets_g) != nranks or len(pt_lo) != nranks + 1:
         raise ValueError("one target per rank and nranks + 1 point bounds")
@@ -478,6 +525,9 @@ def sigma_device_peer(
     idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
     if idx.shape != (o_atoms, n_b):
         raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
+    _check_dev(dc_l, (n_qz, n_w, o_atoms, n_b, 3, 3), "dc_l")
+    _check_dev(dc_g, dc_l.shape, "dc_g", dc_l.device)
+    _check_dev(dh, (o_atoms, n_b, 3, n_o, n_o), "dh", dc_l.device)
     nranks = len(targets_l)
     if not (len(targets_g) == len(sources_l) == len(sources_g) == nranks) or len(pt_lo) != nranks + 1:
         raise ValueError("one source and target per rank and nranks + 1 point bounds")
@@ -543,6 +593,9 @@ def pi_device_peer(
     if len(sources_g) != nranks or len(pt_lo) != nranks + 1:
         raise ValueError("one source per rank and nranks + 1 point bounds")
     n_w = out_l.shape[1]
+    _check_dev(dh, (o_atoms, n_b, 3, n_o, n_o), "dh")
+    _check_dev(out_l, (n_qz, n_w, o_atoms, n_b + 1, 3, 3), "out_l", dh.device)
+    _check_dev(out_g, out_l.shape, "out_g", dh.device)
     offs = np.ascontiguousarray(offsets, dtype=np.int64)
     bounds = np.ascontiguousarray(pt_lo, dtype=np.int64)
     arr = lambda xs: (ctypes.c_void_p * nranks)(*[int(x) for x in xs])  # noqa: E731
@@ -574,8 +627,18 @@ def pi_device(
         n_kz, n_e, g_atoms, n_o = g_l.shape[0], g_l.shape[1], g_l.shape[2], g_l.shape[3]
     o_atoms, n_b = dh.shape[0], dh.shape[1]
     idx = np.ascontiguousarray(nmap_rows, dtype=np.int64)
+    if idx.shape != (o_atoms, n_b):
+        raise ValueError(f"nmap rows must have shape {(o_atoms, n_b)}")
     offs = np.ascontiguousarray(offsets, dtype=np.int64)
+    dev = g_l.device
+    _check_dev(g_l, _electron_shape(n_kz, n_e, g_atoms, n_o, atom_major), "g_l", dev)
+    _check_dev(g_g, g_l.shape, "g_g", dev)
+    _check_dev(dh, (o_atoms, n_b, 3, n_o, n_o), "dh", dev)
+    _check_dev(pi_l, (n_qz, len(offs), o_atoms, n_b + 1, 3, 3), "pi_l", dev)
+    _check_dev(pi_g, pi_l.shape, "pi_g", dev)
     mask = None if point_mask is None else np.ascontiguousarray(point_mask, dtype=np.uint8)
+    if mask is not None and mask.shape != (n_kz, n_e):
+        raise ValueError(f"point mask must have shape ({n_kz}, {n_e})")
     dims = _lib.SseDims(n_kz, n_qz, n_e, len(offs), n_a, n_b, n_o)
     gs = _lib.SseSlab(g_atom0, g_atoms, int(atom_major), 0)
     os_ = _lib.SseSlab(out_atom0, o_atoms, int(atom_major), 0)
@@ -594,8 +657,12 @@ def layout_transform(src, dst, to_atom_major: bool, stream=None) -> None:
     """
     if to_atom_major:
         n_kz, n_e, n_a = src.shape[:3]
+        want = (n_a, n_kz, n_e) + tuple(src.shape[3:])
     else:
         n_a, n_kz, n_e = src.shape[:3]
+        want = (n_kz, n_e, n_a) + tuple(src.shape[3:])
+    _check_dev(src, src.shape, "src")
+    _check_dev(dst, want, "dst", src.device)
     blk = int(np.prod(src.shape[3:])) * 2
     rc = _lib.load().sse_layout_transform(
         _device_ctx(src).handle, n_kz, n_e, n_a, blk, int(to_atom_major), _dptr(src), _dptr(dst),
@@ -619,6 +686,8 @@ def preprocess_D_device(d, dc, nmap_idx: Array, *, d_atom0: int = 0, out_atom0: 
         raise ValueError(
             f"missing neighbor slot: tensor has {n_slots - 1} slots for {idx.shape[-1]} neighbors"
         )
+    _check_dev(d, (n_qz, n_w, d_atoms, n_slots, 3, 3), "d")
+    _check_dev(dc, (n_qz, n_w, o_atoms, n_slots - 1, 3, 3), "dc", d.device)
     rc = _lib.load().sse_preprocess_D(
         _device_ctx(d).handle, n_qz, n_w, idx.shape[0], idx.shape[1], _ptr(idx), d_atom0, d_atoms,
         out_atom0, o_atoms, _dptr(d), _dptr(dc), _stream_ptr(stream),
@@ -629,6 +698,11 @@ def preprocess_D_device(d, dc, nmap_idx: Array, *, d_atom0: int = 0, out_atom0: 
 def fill_synthetic(dst, seed: int, tensor_id: int, atom0: int, natoms: int, outer: int, inner: int,
                    atom_stride: int, outer_stride: int, scale: float = 1.0, stream=None) -> None:
     """Device side of :func:`paper_1912_08810_b200.inputs.atom_keyed_values`."""
+    _check_dev(dst, dst.shape, "dst")
+    if natoms > 0:  # the last element written must lie inside dst
+        last = (natoms - 1) * atom_stride + (outer - 1) * outer_stride + inner - 1
+        if min(atom_stride, outer_stride) < 0 or last >= dst.numel():
+            raise ValueError(f"fill of {natoms} x {outer} x {inner} values overruns dst ({dst.numel()} elements)")
     rc = _lib.load().sse_fill_synthetic(
         _device_ctx(dst).handle, ctypes.c_uint64(seed), ctypes.c_uint32(tensor_id), atom0, natoms,
         outer, inner, atom_stride, outer_stride, float(scale), _dptr(dst), _stream_ptr(stream),

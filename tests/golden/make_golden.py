@@ -161,7 +161,26 @@ def criterion5():
     print("criterion5: 50 instances")
 
 
+def slide_cases():
+    """Shapes that run the production sliding-window Sigma kernel (Nw >= 12, sliding default offsets).
+
+    slide_orb12: No = 12, NB = 4 (the paper's block shape), 480 rows per (atom, k) -> one full and
+    one partial 288-row CTA; slide_orb10: No = 10 (the small config's block); paperlike_w70: the
+    paper's Nw = 70 and offsets 1..70 with NE = 90, so offsets run past the top energy of the first
+    CTAs (empty stages) and each (q, s) segment crosses the stage ring many times.
+    """
+    run_case("slide_orb12_s9", SimParams(n_kz=3, n_qz=3, n_E=40, n_w=14, n_A=6, n_B=4, n_orb=12), 9,
+             dh_scale=0.05, store_bf=False)
+    run_case("slide_orb10_s10", SimParams(n_kz=3, n_qz=3, n_E=48, n_w=16, n_A=6, n_B=4, n_orb=10), 10,
+             dh_scale=0.05, store_bf=False)
+    run_case("paperlike_w70_s11", SimParams(n_kz=3, n_qz=2, n_E=90, n_w=70, n_A=4, n_B=2, n_orb=12), 11,
+             dh_scale=0.05, store_bf=False)
+
+
 def main():
+    if sys.argv[1:] == ["slide"]:
+        slide_cases()
+        return
     scalar_kat()
     criterion5()
     # test_sse.py TINY instance recipe (seeds 3, 4)
@@ -188,6 +207,7 @@ def main():
         energy_weight=0.1,
     )
     run_case("general_grid_s8", p, 8, grid=grid, with_pi=True)
+    slide_cases()
 
 
 if __name__ == "__main__":

@@ -19,8 +19,9 @@ from paper_1912_08810_b200.problem import ShardProblem
 class DeviceProblem(ShardProblem):
     """Rank `rank` of a `world`-way atom sharding, on device `rank`, halo filled locally."""
 
-    def __init__(self, name, seed=0, world=1, rank=0):
-        super().__init__(inputs.CONFIGS[name], rank=rank, world=world, device=rank, seed=seed)
+    def __init__(self, name, seed=0, world=1, rank=0, device=None):
+        super().__init__(inputs.CONFIGS[name], rank=rank, world=world, device=rank if device is None else device,
+                         seed=seed)
 
     def launch(self):
         with self.torch.cuda.device(self.device):
@@ -55,12 +56,8 @@ def host_point(prob: ShardProblem, pol: int, k: int, e: int, a: int) -> np.ndarr
     atoms = sorted(set(nbrs) | {a})
     draw = inputs.atom_keyed_values(seed, d_tid, atoms, p.n_qz * p.n_w, (p.n_B + 1) * 9)
     d = {x: draw[i].reshape(p.n_qz, p.n_w, p.n_B + 1, 3, 3) for i, x in enumerate(atoms)}
-    # Dc[:, :, a] from the reference formula (sse.py:105-113) with reverse slots
-    dc_a = np.empty((p.n_qz, p.n_w, p.n_B, 3, 3), dtype=np.complex128)
-    for s in range(p.n_B):
-        b = int(idx[a, s])
-        rev = int(np.nonzero(idx[b] == a)[0][0])
-        dc_a[:, :, s] = d[b][:, :, 1 + rev] - d[b][:, :, 0] - d[a][:, :, 0] + d[a][:, :, 1 + s]
+    # Dc[:, :, a] from the reference formula (sse.py:105-113), pinned in tests/test_oracle.py
+    dc_a = orc.preprocess_D_atom(lambda x: d[x], idx, a)
     dh_a = inputs.atom_keyed_dh(seed, p, [a])[0]
     return orc.sigma_point(lambda kk, ee, b: gvals[b][kk, ee], dc_a, dh_a, idx[a], prob.offsets,
                            prob.weights, p.n_kz, p.n_qz, k, e)

@@ -165,3 +165,42 @@ def test_reduction_order_permutation():
     np.random.default_rng(0).shuffle(order)
     out = orc.sigma_reference(c.g_l, c.g_g, dc_l, dc_g, c.dh, c.idx, c.offsets, c.weights, qws_order=order)
     assert orc.parity_dev(out[0], out[1], base[0], base[1]) <= 1e-12
+
+
+def test_preprocess_D_atom_matches_reference(case):
+    """The per-atom Dc restatement used by the full-size parity checks (tests/scale_helpers.py)
+    is bitwise equal to the reference's preprocess_D (pinned by the fixture digest)."""
+    dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    assert digest(dc_l, dc_g) == case.meta["dc_sha256"]
+    for a in range(case.p.n_A):
+        assert np.array_equal(orc.preprocess_D_atom(lambda x: case.d_l[:, :, x], case.idx, a), dc_l[:, :, a])
+        assert np.array_equal(orc.preprocess_D_atom(lambda x: case.d_g[:, :, x], case.idx, a), dc_g[:, :, a])
+
+
+def _points(p, offsets, cap=160, seed=0):
+    """Every (k, E, a) of a small case, else a deterministic sample with the edge energies
+    (0, 1, the largest offset, NE - 1) and the chain-end atoms always included."""
+    allpts = list(itertools.product(range(p.n_kz), range(p.n_E), range(p.n_A)))
+    if len(allpts) <= cap:
+        return allpts
+    rng = np.random.default_rng(seed)
+    es = sorted({0, min(1, p.n_E - 1), min(int(max(offsets)), p.n_E - 1), p.n_E - 1})
+    pts = {(k, e, a) for k in range(p.n_kz) for e in es for a in (0, p.n_A - 1)}
+    while len(pts) < cap:
+        pts.add((int(rng.integers(p.n_kz)), int(rng.integers(p.n_E)), int(rng.integers(p.n_A))))
+    return sorted(pts)
+
+
+def test_sigma_point_matches_reference(case):
+    """oracle.sigma_point — the checker of every full-size run (small, paper, kheavy, large and the
+    bench's in-run check) — against the reference's own Sigma at every (or a sampled set of) (k, E, a)."""
+    p = case.p
+    dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
+    scale = max(np.max(np.abs(case.arrays["sigma_l"])), np.max(np.abs(case.arrays["sigma_g"])))
+    worst = 0.0
+    for k, e, a in _points(p, case.offsets):
+        for g_arr, dc, ref in ((case.g_l, dc_l, case.arrays["sigma_l"]), (case.g_g, dc_g, case.arrays["sigma_g"])):
+            got = orc.sigma_point(lambda kk, ee, b: g_arr[kk, ee, b], dc[:, :, a], case.dh[a], case.idx[a],
+                                  case.offsets, case.weights, p.n_kz, p.n_qz, k, e)
+            worst = max(worst, float(np.max(np.abs(got - ref[k, e, a]))) / scale)
+    assert worst <= 1e-14, (case.name, worst)
