@@ -36,25 +36,11 @@ FP64_PEAK_TFLOPS = 36.85  # measured DMMA.8x8x4 sustained, profiles/r01_fp64_pea
 FP64_PEAK_SOURCE = "measured DMMA m8n8k4 sustained on this pool's B200 (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry"
 
 
-def k3_kernel_name() -> str:
-    """The K3 variant libsse launches for the bench workload (SSE_SIGMA_KERNEL, default 3)."""
-    return {
-        "0": "sigma_dmma_kernel<12> (K3 simple)",
-        "1": "sigma_dmma_pipe_kernel<12> (K3 register-pipelined)",
-    }.get(os.environ.get("SSE_SIGMA_KERNEL", "3"),
-          "sigma_dmma_slide_kernel<12,12,3> (K3 TMA sliding window, 12 warps x 3 row tiles)")
+def launched_kernel(kind: str) -> str:
+    """Name (with template arguments) of the kernel of `kind` libsse actually launched last."""
+    from paper_1912_08810_b200 import _lib
 
-
-def k6_kernel_name() -> str:
-    """The K6 variant libsse launches for the bench workload (SSE_PI_KERNEL, default 3)."""
-    return {
-        "0": "pi_dmma_direct_kernel (K6 direct)",
-        "1": "pi_dmma_kernel (K6 v1, 2 momenta per CTA)",
-        "2": "pi_dmma2_kernel (K6 v2, half stages)",
-        "3": "pi_dmma3_kernel (K6 v3: one m-tile x 9 n-tiles per warp, TMA ring of V, 3 CTAs/SM)",
-    }.get(os.environ.get("SSE_PI_KERNEL", "4"),
-          "pi_dmma4_kernel<12,4,4,3,4,true> (K6 v4: 2 lag tiles x 9 n-tiles per warp, 4-warp CTAs for lag "
-          "tiles 0-7 + tail CTAs for the 9th tile of every q in the same launch, TMA ring of V)")
+    return _lib.kernel_name(kind)
 
 
 def env_rank():
@@ -128,41 +114,49 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle BATCHED_FUSED port) on a bounded pair sample
+# CPU reference: the UNMODIFIED reference negflow (oracle/_ref) on single (atom, slot) pairs
 # ---------------------------------------------------------------------------
-def cpu_sample(p, grid, idx, n_pairs: int, seed: int = 0, first_atom: int | None = None) -> dict:
-    """Time the reference's BATCHED_FUSED algorithm (oracle port) on n_pairs (atom, slot) pairs.
+def sample_pairs(p) -> list[tuple[int, int]]:
+    """The (atom, neighbour slot) pairs the reference arm cycles through: both chain ends
+    (duplicate neighbour slots, device.py:123-127) and interior atoms, every slot."""
+    na, nb = p.n_A, p.n_B
+    atoms = [0, na - 1, 1, na - 2, na // 2, na // 4, 3 * na // 4, na // 2 + 1]
+    return [(a, i % nb) for i, a in enumerate(atoms)]
 
-    The per-pair work of BATCHED_FUSED is independent of NA (sse.py:279-301),
-    so seconds per Born iteration = per-pair time x NA x NB.
+
+def negflow_pair(nf, p, idx, a: int, s: int, seed: int = 0) -> dict:
+    """Sigma contribution of ONE (atom a, slot s) pair through the reference's own entry point
+    negflow.sse.sse_sigma(BATCHED_FUSED) (sse.py:265-329), timed.
+
+    The pair is a one-atom sub-problem with the self-map idx = [[0]] (sse_sigma checks neither
+    f(a,s) != a nor reverse closure, sse.py:315-318): G column = G[:, :, f(a,s)], Dc row =
+    Dc[:, :, a, s], dH row = dH[a, s], the full config's frequency map.  BATCHED_FUSED's per-pair
+    work is independent of NA (sse.py:279-301), so NA * NB of these are one Sigma evaluation, and
+    the NB pairs of an atom sum to Sigma[:, :, a].
     """
     from oracle import sse_oracle as orc
     from paper_1912_08810_b200 import inputs
 
-    a0 = p.n_A // 2 if first_atom is None else first_atom
-    pairs_g = [(a0 + i // p.n_B, i % p.n_B) for i in range(n_pairs)]
-    out_atoms = sorted({a for a, _ in pairs_g})
-    others = sorted({int(idx[a, s]) for a in out_atoms for s in range(p.n_B)} - set(out_atoms))
-    order = out_atoms + others  # sub-problem atoms: sampled outputs first, then their neighbours
-    pos = {a: i for i, a in enumerate(order)}
-    sub_idx = np.zeros((len(order), p.n_B), dtype=np.int64)
-    for a in out_atoms:
-        sub_idx[pos[a]] = [pos[int(idx[a, s])] for s in range(p.n_B)]
-    g_l = inputs.atom_keyed_electron(seed, inputs.G_LESSER, p, order)
-    g_g = inputs.atom_keyed_electron(seed, inputs.G_GREATER, p, order)
-    rng = np.random.default_rng(seed)
-    shape = (p.n_qz, p.n_w, len(order), p.n_B, 3, 3)
-    dc_l = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
-    dc_g = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
-    dh = inputs.atom_keyed_dh(seed, p, order)
-    off, wt = np.array(grid.offsets), np.array(grid.weights)
-    pairs = [(pos[a], s) for a, s in pairs_g]
+    b = int(idx[a, s])
+    g_l = inputs.atom_keyed_electron(seed, inputs.G_LESSER, p, [b])
+    g_g = inputs.atom_keyed_electron(seed, inputs.G_GREATER, p, [b])
+    atoms = sorted({a, *(int(x) for x in idx[a])})
+    dcs = []
+    for tid in (inputs.D_LESSER, inputs.D_GREATER):
+        raw = inputs.atom_keyed_values(seed, tid, atoms, p.n_qz * p.n_w, (p.n_B + 1) * 9)
+        d = {x: raw[i].reshape(p.n_qz, p.n_w, p.n_B + 1, 3, 3) for i, x in enumerate(atoms)}
+        dcs.append(orc.preprocess_D_atom(lambda x: d[x], idx, a)[:, :, s].reshape(p.n_qz, p.n_w, 1, 1, 3, 3))
+    dh = inputs.atom_keyed_dh(seed, p, [a])[:, s:s + 1].copy()
+    ref_p = nf.params.SimParams(n_kz=p.n_kz, n_qz=p.n_qz, n_E=p.n_E, n_w=p.n_w, n_A=p.n_A, n_B=p.n_B,
+                                n_orb=p.n_orb)
+    grid = nf.params.default_grid(ref_p)
+    g = nf.gf.GreensTensor(g_l, g_g)
+    dc = nf.sse.CombinedD(dcs[0], dcs[1])
+    nmap = nf.device.NeighborMap(np.zeros((1, 1), dtype=np.int64))
     t0 = time.perf_counter()
-    orc.sigma_batched_fused(g_l, g_g, dc_l, dc_g, dh, sub_idx, off, wt, pairs=pairs)
+    out = nf.sse.sse_sigma(nf.sse.SseVariant.BATCHED_FUSED, g, dc, dh, nmap, grid)
     dt = time.perf_counter() - t0
-    per_pair = dt / n_pairs
-    return {"seconds": dt, "per_pair_s": per_pair, "pairs": n_pairs,
-            "extrapolated_s": per_pair * p.n_A * p.n_B}
+    return {"seconds": dt, "atom": a, "slot": s, "sigma_l": out.lesser[:, :, 0], "sigma_g": out.greater[:, :, 0]}
 
 
 def blas_threads() -> int:
@@ -174,33 +168,54 @@ def blas_threads() -> int:
         return 1
 
 
+def ref_provenance() -> str:
+    from oracle.ref import ref_path
+
+    path = ref_path()
+    return f"{os.path.relpath(path, REPO) if path.startswith(REPO) else path}/negflow (unmodified reference)"
+
+
+def bench_config(args, p) -> dict:
+    """The workload both arms measure (identical dicts, so the driver can match the arms)."""
+    return {"workload": workload_name(p), "name": args.config,
+            "l2": "no flush: inputs (G 47.5 GB at paper) >> 126 MB L2"}
+
+
 def run_reference(args, p, grid, idx) -> None:
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    n_pairs = args.ref_pairs
-    for _ in range(args.warmup):
-        cpu_sample(p, grid, idx, n_pairs)
-    samples = [cpu_sample(p, grid, idx, n_pairs) for _ in range(args.steps)]
-    per_pair = float(np.mean([s["per_pair_s"] for s in samples]))
+    from oracle.ref import import_negflow
+
+    nf = import_negflow()
+    pairs = sample_pairs(p)
+    for i in range(args.warmup):
+        negflow_pair(nf, p, idx, *pairs[i % len(pairs)])
+    times = []
+    for i in range(args.steps):
+        a, s = pairs[i % len(pairs)]
+        times.append((a, s, negflow_pair(nf, p, idx, a, s)["seconds"]))
+    per_pair = float(np.mean([t for _, _, t in times]))
     value = per_pair * p.n_A * p.n_B
     from paper_1912_08810_b200.sse import alg_flops
 
     flops = alg_flops(p.n_kz, p.n_qz, p.n_E, p.n_A, p.n_B, p.n_orb, grid.offsets)
+    sample = (f"{args.steps} steps, one (atom, neighbour) pair each, cycling {len(pairs)} pairs (chain ends "
+              f"and interior atoms, every slot) through negflow.sse.sse_sigma(BATCHED_FUSED) "
+              f"(sse.py:265-329, the fastest reference arrangement) at the real per-pair shapes; "
+              f"value = mean s/pair x NA*NB={p.n_A * p.n_B}; numpy/OpenBLAS {blas_threads()} threads of "
+              f"{os.cpu_count()} host cores (the path is ~1 busy core)")
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
-        "data": "synthetic (atom-keyed generator)",
-        "config": {"workload": workload_name(p), "name": args.config, "parallelism": "cpu"},
+        "data": "synthetic (atom-keyed generator)", "parallelism": "cpu (reference)",
+        "config": bench_config(args, p),
         "tflops": flops / value / 1e12,
-        "cpu_baseline": {
-            "value": value, "unit": "s", "cores": blas_threads(), "kind": "port",
-            "sample": (f"{n_pairs} (atom, neighbour) pairs per step of the reference BATCHED_FUSED algorithm "
-                       f"(oracle/sse_oracle.py:sigma_batched_fused, sse.py:265-302) at the real per-pair "
-                       f"shapes, x NA*NB={p.n_A * p.n_B}; numpy/OpenBLAS with {blas_threads()} threads "
-                       f"of {os.cpu_count()} host cores (the path is ~1 busy core)"),
-        },
+        "per_pair_s": {"mean": per_pair, "min": min(t for *_, t in times), "max": max(t for *_, t in times),
+                       "pairs": [{"atom": a, "slot": s, "s": t} for a, s, t in times]},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": blas_threads(), "kind": "reference",
+                         "sample": sample, "reference": ref_provenance()},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -398,7 +413,7 @@ def pi_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, s
     pi_info = {
         "s_per_eval": pi_ms / 1e3, "steps": args.pi_steps, "tflops": pi_flops / (pi_ms * 1e-3) / 1e12,
         "flops_alg": pi_flops,
-        "roofline": {"bound": "tensor", "kernel": k6_kernel_name(),
+        "roofline": {"bound": "tensor", "kernel": launched_kernel("pi"), "build_kernel": launched_kernel("pi_build"),
                      "achieved": k6_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": k6_tflops / FP64_PEAK_TFLOPS},
         "kernels": {k: pprof.result[k] for k in ("pi_build", "pi", "pi_assemble")},
@@ -597,9 +612,14 @@ def gf_fused_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, 
 
 
 def cpu_baseline_leg(args, p, grid, idx, prob):
-    """The bench's CPU leg: parity of a few Sigma blocks of this run against the oracle
-    (pointwise, host regeneration of the atom-keyed inputs) and the reference algorithm
-    (oracle port of BATCHED_FUSED) timed on a bounded sample."""
+    """The bench's CPU leg (rank 0, N = 1).
+
+    * check: a few Sigma blocks of this run against the pointwise oracle (oracle.sigma_point,
+      pinned to the reference by tests/test_oracle.py);
+    * cpu_baseline: the UNMODIFIED reference (negflow from oracle/_ref) on the NB pairs of one
+      chain-end atom, timed; their sum is the reference's Sigma[:, :, a] over every (k, E) and is
+      compared with this run's GPU Sigma of that atom (reference_atom_parity).
+    """
     check = None
     if args.check:
         sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -613,14 +633,30 @@ def cpu_baseline_leg(args, p, grid, idx, prob):
                     ref = host_point(prob, pol, k, e, a)
                     worst = max(worst, float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)))
         check = worst
-    cpu = None
-    if args.cpu_pairs > 0:
-        s = cpu_sample(p, grid, idx, args.cpu_pairs)
-        cpu = {"value": s["extrapolated_s"], "unit": "s", "cores": blas_threads(), "kind": "port",
-               "sample": (f"{s['pairs']} (atom, neighbour) pairs of the reference BATCHED_FUSED algorithm "
-                          f"(oracle port of sse.py:265-302) at the real per-pair shapes in {s['seconds']:.1f} s, "
-                          f"x NA*NB={p.n_A * p.n_B}; {os.cpu_count()} host cores, ~1 busy")}
-    return check, cpu
+    cpu, atom_parity = None, None
+    if args.cpu_atoms > 0:
+        from oracle.ref import import_negflow
+
+        nf = import_negflow()
+        a = p.n_A - 1
+        runs = [negflow_pair(nf, p, idx, a, s) for s in range(p.n_B)]
+        secs = [r["seconds"] for r in runs]
+        ref_l = sum(r["sigma_l"] for r in runs)
+        ref_g = sum(r["sigma_g"] for r in runs)
+        got_l = prob.sig[0][a - prob.lo].cpu().numpy()
+        got_g = prob.sig[1][a - prob.lo].cpu().numpy()
+        scale = max(np.max(np.abs(ref_l)), np.max(np.abs(ref_g)))
+        dev = max(np.max(np.abs(got_l - ref_l)), np.max(np.abs(got_g - ref_g))) / scale
+        atom_parity = {"atom": a, "blocks": int(2 * p.n_kz * p.n_E), "max_rel_dev": float(dev),
+                       "metric": "max|gpu - ref| / max(max|ref<|, max|ref>|) over Sigma[:, :, a] (test_acceptance.py:163-171)"}
+        per_pair = float(np.mean(secs))
+        cpu = {"value": per_pair * p.n_A * p.n_B, "unit": "s", "cores": blas_threads(), "kind": "reference",
+               "sample": (f"the {p.n_B} (atom, neighbour) pairs of chain-end atom {a} through "
+                          f"negflow.sse.sse_sigma(BATCHED_FUSED) (unmodified reference, sse.py:265-329) in "
+                          f"{sum(secs):.1f} s ({min(secs):.2f}-{max(secs):.2f} s per pair), x NA*NB="
+                          f"{p.n_A * p.n_B} / {p.n_B}; {os.cpu_count()} host cores, ~1 busy"),
+               "reference": ref_provenance()}
+    return check, cpu, atom_parity
 
 
 def run_gpu(args, p, grid, idx) -> None:
@@ -665,6 +701,7 @@ def run_gpu(args, p, grid, idx) -> None:
         barrier(world)
     step_ms = start.elapsed_time(end) / args.steps
     step_ms = allreduce_max(step_ms, world)
+    k3_name = launched_kernel("sigma")
     total_flops = alg_flops(p.n_kz, p.n_qz, p.n_E, p.n_A, p.n_B, p.n_orb, grid.offsets)
     sig = prof.result["sigma"]
     k3_ms_per_launch = sig["ms"] / max(sig["launches"], 1)
@@ -679,9 +716,9 @@ def run_gpu(args, p, grid, idx) -> None:
 
     # cpu_baseline leg (rank 0, N = 1): the reference algorithm timed on the host cores, and the
     # oracle as the checker of a few output blocks of this run (the only oracle use in the bench)
-    check, cpu = None, None
+    check, cpu, atom_parity = None, None, None
     if rank == 0 and world == 1:
-        check, cpu = cpu_baseline_leg(args, p, grid, idx, prob)
+        check, cpu, atom_parity = cpu_baseline_leg(args, p, grid, idx, prob)
 
     common = (args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream)
     pi_info = pi_phase(*common)
@@ -710,17 +747,14 @@ def run_gpu(args, p, grid, idx) -> None:
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128 (f64)",
             "data": "synthetic (atom-keyed counter-based generator, filled on device)",
-            "config": {
-                "workload": workload_name(p), "name": args.config,
-                "parallelism": f"atom-shard x{world}" + (" + NCCL G halo exchange" if world > 1 else ""),
-                "l2": "no flush: inputs (G 47.5 GB) >> 126 MB L2",
-                "step": "preprocess_D + operator build (K2) + fused DMMA Sigma (K3), both polarities"
-                        + (" + G halo exchange" if world > 1 else ""),
-            },
+            "config": bench_config(args, p),
+            "parallelism": f"atom-shard x{world}" + (" + NCCL G halo exchange" if world > 1 else ""),
+            "step": "preprocess_D + operator build (K2) + fused DMMA Sigma (K3), both polarities"
+                    + (" + G halo exchange" if world > 1 else ""),
             "tflops": total_flops / (step_ms * 1e-3) / 1e12,
             "tflops_per_gpu": total_flops / (step_ms * 1e-3) / 1e12 / world,
             "roofline": {
-                "bound": "tensor", "kernel": k3_kernel_name(),
+                "bound": "tensor", "kernel": k3_name,
                 "achieved": k3_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": k3_tflops / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
@@ -736,6 +770,8 @@ def run_gpu(args, p, grid, idx) -> None:
                             "bytes_per_step": sdist.halo_bytes(plan, p.n_kz * p.n_E * p.n_orb**2 * 16)}
         if check is not None:
             line["parity_check_max_rel_dev"] = check
+        if atom_parity is not None:
+            line["reference_atom_parity"] = atom_parity
         if pi_info is not None:
             line["pi"] = pi_info
             # the whole SSE phase of a Born iteration (sse.py:532-534): Sigma (`value`, SURVEY 8d's
@@ -768,8 +804,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1)
-    ap.add_argument("--cpu-pairs", type=int, default=2, help="pairs timed for cpu_baseline (0 = skip)")
-    ap.add_argument("--ref-pairs", type=int, default=1, help="pairs per step of --impl reference")
+    ap.add_argument("--cpu-atoms", type=int, default=1,
+                    help="cpu_baseline: time the reference on the NB pairs of one atom and compare (0 = skip)")
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--pi-steps", type=int, default=1, help="timed Pi evaluations after Sigma (0 = skip)")
     ap.add_argument("--phase-steps", type=int, default=0,

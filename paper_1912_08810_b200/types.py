@@ -85,6 +85,52 @@ class SimParams:
         return replace(self, **kwargs)
 
 
+# params.py:11-21 soft ranges (warnings only) and the integer count fields
+_TYPICAL_RANGES = {"n_kz": (1, 21), "n_qz": (1, 21), "n_E": (700, 1500), "n_w": (10, 100), "n_B": (4, 50),
+                   "n_orb": (1, 30)}
+_COUNT_FIELDS = ("n_kz", "n_qz", "n_E", "n_w", "n_A", "n_B", "n_orb", "n_3D", "bnum")
+
+
+@dataclass(frozen=True)
+class ValidationReport:
+    """Result of :func:`validate` (params.py:71-81)."""
+
+    ok: bool
+    violations: tuple[str, ...]
+    warnings: tuple[str, ...]
+
+
+def validate(params: SimParams) -> ValidationReport:
+    """The reference's hard invariants and soft ranges of a parameter set (params.py:84-129);
+    report-only, never raises."""
+    violations: list[str] = []
+    warnings: list[str] = []
+    ints = {name: isinstance(getattr(params, name), (int, np.integer)) for name in _COUNT_FIELDS}
+    for name in _COUNT_FIELDS:
+        value = getattr(params, name)
+        if not ints[name]:
+            violations.append(f"{name} must be an integer, got {value!r}")
+        elif value < 1:
+            violations.append(f"{name} must be >= 1, got {value}")
+    if ints["n_3D"] and params.n_3D != 3:
+        violations.append("n_3D must equal 3")
+    if ints["n_A"] and ints["bnum"] and params.bnum >= 1 and params.n_A >= 1 and params.n_A % params.bnum != 0:
+        violations.append(f"n_A must be divisible by bnum ({params.n_A} % {params.bnum} != 0)")
+    if params.n_qz > params.n_kz:
+        violations.append(f"n_qz must be <= n_kz ({params.n_qz} > {params.n_kz})")
+    if ints["n_A"] and ints["n_B"] and params.n_A % 2 == 1 and params.n_B % 2 == 1:
+        violations.append(f"n_A * n_B must be even (got n_A={params.n_A}, n_B={params.n_B})")
+    if params.n_w >= params.n_E:
+        violations.append(f"n_w must be < n_E ({params.n_w} >= {params.n_E})")
+    if not params.eta > 0:
+        violations.append(f"eta must be > 0, got {params.eta}")
+    for name, (lo, hi) in _TYPICAL_RANGES.items():
+        value = getattr(params, name)
+        if ints.get(name, isinstance(value, (int, np.integer))) and value >= 1 and not lo <= value <= hi:
+            warnings.append(f"{name} outside [{lo},{hi}]: {value}")
+    return ValidationReport(ok=not violations, violations=tuple(violations), warnings=tuple(warnings))
+
+
 @dataclass(frozen=True)
 class GreensTensor:
     """Lesser/greater pair; electron 5-D, phonon 6-D (gf.py:37-69)."""
@@ -189,6 +235,12 @@ class EnergyGrid:
         vals = np.asarray(self.values, dtype=float)
         if vals.ndim != 1 or vals.size < 1:
             raise ValueError("energy grid must be a non-empty 1-D sequence")
+        if vals.size > 1:  # params.py:151-156
+            steps = np.diff(vals)
+            if np.any(steps <= 0):
+                raise ValueError("energy grid must be strictly increasing")
+            if not np.allclose(steps, steps[0], rtol=1e-9, atol=1e-12):
+                raise ValueError("energy grid must be uniformly spaced")
         n_e = vals.size
         for w, (off, weight) in enumerate(self.frequency_map):
             if not isinstance(off, (int, np.integer)) or not 0 <= off < n_e:

@@ -1,8 +1,10 @@
 """C-ABI boundary checks that need no GPU: symbols, loading, error mapping."""
 
 import ctypes
+import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -121,6 +123,40 @@ def test_types_mirror_reference_validation():
         NeighborMap(np.zeros((2, 2)))
     with pytest.raises(ValueError, match="outside"):
         EnergyGrid(values=(0.0, 1.0), frequency_map=((2, 1.0),), energy_weight=1.0)
+    # params.py:151-156: the grid itself must be strictly increasing and uniform
+    with pytest.raises(ValueError, match="strictly increasing"):
+        EnergyGrid(values=(0.0, 1.0, 0.5), frequency_map=((1, 1.0),), energy_weight=1.0)
+    with pytest.raises(ValueError, match="uniformly spaced"):
+        EnergyGrid(values=(0.0, 1.0, 3.0), frequency_map=((1, 1.0),), energy_weight=1.0)
+
+
+@pytest.mark.parametrize("kwargs", [
+    dict(n_kz=3, n_qz=3, n_E=706, n_w=70, n_A=4864, n_B=4, n_orb=12),   # paper: ok
+    dict(n_kz=3, n_qz=3, n_E=32, n_w=4, n_A=64, n_B=4, n_orb=4),        # tiny: ok with warnings
+    dict(n_kz=2, n_qz=3, n_E=8, n_w=2, n_A=8, n_B=2, n_orb=2),          # n_qz > n_kz
+    dict(n_kz=3, n_qz=2, n_E=4, n_w=4, n_A=5, n_B=3, n_orb=2),          # n_w >= n_E, odd n_A * n_B
+    dict(n_kz=3, n_qz=2, n_E=8, n_w=2, n_A=9, n_B=2, n_orb=2, bnum=4),  # n_A % bnum
+    dict(n_kz=0, n_qz=1, n_E=8, n_w=2, n_A=8, n_B=2, n_orb=2, eta=0.0),  # count < 1, eta <= 0
+])
+def test_validate_mirrors_reference(kwargs):
+    """SimParams validation (params.py:84-129): the same verdict, violations and warnings as
+    the reference's validate() when the reference is importable (build container)."""
+    from paper_1912_08810_b200.types import SimParams, validate
+
+    rep = validate(SimParams(**kwargs))
+    assert rep.ok == (not rep.violations)
+    ref_src = "/root/reference/pkg/src"
+    if not os.path.isdir(ref_src):
+        return
+    sys.path.insert(0, ref_src)
+    try:
+        from negflow.params import SimParams as RefParams
+        from negflow.params import validate as ref_validate
+
+        want = ref_validate(RefParams(**kwargs))
+    finally:
+        sys.path.remove(ref_src)
+    assert (rep.ok, rep.violations, rep.warnings) == (want.ok, want.violations, want.warnings)
 
 
 def test_sse_phase_argument_errors():
