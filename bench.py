@@ -253,69 +253,132 @@ def barrier(world):
         dist.barrier()
 
 
-def e2e_phase(args, p, grid, idx, rank, world, local_rank) -> dict:
-    """Per-rank host-memory drop-in call (pinned buffers, H2D/D2H inside)."""
+def _host_inputs(p, idx, glo, gA, lo, oA, local_rank, pinned: bool):
+    """The step's inputs in host memory (same atom-keyed values as the resident run, generated on
+    the device and copied out once): G slab [Nkz, NE, gA, No, No], Dc / dH of the owned atoms.
+    pinned=False gives pageable numpy arrays (what a reference caller hands over)."""
     import torch
 
     from paper_1912_08810_b200 import inputs
     from paper_1912_08810_b200 import sse as dev
+
+    no2 = p.n_orb * p.n_orb
+    cuda = torch.device("cuda", local_rank)
+
+    def host(t):
+        if pinned:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+        return t.cpu().numpy()
+
+    g = []
+    for tid in (inputs.G_LESSER, inputs.G_GREATER):
+        tmp = torch.empty((p.n_kz, p.n_E, gA, p.n_orb, p.n_orb), dtype=torch.complex128, device=cuda)
+        dev.fill_synthetic(tmp, 0, tid, glo, gA, p.n_kz * p.n_E, no2, no2, gA * no2)
+        g.append(host(tmp))
+        del tmp
+    slots = (p.n_B + 1) * 9
+    dc = []
+    for tid in (inputs.D_LESSER, inputs.D_GREATER):
+        d = torch.empty((p.n_qz, p.n_w, gA, p.n_B + 1, 3, 3), dtype=torch.complex128, device=cuda)
+        dev.fill_synthetic(d, 0, tid, glo, gA, p.n_qz * p.n_w, slots, slots, gA * slots)
+        out = torch.empty((p.n_qz, p.n_w, oA, p.n_B, 3, 3), dtype=torch.complex128, device=cuda)
+        dev.preprocess_D_device(d, out, idx, d_atom0=glo, out_atom0=lo)
+        dc.append(host(out))
+        del d, out
+    dht = torch.empty((oA, p.n_B, 3, p.n_orb, p.n_orb), dtype=torch.complex128, device=cuda)
+    inner = p.n_B * 3 * no2
+    dev.fill_synthetic(dht, 0, inputs.DH, lo, oA, 1, inner, inner, 0, scale=inputs.DH_SCALE)
+    dh = host(dht)
+    del dht
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return g, dc, dh
+
+
+def _digest(arrays) -> int:
+    """Layout-independent bit checksum (wrap-around int64 sum of the raw doubles)."""
+    tot = 0
+    for a in arrays:
+        v = a if isinstance(a, np.ndarray) else a.numpy()
+        tot += int(v.view(np.int64).sum(dtype=np.int64))
+    return tot & ((1 << 64) - 1)
+
+
+def e2e_phase(args, p, grid, idx, rank, world, local_rank, want_digest) -> dict:
+    """End to end through the public API, host memory in and out, H2D/D2H inside the timed region.
+
+    N = 1: `paper_1912_08810_b200.sse_sigma(BATCHED_FUSED, GreensTensor, CombinedD, dH, NeighborMap,
+    EnergyGrid)` -- the drop-in for negflow.sse.sse_sigma (sse.py:305-329) -- on pageable numpy
+    arrays, output allocated by the call as the reference does, wall clock (perf_counter) around
+    the call.  N > 1: each rank's share through sigma_host_slab (sse_sigma_c128_slab) on pageable
+    numpy slabs.  Also timed from pinned buffers (e2e.pinned), the same C-ABI pipeline without the
+    staging ring.  The outputs are checked bit-for-bit against the device-resident run (digest).
+    """
+    from paper_1912_08810_b200 import sse as dev
     from paper_1912_08810_b200.problem import chunk
+    from paper_1912_08810_b200.types import CombinedD, GreensTensor, NeighborMap, SseVariant
 
     lo, hi = chunk(p.n_A, world, rank)
     rows = idx[lo:hi]
     glo, ghi = int(min(lo, rows.min())), int(max(hi, rows.max() + 1))
     gA, oA = ghi - glo, hi - lo
-    no2 = p.n_orb * p.n_orb
-    cuda = torch.device("cuda", local_rank)
-    pin = dict(dtype=torch.complex128, pin_memory=True)
-    g_host = [torch.empty((p.n_kz, p.n_E, gA, p.n_orb, p.n_orb), **pin) for _ in range(2)]
-    s_host = [torch.empty((p.n_kz, p.n_E, oA, p.n_orb, p.n_orb), **pin) for _ in range(2)]
-    dc_host = [torch.empty((p.n_qz, p.n_w, oA, p.n_B, 3, 3), **pin) for _ in range(2)]
-    dh_host = torch.empty((oA, p.n_B, 3, p.n_orb, p.n_orb), **pin)
-    # inputs generated on the device (same atom-keyed values as the resident run), copied once
-    for pol, tid in ((0, inputs.G_LESSER), (1, inputs.G_GREATER)):
-        tmp = torch.empty(g_host[pol].shape, dtype=torch.complex128, device=cuda)
-        dev.fill_synthetic(tmp, 0, tid, glo, gA, p.n_kz * p.n_E, no2, no2, gA * no2)
-        g_host[pol].copy_(tmp)
-        del tmp
-    slots = (p.n_B + 1) * 9
-    for pol, tid in ((0, inputs.D_LESSER), (1, inputs.D_GREATER)):
-        d = torch.empty((p.n_qz, p.n_w, gA, p.n_B + 1, 3, 3), dtype=torch.complex128, device=cuda)
-        dev.fill_synthetic(d, 0, tid, glo, gA, p.n_qz * p.n_w, slots, slots, gA * slots)
-        dc = torch.empty(dc_host[pol].shape, dtype=torch.complex128, device=cuda)
-        dev.preprocess_D_device(d, dc, idx, d_atom0=glo, out_atom0=lo)
-        dc_host[pol].copy_(dc)
-        del d, dc
-    dht = torch.empty(dh_host.shape, dtype=torch.complex128, device=cuda)
-    inner = p.n_B * 3 * no2
-    dev.fill_synthetic(dht, 0, inputs.DH, lo, oA, 1, inner, inner, 0, scale=inputs.DH_SCALE)
-    dh_host.copy_(dht)
-    del dht
-    torch.cuda.synchronize()
-    torch.cuda.empty_cache()
-
     offs, wts = np.array(grid.offsets), np.array(grid.weights)
+    res = {}
+    for pinned in (False, True):
+        g, dc, dh = _host_inputs(p, idx, glo, gA, lo, oA, local_rank, pinned)
+        if world == 1 and not pinned:
+            g_t, dc_t, nmap = GreensTensor(g[0], g[1]), CombinedD(dc[0], dc[1]), NeighborMap(idx)
 
-    def call():
-        return dev.sigma_host_slab(g_host[0], g_host[1], dc_host[0], dc_host[1], dh_host, rows, offs, wts,
-                                   s_host[0], s_host[1], n_a=p.n_A, g_atom0=glo, out_atom0=lo,
-                                   device=local_rank)
+            def call(tim):
+                out = dev.sse_sigma(SseVariant.BATCHED_FUSED, g_t, dc_t, dh, nmap, grid, timing=tim)
+                return out.lesser, out.greater
+        else:
+            import torch
 
-    for _ in range(args.e2e_warmup):
-        call()
-    times, tim = [], None
-    for _ in range(args.e2e_steps):
-        barrier(world)
-        tim = call()
-        times.append(tim["total_ms"])
-    t = allreduce_max(float(np.mean(times)), world)
-    h2d = allreduce_sum(float(tim["h2d_bytes"]), world)
-    d2h = allreduce_sum(float(tim["d2h_bytes"]), world)
-    out = {"value": t / 1e3, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "steps": args.e2e_steps, "warmup": args.e2e_warmup,
-           "path": "sse_sigma_c128_slab (C ABI) from pinned host memory, 3-stream H2D/compute/D2H pipeline"}
-    del g_host, s_host, dc_host, dh_host
-    return out
+            shape = (p.n_kz, p.n_E, oA, p.n_orb, p.n_orb)
+            outs = ([torch.empty(shape, dtype=torch.complex128, pin_memory=True) for _ in range(2)] if pinned
+                    else None)
+
+            def call(tim):
+                o = outs if pinned else [np.zeros(shape, dtype=np.complex128) for _ in range(2)]
+                tim.update(dev.sigma_host_slab(g[0], g[1], dc[0], dc[1], dh, rows, offs, wts, o[0], o[1],
+                                               n_a=p.n_A, g_atom0=glo, out_atom0=lo, device=local_rank))
+                return o[0], o[1]
+        for _ in range(args.e2e_warmup):
+            call({})
+        times, tim, out = [], {}, None
+        for _ in range(args.e2e_steps):
+            barrier(world)
+            tim = {}
+            out = None
+            t0 = time.perf_counter()
+            out = call(tim)
+            times.append(time.perf_counter() - t0)
+        same = float(_digest(out) == want_digest)
+        same = -allreduce_max(-same, world)
+        t = allreduce_max(float(np.mean(times)), world)
+        h2d = allreduce_sum(float(tim["h2d_bytes"]), world)
+        d2h = allreduce_sum(float(tim["d2h_bytes"]), world)
+        entry = {"value": t, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                 "steps": args.e2e_steps, "warmup": args.e2e_warmup, "step_s": times,
+                 "bitwise_equal_to_device_run": bool(same == 1.0),
+                 "host_pack_ms": tim.get("h2d_ms"), "host_unpack_ms": tim.get("d2h_ms"),
+                 "staged": tim.get("staged"), "host_threads": tim.get("host_threads")}
+        if pinned:
+            entry["path"] = ("sigma_host_slab -> sse_sigma_c128_slab (C ABI) from pinned torch buffers: direct DMA "
+                             "in the 3-stream H2D / compute / D2H pipeline")
+            res["pinned"] = entry
+        else:
+            entry["path"] = (("paper_1912_08810_b200.sse_sigma (the drop-in, public API) on pageable numpy arrays, "
+                              "output allocated by the call; " if world == 1 else
+                              "sigma_host_slab (sse_sigma_c128_slab, C ABI) on pageable numpy slabs per rank; ")
+                             + "libsse stages through its pinned ring (host worker pool) under the compute; "
+                               "wall clock around the call")
+            res.update(entry)
+        del g, dc, dh, out, call
+    return res
 
 
 def phase_e2e(args, p, grid, idx, local_rank) -> dict:
@@ -702,6 +765,8 @@ def run_gpu(args, p, grid, idx) -> None:
     step_ms = start.elapsed_time(end) / args.steps
     step_ms = allreduce_max(step_ms, world)
     k3_name = launched_kernel("sigma")
+    # layout-independent bit checksum of this rank's Sigma (checked against the e2e outputs)
+    sig_digest = sum(int(torch.view_as_real(t).view(torch.int64).sum()) for t in prob.sig) & ((1 << 64) - 1)
     total_flops = alg_flops(p.n_kz, p.n_qz, p.n_E, p.n_A, p.n_B, p.n_orb, grid.offsets)
     sig = prof.result["sigma"]
     k3_ms_per_launch = sig["ms"] / max(sig["launches"], 1)
@@ -733,7 +798,7 @@ def run_gpu(args, p, grid, idx) -> None:
 
     e2e = None
     if args.e2e:
-        e2e = e2e_phase(args, p, grid, idx, rank, world, local_rank)
+        e2e = e2e_phase(args, p, grid, idx, rank, world, local_rank, sig_digest)
 
     phase = None
     if args.phase_steps > 0 and world == 1:

@@ -67,15 +67,17 @@ typedef struct sse_slab {
 
 /* Per-call timing (CUDA events on the library's stream, milliseconds). */
 typedef struct sse_timing {
-  double h2d_ms;
+  double h2d_ms;    /* host calls with pageable inputs: host time packing the staging ring */
   double prep_ms;   /* M-operator build (and layout transforms) */
   double sigma_ms;  /* fused Sigma kernel */
-  double d2h_ms;
+  double d2h_ms;    /* host calls with pageable outputs: host time unpacking the staging ring */
   double total_ms;
   double flops;     /* algorithmic flops of the call (8 per complex MAC) */
   int64_t h2d_bytes, d2h_bytes;
   int32_t kernel_launches;
   int32_t n_devices;
+  int32_t staged;       /* host calls: bit 0 inputs, bit 1 outputs went through the pinned staging ring */
+  int32_t host_threads; /* host worker threads of the staging ring */
 } sse_timing;
 
 /* Context: owns a CUDA stream and cached device buffers per device.
@@ -89,7 +91,11 @@ int sse_version(void);
 
 /* Host-memory drop-in for sse_sigma (sse.py:305-329).  All pointers are host
  * pointers to C-contiguous caller-owned buffers (pinned or pageable); the
- * call copies in, computes on the GPU(s) and copies Sigma back.
+ * call copies in, computes on the GPU(s) and copies Sigma back, pipelined over
+ * atom chunks.  Pinned buffers are DMA'd directly; pageable ones (numpy
+ * arrays, the reference's convention) go through a library-owned pinned
+ * double-buffered staging ring that a host worker pool (SSE_HOST_THREADS,
+ * default all hardware threads) packs / unpacks while the GPU computes.
  * off/wt: frequency_map offsets and weights.  t may be NULL. */
 int sse_sigma_c128(sse_ctx* ctx, const sse_dims* d, int variant,
                    const double* G_l, const double* G_g,

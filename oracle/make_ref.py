@@ -7,9 +7,9 @@ package
 
     python oracle/make_ref.py        # also run by __graft_entry__.build()
 
--> oracle/_ref/negflow/<module>.pyc (imported by CPython's sourceless loader;
-the image's Python 3.12 on both sides) plus oracle/_ref/SOURCE.json (sha256 of
-every source file compiled).  No reference source is copied into the repo.
+-> oracle/_ref/negflow.zip holding negflow/<module>.pyc (imported by CPython's
+zipimport, which loads sourceless bytecode; the image's Python 3.12 on both
+sides) plus oracle/_ref/SOURCE.json (sha256 of every source file compiled).  No reference source is copied into the repo.
 oracle/_ref/ is git-ignored but travels to the GPU box with the gpurun
 snapshot, where /root/reference does not exist: there it is the reference
 arm of bench.py (``--impl reference``), the cpu_baseline leg and the checker
@@ -25,10 +25,12 @@ import os
 import py_compile
 import shutil
 import sys
+import tempfile
+import zipfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = "/root/reference/pkg/src/negflow"
-DST = os.path.join(HERE, "_ref", "negflow")
+DST = os.path.join(HERE, "_ref", "negflow.zip")
 MANIFEST = os.path.join(HERE, "_ref", "SOURCE.json")
 
 
@@ -41,13 +43,16 @@ def stage(src: str = SRC) -> str | None:
     """Compile the reference package into oracle/_ref; None when the reference is absent."""
     if not os.path.isdir(src):
         return None
-    if os.path.isdir(DST):
-        shutil.rmtree(DST)
-    os.makedirs(DST)
+    os.makedirs(os.path.dirname(DST), exist_ok=True)
     files = sorted(f for f in os.listdir(src) if f.endswith(".py"))
-    for f in files:
-        py_compile.compile(os.path.join(src, f), cfile=os.path.join(DST, f[:-3] + ".pyc"), doraise=True,
-                           invalidation_mode=py_compile.PycInvalidationMode.UNCHECKED_HASH)
+    tmp = DST + ".tmp"
+    with tempfile.TemporaryDirectory() as work, zipfile.ZipFile(tmp, "w", zipfile.ZIP_DEFLATED) as zf:
+        for f in files:
+            pyc = os.path.join(work, f[:-3] + ".pyc")
+            py_compile.compile(os.path.join(src, f), cfile=pyc, doraise=True,
+                               invalidation_mode=py_compile.PycInvalidationMode.UNCHECKED_HASH)
+            zf.write(pyc, arcname=f"negflow/{f[:-3]}.pyc")
+    os.replace(tmp, DST)
     manifest = {"source": src, "python": sys.version.split()[0],
                 "files": {f: sha256(os.path.join(src, f)) for f in files}}
     with open(MANIFEST, "w") as fh:

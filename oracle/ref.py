@@ -1,6 +1,6 @@
 """Import the unmodified reference package ``negflow`` (test infrastructure only).
 
-Looks in oracle/_ref/ (staged by oracle/make_ref.py; present on the GPU box)
+Looks in oracle/_ref/negflow.zip (bytecode staged by oracle/make_ref.py; present on the GPU box)
 and then in /root/reference/pkg/src (the build container).  Only tests/,
 __graft_entry__.smoke() and bench.py's reference arm / cpu_baseline leg may
 call this; the product path never does.
@@ -13,13 +13,15 @@ import os
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CANDIDATES = (os.path.join(HERE, "_ref"), "/root/reference/pkg/src")
+CANDIDATES = (os.path.join(HERE, "_ref", "negflow.zip"), "/root/reference/pkg/src")
 
 
 def ref_path() -> str | None:
+    """sys.path entry holding the reference: the staged bytecode archive, else the source tree."""
     for path in CANDIDATES:
-        pkg = os.path.join(path, "negflow")
-        if os.path.isfile(os.path.join(pkg, "sse.py")) or os.path.isfile(os.path.join(pkg, "sse.pyc")):
+        if path.endswith(".zip") and os.path.isfile(path):
+            return path
+        if os.path.isfile(os.path.join(path, "negflow", "sse.py")):
             return path
     return None
 

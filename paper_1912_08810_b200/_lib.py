@@ -74,6 +74,8 @@ class SseTiming(ctypes.Structure):
         ("d2h_bytes", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int32),
         ("n_devices", ctypes.c_int32),
+        ("staged", ctypes.c_int32),
+        ("host_threads", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -13,12 +13,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -84,6 +88,89 @@ struct DevBuf {
   }
 };
 
+// Host worker pool for the pageable-memory staging of the host calls: fork-join
+// parallel_for over [0, n) (the calling thread works too).  One job at a time.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  int threads() const { return (int)workers_.size() + 1; }
+  void parallel_for(int64_t n, const std::function<void(int64_t)>& f) {
+    if (n <= 0) return;
+    std::lock_guard<std::mutex> job_lock(job_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &f;
+      n_ = n;
+      next_.store(0);
+      active_ = (int)workers_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain_items();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  HostPool() {
+    int n = (int)std::thread::hardware_concurrency();
+    if (const char* env = getenv("SSE_HOST_THREADS")) n = atoi(env);
+    n = std::max(1, std::min(n, 64));
+    for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  void drain_items() {
+    for (int64_t i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*fn_)(i);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      drain_items();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, job_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t)>* fn_ = nullptr;
+  int64_t n_ = 0;
+  std::atomic<int64_t> next_{0};
+  int active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// Grow-only pinned host buffer (staging ring slot).
+struct PinnedBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need);
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
 struct ProfRec {
   int kind;
   cudaEvent_t a, b;
@@ -96,6 +183,8 @@ struct DevState {
   cudaEvent_t ev[6] = {};
   DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev;
   DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2], draw[2];
+  PinnedBuf stage_in[2], stage_out[2];  // host staging ring of the pageable-memory host calls
+  cudaEvent_t stage_ev[2] = {};         // H2D from stage_in[b] done
   std::vector<unsigned char> pi_mask_host;
   // host copies of the small tables last uploaded (skip re-uploads: a pageable
   // upload would otherwise serialise the host with the stream on every call)
@@ -162,6 +251,19 @@ int upload_cached(DevBuf& buf, std::vector<T>& host_copy, const std::vector<T>& 
   return SSE_OK;
 }
 
+int PinnedBuf::ensure(size_t need) {
+  if (need <= bytes) return SSE_OK;
+  release();
+  cudaError_t e = cudaHostAlloc(&ptr, need, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    cudaGetLastError();
+    return fail(SSE_ENOMEM, "cannot allocate %.2f GB of pinned staging memory", need / 1e9);
+  }
+  bytes = need;
+  return SSE_OK;
+}
+
 int init_dev(DevState& d, int device) {
   d.device = device;
   CU(cudaSetDevice(device));
@@ -175,6 +277,7 @@ int init_dev(DevState& d, int device) {
   CU(cudaStreamCreateWithFlags(&d.s_d2h, cudaStreamNonBlocking));
   for (auto& e : d.ev) CU(cudaEventCreate(&e));
   CU(cudaEventCreateWithFlags(&d.scratch_done, cudaEventDisableTiming));
+  for (auto& e : d.stage_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return SSE_OK;
 }
 
@@ -211,6 +314,9 @@ void destroy_dev(DevState& d) {
   for (auto& e : d.pool) cudaEventDestroy(e);
   for (auto& e : d.pipe) cudaEventDestroy(e);
   if (d.scratch_done) cudaEventDestroy(d.scratch_done);
+  for (auto& e : d.stage_ev)
+    if (e) cudaEventDestroy(e);
+  for (PinnedBuf* b : {&d.stage_in[0], &d.stage_in[1], &d.stage_out[0], &d.stage_out[1]}) b->release();
   for (cudaStream_t s : {d.stream, d.s_h2d, d.s_d2h})
     if (s) cudaStreamDestroy(s);
 }
@@ -690,31 +796,122 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
       while (bounds.back() + chunk < on) bounds.push_back(bounds.back() + chunk);
     }
     bounds.push_back(on);
-    const DevPtrs ptr{ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dc[0].as<double2>(),
-                      ds.dc[1].as<double2>(), ds.dh.as<double2>(), ds.s[0].as<double2>(),
-                      ds.s[1].as<double2>()};
+    // per chunk: owned atoms [a0, a0 + n) and the G columns [c0, c1) first needed by it
+    struct Piece {
+      int64_t a0, n, c0, c1;
+    };
+    std::vector<Piece> plan;
     int64_t copied = glo;  // G columns [glo, copied) are on their way
-    size_t ei = 0;
     for (size_t ci = 0; ci + 1 < bounds.size(); ++ci) {
       const int64_t a0 = bounds[ci], n = bounds[ci + 1] - bounds[ci];
       if (n <= 0) continue;
       int64_t need = copied;
       for (int64_t i = a0 * d->nb; i < (a0 + n) * d->nb; ++i) need = std::max(need, rows_nmap[i] + 1);
       need = std::max(need, lo + a0 + n);
-      if (need > copied) {
-        for (int p = 0; p < 2; ++p)
-          CU(cudaMemcpy2DAsync((char*)ds.g[p].ptr + (copied - glo) * blk, gn * blk,
-                               Gh[p] + (copied - c.hg.atom0) * blk, hg_pitch, (need - copied) * blk,
-                               rows, cudaMemcpyHostToDevice, ds.s_h2d));
-        copied = need;
+      plan.push_back({a0, n, copied, std::max(copied, need)});
+      copied = std::max(copied, need);
+    }
+    // Pageable caller memory cannot be DMA'd asynchronously (a pageable D2H blocks the host until
+    // the chunk's kernels finish, serialising the pipeline), so it is staged through a pinned
+    // double-buffered ring: the host worker pool packs chunk i+1's G columns / Dc / dH rows and
+    // unpacks chunk i-1's Sigma columns while the GPU computes chunk i.  Pinned callers (and
+    // SSE_HOST_STAGING=0) take the direct DMA path.
+    auto pinned = [](const void* ptr) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
       }
-      if (!c.dc_resident)
-        for (int p = 0; p < 2; ++p)
-          CU(cudaMemcpy2DAsync((char*)ds.dc[p].ptr + a0 * dc_row, on * dc_row,
-                               Dh[p] + (lo + a0 - c.hs.atom0) * dc_row, hdc_pitch, n * dc_row, dc_rows,
-                               cudaMemcpyHostToDevice, ds.s_h2d));
-      CU(cudaMemcpyAsync((char*)ds.dh.ptr + a0 * dh_atom, dHh + a0 * dh_atom, n * dh_atom,
-                         cudaMemcpyHostToDevice, ds.s_h2d));
+      return a.type == cudaMemoryTypeHost;
+    };
+    const char* stage_env = getenv("SSE_HOST_STAGING");
+    const int stage_mode = stage_env ? atoi(stage_env) : -1;  // -1 auto, 0 never, 1 always
+    const bool in_pinned = pinned(c.G_l) && pinned(c.G_g) && pinned(c.dH) &&
+                           (c.dc_resident || (pinned(c.Dc_l) && pinned(c.Dc_g)));
+    const bool out_pinned = pinned(c.S_l) && pinned(c.S_g);
+    const bool stage_in = stage_mode == 1 || (stage_mode == -1 && !in_pinned);
+    const bool stage_out = stage_mode == 1 || (stage_mode == -1 && !out_pinned);
+    size_t in_cap = 0, out_cap = 0;
+    for (const Piece& pc : plan) {
+      in_cap = std::max(in_cap, 2 * rows * (pc.c1 - pc.c0) * blk + (c.dc_resident ? 0 : 2 * dc_rows * pc.n * dc_row) +
+                                    pc.n * dh_atom);
+      out_cap = std::max(out_cap, 2 * rows * pc.n * blk);
+    }
+    if (stage_in)
+      for (int b = 0; b < 2; ++b) CHECK(ds.stage_in[b].ensure(in_cap));
+    if (stage_out)
+      for (int b = 0; b < 2; ++b) CHECK(ds.stage_out[b].ensure(out_cap));
+    HostPool& pool = HostPool::get();
+    double pack_ms = 0, unpack_ms = 0;
+    auto now_ms = [] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    // strided row copies (rows x width bytes) split over the pool, ~1 MB per work item
+    auto copy_rows = [&](char* dst, size_t dpitch, const char* src, size_t spitch, size_t width, size_t nrows) {
+      const size_t per = std::max<size_t>(1, (1u << 20) / std::max<size_t>(width, 1));
+      const int64_t items = (int64_t)((nrows + per - 1) / per);
+      pool.parallel_for(items, [&](int64_t it) {
+        const size_t r0 = it * per, r1 = std::min(nrows, r0 + per);
+        for (size_t r = r0; r < r1; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, width);
+      });
+    };
+    auto unpack = [&](size_t k) {  // chunk k's Sigma columns: staging -> caller rows
+      const Piece& pc = plan[k];
+      const double t0 = now_ms();
+      const char* src = (const char*)ds.stage_out[k % 2].ptr;
+      for (int p = 0; p < 2; ++p)
+        copy_rows(Sh[p] + (lo + pc.a0 - c.hs.atom0) * blk, hs_pitch, src + p * rows * pc.n * blk, pc.n * blk,
+                  pc.n * blk, rows);
+      unpack_ms += now_ms() - t0;
+    };
+    const DevPtrs ptr{ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dc[0].as<double2>(),
+                      ds.dc[1].as<double2>(), ds.dh.as<double2>(), ds.s[0].as<double2>(),
+                      ds.s[1].as<double2>()};
+    size_t ei = 0;
+    std::vector<cudaEvent_t> out_ready(plan.size(), nullptr);
+    for (size_t ci = 0; ci < plan.size(); ++ci) {
+      const Piece& pc = plan[ci];
+      const int64_t a0 = pc.a0, n = pc.n, ncols = pc.c1 - pc.c0;
+      if (stage_in) {
+        const int b = (int)(ci % 2);
+        if (ci >= 2) CU(cudaEventSynchronize(ds.stage_ev[b]));  // H2D of chunk ci-2 left stage_in[b]
+        const double t0 = now_ms();
+        char* buf = (char*)ds.stage_in[b].ptr;
+        char* g_st[2] = {buf, buf + rows * ncols * blk};
+        char* dc_st[2] = {buf + 2 * rows * ncols * blk, buf + 2 * rows * ncols * blk + dc_rows * n * dc_row};
+        char* dh_st = buf + 2 * rows * ncols * blk + (c.dc_resident ? 0 : 2 * dc_rows * n * dc_row);
+        for (int p = 0; p < 2; ++p) {
+          if (ncols > 0)
+            copy_rows(g_st[p], ncols * blk, Gh[p] + (pc.c0 - c.hg.atom0) * blk, hg_pitch, ncols * blk, rows);
+          if (!c.dc_resident)
+            copy_rows(dc_st[p], n * dc_row, Dh[p] + (lo + a0 - c.hs.atom0) * dc_row, hdc_pitch, n * dc_row, dc_rows);
+        }
+        copy_rows(dh_st, n * dh_atom, dHh + a0 * dh_atom, n * dh_atom, n * dh_atom, 1);
+        pack_ms += now_ms() - t0;
+        for (int p = 0; p < 2; ++p) {
+          if (ncols > 0)
+            CU(cudaMemcpy2DAsync((char*)ds.g[p].ptr + (pc.c0 - glo) * blk, gn * blk, g_st[p], ncols * blk, ncols * blk,
+                                 rows, cudaMemcpyHostToDevice, ds.s_h2d));
+          if (!c.dc_resident)
+            CU(cudaMemcpy2DAsync((char*)ds.dc[p].ptr + a0 * dc_row, on * dc_row, dc_st[p], n * dc_row, n * dc_row,
+                                 dc_rows, cudaMemcpyHostToDevice, ds.s_h2d));
+        }
+        CU(cudaMemcpyAsync((char*)ds.dh.ptr + a0 * dh_atom, dh_st, n * dh_atom, cudaMemcpyHostToDevice, ds.s_h2d));
+        CU(cudaEventRecord(ds.stage_ev[b], ds.s_h2d));
+      } else {
+        if (ncols > 0)
+          for (int p = 0; p < 2; ++p)
+            CU(cudaMemcpy2DAsync((char*)ds.g[p].ptr + (pc.c0 - glo) * blk, gn * blk,
+                                 Gh[p] + (pc.c0 - c.hg.atom0) * blk, hg_pitch, ncols * blk, rows,
+                                 cudaMemcpyHostToDevice, ds.s_h2d));
+        if (!c.dc_resident)
+          for (int p = 0; p < 2; ++p)
+            CU(cudaMemcpy2DAsync((char*)ds.dc[p].ptr + a0 * dc_row, on * dc_row,
+                                 Dh[p] + (lo + a0 - c.hs.atom0) * dc_row, hdc_pitch, n * dc_row, dc_rows,
+                                 cudaMemcpyHostToDevice, ds.s_h2d));
+        CU(cudaMemcpyAsync((char*)ds.dh.ptr + a0 * dh_atom, dHh + a0 * dh_atom, n * dh_atom,
+                           cudaMemcpyHostToDevice, ds.s_h2d));
+      }
       cudaEvent_t in = pipe_event(ds, ei++), done = pipe_event(ds, ei++);
       if (!in || !done) return fail(SSE_ECUDA, "event creation failed");
       CU(cudaEventRecord(in, ds.s_h2d));
@@ -722,10 +919,34 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
       CHECK(run_chunk(ds, d, gslab, oslab, ptr, c.off, a0, n, st, 2, &launches));
       CU(cudaEventRecord(done, st));
       CU(cudaStreamWaitEvent(ds.s_d2h, done, 0));
-      for (int p = 0; p < 2; ++p)
-        CU(cudaMemcpy2DAsync(Sh[p] + (lo + a0 - c.hs.atom0) * blk, hs_pitch,
-                             (char*)ds.s[p].ptr + a0 * blk, on * blk, n * blk, rows,
-                             cudaMemcpyDeviceToHost, ds.s_d2h));
+      if (stage_out) {
+        char* dst = (char*)ds.stage_out[ci % 2].ptr;  // its previous chunk (ci-2) was unpacked at ci-1
+        for (int p = 0; p < 2; ++p)
+          CU(cudaMemcpy2DAsync(dst + p * rows * n * blk, n * blk, (char*)ds.s[p].ptr + a0 * blk, on * blk, n * blk,
+                               rows, cudaMemcpyDeviceToHost, ds.s_d2h));
+        out_ready[ci] = pipe_event(ds, ei++);
+        if (!out_ready[ci]) return fail(SSE_ECUDA, "event creation failed");
+        CU(cudaEventRecord(out_ready[ci], ds.s_d2h));
+        if (ci >= 1) {  // the previous chunk's Sigma, while this chunk computes
+          CU(cudaEventSynchronize(out_ready[ci - 1]));
+          unpack(ci - 1);
+        }
+      } else {
+        for (int p = 0; p < 2; ++p)
+          CU(cudaMemcpy2DAsync(Sh[p] + (lo + a0 - c.hs.atom0) * blk, hs_pitch,
+                               (char*)ds.s[p].ptr + a0 * blk, on * blk, n * blk, rows,
+                               cudaMemcpyDeviceToHost, ds.s_d2h));
+      }
+    }
+    if (stage_out && !plan.empty()) {
+      CU(cudaEventSynchronize(out_ready.back()));
+      unpack(plan.size() - 1);
+    }
+    if (t) {
+      t->h2d_ms += pack_ms;
+      t->d2h_ms += unpack_ms;
+      t->staged = (stage_in ? 1 : 0) | (stage_out ? 2 : 0);
+      t->host_threads = pool.threads();
     }
     CU(cudaEventRecord(ds.ev[3], ds.s_d2h));
     CU(cudaStreamWaitEvent(st, ds.ev[3], 0));
@@ -823,6 +1044,10 @@ int host_call(sse_ctx* ctx, const HostCall& c, sse_timing* t) {
       t->h2d_bytes += ts[i].h2d_bytes;
       t->d2h_bytes += ts[i].d2h_bytes;
       t->kernel_launches += ts[i].kernel_launches;
+      t->h2d_ms = std::max(t->h2d_ms, ts[i].h2d_ms);
+      t->d2h_ms = std::max(t->d2h_ms, ts[i].d2h_ms);
+      t->staged |= ts[i].staged;
+      t->host_threads = std::max(t->host_threads, ts[i].host_threads);
     }
   }
   return SSE_OK;
@@ -1307,6 +1532,10 @@ int sse_pi_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const double
       t->h2d_bytes += ts[i].h2d_bytes;
       t->d2h_bytes += ts[i].d2h_bytes;
       t->kernel_launches += ts[i].kernel_launches;
+      t->h2d_ms = std::max(t->h2d_ms, ts[i].h2d_ms);
+      t->d2h_ms = std::max(t->d2h_ms, ts[i].d2h_ms);
+      t->staged |= ts[i].staged;
+      t->host_threads = std::max(t->host_threads, ts[i].host_threads);
     }
   }
   return SSE_OK;
@@ -1389,6 +1618,10 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
     CU(cudaEventSynchronize(e1));
     if (tt) {
       tt->total_ms = std::max(tt->total_ms, (double)elapsed(e0, e1));
+      tt->h2d_ms += ts.h2d_ms;
+      tt->d2h_ms += ts.d2h_ms;
+      tt->staged |= ts.staged;
+      tt->host_threads = ts.host_threads;
       tt->h2d_bytes += ts.h2d_bytes + 2 * d_rows * gn * d_row;
       tt->d2h_bytes += ts.d2h_bytes + 2 * pi_rows * on * pi_row;
       tt->kernel_launches += launches;
@@ -1421,6 +1654,10 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
       t->h2d_bytes += ts[i].h2d_bytes;
       t->d2h_bytes += ts[i].d2h_bytes;
       t->kernel_launches += ts[i].kernel_launches;
+      t->h2d_ms = std::max(t->h2d_ms, ts[i].h2d_ms);
+      t->d2h_ms = std::max(t->d2h_ms, ts[i].d2h_ms);
+      t->staged |= ts[i].staged;
+      t->host_threads = std::max(t->host_threads, ts[i].host_threads);
     }
   }
   return SSE_OK;

@@ -404,3 +404,39 @@ def test_large_config_sampled_points():
     """NA = 10,240, NE = 1,220, Nkz = Nqz = 5, 575.7 GB in total: three of its 8-way atom shards
     (72 GB each; the 8-GPU run's per-GPU share) on one B200, chain ends included."""
     assert _sharded_points("large", 8, (0, 4, 7)) <= TOL
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "auto"])
+def test_host_staging_ring_bitwise(monkeypatch, mode):
+    """The pageable-memory staging ring (SSE_HOST_STAGING auto/1: host worker pool packs and
+    unpacks pinned double buffers) and direct DMA (0) give the same bits as the device-resident
+    call, over many pipeline chunks (ramped chunk sizes, halo columns, both polarities)."""
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    p = SimParams(n_kz=3, n_qz=3, n_E=40, n_w=14, n_A=150, n_B=4, n_orb=12)
+    g_l, g_g, d_l, d_g, dh = inputs.stream_instance(21, p, dh_scale=0.05)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    dc = CombinedD(*orc.preprocess_D(d_l, d_g, nmap.idx))
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    ref = [torch.zeros(p.electron_shape, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    dev.sigma_device(cu(g_l), cu(g_g), cu(dc.lesser), cu(dc.greater), cu(dh), nmap.idx, grid.offsets,
+                     grid.weights, ref[0], ref[1], n_a=p.n_A)
+    torch.cuda.synchronize()
+    ref = [r.cpu().numpy() for r in ref]
+    monkeypatch.setenv("SSE_OP_CHUNK_ATOMS", "16")
+    if mode != "auto":
+        monkeypatch.setenv("SSE_HOST_STAGING", mode)
+    timing = {}
+    out = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(g_l, g_g), dc, dh, nmap, grid, timing=timing)
+    assert np.array_equal(out.lesser, ref[0]) and np.array_equal(out.greater, ref[1])
+    assert timing["staged"] == (0 if mode == "0" else 3)
+    # pinned caller buffers take the direct path in auto mode
+    if mode == "auto":
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        o = [torch.empty(p.electron_shape, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
+        tim = dev.sigma_host_slab(pin(g_l), pin(g_g), pin(dc.lesser), pin(dc.greater), pin(dh), nmap.idx,
+                                  grid.offsets, grid.weights, o[0], o[1], n_a=p.n_A, g_atom0=0, out_atom0=0)
+        assert tim["staged"] == 0
+        assert np.array_equal(o[0].numpy(), ref[0]) and np.array_equal(o[1].numpy(), ref[1])

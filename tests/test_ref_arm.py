@@ -69,5 +69,8 @@ def test_staged_reference_matches_source():
     assert sorted(manifest["files"]) == srcs
     for f in srcs:
         assert manifest["files"][f] == make_ref.sha256(os.path.join(make_ref.SRC, f)), f
-        assert os.path.isfile(os.path.join(make_ref.DST, f[:-3] + ".pyc"))
-    assert not any(f.endswith(".py") for f in os.listdir(make_ref.DST)), "no reference source in the repo"
+    import zipfile
+
+    names = zipfile.ZipFile(make_ref.DST).namelist()
+    assert sorted(names) == sorted(f"negflow/{f[:-3]}.pyc" for f in srcs)
+    assert not any(n.endswith(".py") for n in names), "no reference source in the repo"
