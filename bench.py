@@ -486,6 +486,33 @@ def pi_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, s
     return pi_info
 
 
+def device_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream):
+    """the whole SSE phase (preprocess_D + Sigma + Pi) as ONE device call on the
+    resident slabs (sse_phase_device; no host copies), CUDA events, max over ranks."""
+    import torch
+
+    from paper_1912_08810_b200.sse import Profile
+
+    if args.phase_device_steps <= 0:
+        return None
+    prob.phase()
+    torch.cuda.synchronize()
+    barrier(world)
+    with Profile(device=local_rank) as prof:
+        start.record(stream)
+        for _ in range(args.phase_device_steps):
+            prob.phase()
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = allreduce_max(start.elapsed_time(end) / args.phase_device_steps, world)
+    return {"s_per_phase": ms / 1e3, "steps": args.phase_device_steps,
+            "kernel_ms_per_phase": {k: v["ms"] / args.phase_device_steps for k, v in prof.result.items()
+                                    if v["launches"]},
+            "path": "sse_phase_device (C ABI): preprocess_D -> K2/K3 Sigma -> K5-K7 Pi on the resident G / raw D "
+                    "slabs, outputs left in HBM (the loop's device-resident SSE phase, "
+                    "loop.self_consistent_loop_device)"}
+
+
 def gf_layout_phase(args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream):
     """the step as it follows a distributed GF phase: G from the (k, E)-point layout and raw D
     from the (q, w) points by NCCL all-to-all into the atom slabs (halos included), Sigma back to the point
@@ -787,6 +814,7 @@ def run_gpu(args, p, grid, idx) -> None:
 
     common = (args, p, grid, idx, prob, world, local_rank, step_ms, start, end, stream)
     pi_info = pi_phase(*common)
+    phase_dev = device_phase(*common)
     gf_info = gf_layout_phase(*common)
     fused_info = gf_fused_phase(*common)
 
@@ -841,7 +869,9 @@ def run_gpu(args, p, grid, idx) -> None:
             line["pi"] = pi_info
             # the whole SSE phase of a Born iteration (sse.py:532-534): Sigma (`value`, SURVEY 8d's
             # unit of work) + Pi, both device-resident
-            line["sse_phase_device_s"] = step_ms / 1e3 + pi_info["s_per_eval"]
+            line["sigma_plus_pi_device_s"] = step_ms / 1e3 + pi_info["s_per_eval"]
+        if phase_dev is not None:
+            line["sse_phase_device"] = phase_dev
         if gf_info is not None:
             line["gf_layout"] = gf_info
         if fused_info is not None:
@@ -873,6 +903,8 @@ def main():
                     help="cpu_baseline: time the reference on the NB pairs of one atom and compare (0 = skip)")
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--pi-steps", type=int, default=1, help="timed Pi evaluations after Sigma (0 = skip)")
+    ap.add_argument("--phase-device-steps", type=int, default=1,
+                    help="timed SSE phases (preprocess_D + Sigma + Pi) as one device call (0 = skip)")
     ap.add_argument("--phase-steps", type=int, default=0,
                     help="N=1: timed SSE phases (preprocess_D + Sigma + Pi) through sse_phase from pinned host memory")
     ap.add_argument("--gf-fused-steps", type=int, default=0,

@@ -233,6 +233,20 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
                    double energy_weight, double* Sig_l, double* Sig_g, double* Pi_l,
                    double* Pi_g, sse_timing* t);
 
+/* The same SSE phase on device-resident tensors of one rank (no host copies; the
+ * device-side plug for a GPU GF phase): g = slab of G<> and of the
+ * RAW phonon tensors D<> [Nqz, Nw, g.natoms, NB+1, 3, 3] over the owned atoms and
+ * all their neighbours (layout of G by g.atom_major); out = the owned atoms:
+ * dH [out.natoms, NB, 3, No, No], Sigma (out.atom_major layout) and Pi
+ * [Nqz, Nw, out.natoms, NB+1, 3, 3].  nmap: HOST int64 [NA, NB], the full map
+ * (preprocess_D needs the neighbours' reverse slots).  preprocess_D -> K2/K3 ->
+ * K5-K7 on `stream` (NULL = the library's); asynchronous unless t != NULL. */
+int sse_phase_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out,
+                     const double* G_l, const double* G_g, const double* D_l, const double* D_g,
+                     const double* dH, const int64_t* nmap, const int64_t* off, const double* wt,
+                     double energy_weight, double* Sig_l, double* Sig_g, double* Pi_l, double* Pi_g,
+                     void* stream, sse_timing* t);
+
 /* Layout transform K1 (to_atom_major / to_grid_major, sse.py:48-55):
  * [Nkz, NE, NA, blk] <-> [NA, Nkz, NE, blk], blk = block_doubles doubles.
  * to_atom_major = 1: grid -> atom major; 0: atom -> grid major.  Device ptrs. */

@@ -38,6 +38,7 @@ EXPORTED = (
     "sse_pi_c128",
     "sse_pi_device",
     "sse_phase_c128",
+    "sse_phase_device",
     "sse_layout_transform",
     "sse_preprocess_D",
     "sse_fill_synthetic",
@@ -129,6 +130,7 @@ def load() -> ctypes.CDLL:
         lib.sse_pi_c128.argtypes = [_P, pdims, _P, _P, _P, _P, _P, dbl, _P, i64, i64, _P, _P, ptim]
         lib.sse_pi_device.argtypes = [_P, pdims, pslab, pslab, _P, _P, _P, _P, _P, dbl, _P, _P, _P, _P, ptim]
         lib.sse_phase_c128.argtypes = [_P, pdims] + [_P] * 8 + [dbl] + [_P] * 4 + [ptim]
+        lib.sse_phase_device.argtypes = [_P, pdims, pslab, pslab] + [_P] * 8 + [dbl] + [_P] * 5 + [ptim]
         lib.sse_profile_begin.argtypes = [_P]
         lib.sse_profile_end.argtypes = [_P, ctypes.POINTER(SseProfile)]
         lib.sse_sigma_device.argtypes = [_P, pdims, pslab, pslab] + [_P] * 6 + [_P, _P, _P, _P, _P, ptim]

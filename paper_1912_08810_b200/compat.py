@@ -10,7 +10,8 @@ time:
 * ``negflow.cli.sse_sigma``      cmd_distsim (cli.py:24-31,222)
 * ``negflow.sse_sigma``          the package re-export (__init__.py:16-26)
 
-``patch_reference()`` rebinds all four to a wrapper around
+``patch_reference()`` rebinds all four (and, with ``pi=True``, ``sse_pi`` and the
+``sse_pi_chains`` that distsim's schemes call) to a wrapper around
 :func:`paper_1912_08810_b200.sse.sse_sigma` that returns the reference's own
 ``SelfEnergyTensor`` type; ``unpatch_reference()`` restores the originals.
 The reference stays read-only.
@@ -27,12 +28,16 @@ from __future__ import annotations
 import importlib
 
 from .sse import sse_pi as _b200_sse_pi
+from .sse import sse_pi_chains as _b200_sse_pi_chains
 from .sse import sse_sigma as _b200_sse_sigma
 
 _TARGETS = ("negflow.sse", "negflow.distsim", "negflow.cli", "negflow")
 # sse_pi is bound by name in negflow.sse (self_consistent_loop sse.py:534,
 # count_sse_phase sse.py:450), negflow.cli (cli.py:223) and the package root.
 _PI_TARGETS = ("negflow.sse", "negflow.cli", "negflow")
+# sse_pi_chains: called by sse_pi (sse.py:417) and bound by name in negflow.distsim (distsim.py:24;
+# run_omen_scheme distsim.py:227, run_tiled_scheme distsim.py:344)
+_PI_CHAINS_TARGETS = ("negflow.sse", "negflow.distsim")
 # self_consistent_loop: sse.py:495, re-exported at __init__.py:22, bound in cli.py:28
 _LOOP_TARGETS = ("negflow.sse", "negflow.cli", "negflow")
 _saved: dict[tuple[str, str], object] = {}
@@ -59,6 +64,18 @@ def make_pi_drop_in(self_energy_cls, **kwargs):
 
     sse_pi.__doc__ = "B200 drop-in for negflow.sse.sse_pi (sse.py:409-428)."
     return sse_pi
+
+
+def make_pi_chains_drop_in(**kwargs):
+    """sse_pi_chains with the reference signature (a (lesser, greater) pair of chain arrays)."""
+
+    def sse_pi_chains(g, dh, nmap, grid, n_qz, counter=None, hoist_invariant=True, point_mask=None,
+                      atom_range=None):
+        return _b200_sse_pi_chains(g, dh, nmap, grid, n_qz, counter=counter, hoist_invariant=hoist_invariant,
+                                   point_mask=point_mask, atom_range=atom_range, **kwargs)
+
+    sse_pi_chains.__doc__ = "B200 drop-in for negflow.sse.sse_pi_chains (sse.py:332-390)."
+    return sse_pi_chains
 
 
 def make_loop_drop_in(**kwargs):
@@ -95,6 +112,9 @@ def patch_reference(pi: bool = True, loop: bool = True, **kwargs) -> None:
         pi_drop_in = make_pi_drop_in(gf.SelfEnergyTensor, **kwargs)
         for name in _PI_TARGETS:
             _bind(name, "sse_pi", pi_drop_in)
+        chains_drop_in = make_pi_chains_drop_in(**kwargs)
+        for name in _PI_CHAINS_TARGETS:
+            _bind(name, "sse_pi_chains", chains_drop_in)
     if loop:
         loop_drop_in = make_loop_drop_in(**kwargs)
         for name in _LOOP_TARGETS:

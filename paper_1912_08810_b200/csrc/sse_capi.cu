@@ -1663,6 +1663,61 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
   return SSE_OK;
 }
 
+// SSE phase of one Born iteration (sse.py:532-534) on device-resident tensors of one
+// rank: preprocess_D of the owned atoms from the raw D slab, Sigma and Pi from the G slab;
+// nothing crosses the host link.  g: G / raw-D slab (owned atoms + every neighbour), out: owned.
+int sse_phase_device(sse_ctx* ctx, const sse_dims* d, const sse_slab* g, const sse_slab* out, const double* G_l,
+                     const double* G_g, const double* D_l, const double* D_g, const double* dH, const int64_t* nmap,
+                     const int64_t* off, const double* wt, double energy_weight, double* Sig_l, double* Sig_g,
+                     double* Pi_l, double* Pi_g, void* stream, sse_timing* t) {
+  if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "device call needs a 1-device context");
+  CHECK(validate_dims(d));
+  CHECK(validate_grid(d, off, wt));
+  CHECK(validate_offsets(d, off, energy_weight));
+  CHECK(validate_slab(d, g, "G"));
+  CHECK(validate_slab(d, out, "output"));
+  if (!G_l || !G_g || !D_l || !D_g || !dH || !nmap || !Sig_l || !Sig_g || !Pi_l || !Pi_g)
+    return fail(SSE_EINVAL, "NULL tensor pointer");
+  DevState& ds = ctx->devs[0];
+  CU(cudaSetDevice(ds.device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : ds.stream;
+  std::vector<int> nbr, rev;
+  CHECK(preprocess_tables(nmap, d->na, d->nb, g->atom0, g->natoms, out->atom0, out->natoms, nbr, rev));
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->flops = alg_flops(d, off, out->natoms);
+    t->n_devices = 1;
+    CU(cudaEventRecord(ds.ev[0], st));
+  }
+  CHECK(scratch_enter(ds, st));
+  const size_t dc_bytes = (size_t)(d->nqz * d->nw) * out->natoms * d->nb * 9 * 16;
+  for (int p = 0; p < 2; ++p) CHECK(ds.dc[p].ensure(dc_bytes));
+  CHECK(upload_cached(ds.pp_nbr, ds.pp_nbr_host, nbr, st));
+  CHECK(upload_cached(ds.pp_rev, ds.pp_rev_host, rev, st));
+  const double* Dr[2] = {D_l, D_g};
+  for (int p = 0; p < 2; ++p)
+    CHECK(profiled(ds, st, SSE_PROF_PREPROCESS, 0.0, [&] {
+      return sse::launch_preprocess_D(d->nqz, d->nw, g->natoms, g->atom0, out->atom0, out->natoms, d->nb,
+                                      ds.pp_nbr.as<int>(), ds.pp_rev.as<int>(), (const double2*)Dr[p],
+                                      ds.dc[p].as<double2>(), st);
+    }));
+  int launches = 2;
+  const int64_t* rows = nmap + out->atom0 * d->nb;
+  const DevPtrs p{(const double2*)G_l, (const double2*)G_g, ds.dc[0].as<double2>(), ds.dc[1].as<double2>(),
+                  (const double2*)dH, (double2*)Sig_l, (double2*)Sig_g};
+  CHECK(sigma_on_device(ds, d, *g, *out, p, rows, off, wt, st, &launches));
+  CHECK(pi_on_device(ds, d, *g, *out, (const double2*)G_l, (const double2*)G_g, (const double2*)dH, rows, off,
+                     energy_weight, nullptr, (double2*)Pi_l, (double2*)Pi_g, st, &launches));
+  CHECK(scratch_leave(ds, st));
+  if (t) {
+    CU(cudaEventRecord(ds.ev[1], st));
+    CU(cudaEventSynchronize(ds.ev[1]));
+    t->total_ms = elapsed(ds.ev[0], ds.ev[1]);
+    t->kernel_launches = launches;
+  }
+  return SSE_OK;
+}
+
 int sse_layout_transform(sse_ctx* ctx, int64_t nkz, int64_t ne, int64_t na, int64_t block_doubles,
                          int to_atom_major, const double* src, double* dst, void* stream) {
   if (!ctx || ctx->devs.empty()) return fail(SSE_EINVAL, "context is NULL");

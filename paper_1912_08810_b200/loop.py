@@ -105,3 +105,75 @@ def self_consistent_loop(
         sigma = self_energy_cls(lesser=s.lesser, greater=s.greater)
         pi = self_energy_cls(lesser=p.lesser, greater=p.greater)
     return result_cls(g_e, g_ph, sigma, pi, max_iter, False, deltas, abs_deltas)
+
+
+def gf_change_device(old, new) -> tuple[float, float]:
+    """gf_change (sse.py:468-475) on device tensors: only the two scalars come back to the host."""
+    import torch
+
+    scale = torch.maximum(old.lesser.abs().max(), old.greater.abs().max()).clamp_min(1e-300)
+    diff = torch.maximum((new.lesser - old.lesser).abs().max(), (new.greater - old.greater).abs().max())
+    d, s = (float(x) for x in torch.stack([diff, scale]).cpu())
+    return d, d / s
+
+
+def self_consistent_loop_device(
+    gf_phase_device,
+    dh,
+    nmap,
+    params,
+    grid,
+    max_iter: int = 20,
+    tol: float = 1e-8,
+    initial_sigma=None,
+    initial_pi=None,
+    *,
+    self_energy_cls=None,
+    greens_cls=None,
+    result_cls=None,
+):
+    """The Born loop with G, D, Sigma and Pi resident in HBM between the phases.
+
+    Same iteration order, convergence test and result record as ``self_consistent_loop``
+    (sse.py:495-535), but the SSE phase is :func:`sse.sse_phase_device` on torch CUDA tensors and
+    nothing crosses the host link except the two convergence scalars per iteration:
+
+    ``gf_phase_device(sigma, pi, iteration) -> (g_e, g_ph)`` is the (device) GF phase: it receives
+    the self-energies as ``self_energy_cls`` pairs of CUDA tensors and returns ``greens_cls`` pairs
+    of CUDA tensors (G<> [Nkz, NE, NA, No, No], raw D<> [Nqz, Nw, NA, NB+1, 3, 3]).  ``dh`` is the
+    coupling tensor on the device.  The reference's GF phase is a CPU solver (out of scope here);
+    any GPU GF phase with this signature plugs in without host copies.
+    """
+    import torch
+
+    from .sse import sse_phase_device
+    from .types import GreensTensor, SelfEnergyTensor
+
+    self_energy_cls = self_energy_cls or SelfEnergyTensor
+    greens_cls = greens_cls or GreensTensor
+    result_cls = result_cls or LoopResult
+    dev = dh.device
+    c128 = dict(dtype=torch.complex128, device=dev)
+    sigma = initial_sigma or self_energy_cls(lesser=torch.zeros(params.electron_shape, **c128),
+                                             greater=torch.zeros(params.electron_shape, **c128))
+    pi = initial_pi or self_energy_cls(lesser=torch.zeros(params.phonon_shape, **c128),
+                                       greater=torch.zeros(params.phonon_shape, **c128))
+    idx = np.ascontiguousarray(nmap.idx, dtype=np.int64)
+    g_e = g_ph = prev = None
+    deltas: list[float] = []
+    abs_deltas: list[float] = []
+    for iteration in range(1, max_iter + 1):
+        g_e, g_ph = gf_phase_device(sigma, pi, iteration)
+        if prev is not None:
+            diff, delta = gf_change_device(prev, g_e)
+            deltas.append(delta)
+            abs_deltas.append(diff)
+            if delta <= tol:
+                return result_cls(g_e, g_ph, sigma, pi, iteration, True, deltas, abs_deltas)
+        prev = g_e
+        s = [torch.empty(params.electron_shape, **c128) for _ in range(2)]
+        p = [torch.empty(params.phonon_shape, **c128) for _ in range(2)]
+        sse_phase_device(g_e.lesser, g_e.greater, g_ph.lesser, g_ph.greater, dh, idx, grid, s[0], s[1], p[0], p[1])
+        sigma = self_energy_cls(lesser=s[0], greater=s[1])
+        pi = self_energy_cls(lesser=p[0], greater=p[1])
+    return result_cls(g_e, g_ph, sigma, pi, max_iter, False, deltas, abs_deltas)

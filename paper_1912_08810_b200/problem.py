@@ -142,6 +142,17 @@ class ShardProblem:
             atom_major=True, stream=stream,
         )
 
+    def phase(self, stream=None) -> None:
+        """The SSE phase of a Born iteration in one device call (sse_phase_device, sse.py:532-534):
+        preprocess_D + Sigma + Pi of the owned atoms from the resident G / raw D slabs."""
+        t, p = self.torch, self.p
+        if self.pi_out is None:
+            shape = (p.n_qz, p.n_w, self.n_owned, p.n_B + 1, 3, 3)
+            self.pi_out = [t.zeros(shape, dtype=t.complex128, device=self.device) for _ in range(2)]
+        dev.sse_phase_device(self.g[0], self.g[1], self.d[0], self.d[1], self.dh, self.idx, self.grid, self.sig[0],
+                             self.sig[1], self.pi_out[0], self.pi_out[1], g_atom0=self.glo, out_atom0=self.lo,
+                             atom_major=True, stream=stream)
+
     def pi_peer(self, peer_g, stream=None) -> None:
         """Pi of the owned atoms with G read from the GF point owners (dist.PeerPointBuffers)."""
         t, p = self.torch, self.p

@@ -33,6 +33,7 @@ Array = np.ndarray
 __all__ = [
     "sse_sigma",
     "sse_pi",
+    "sse_pi_chains",
     "pi_tallies",
     "pi_device",
     "sigma_tallies",
@@ -41,6 +42,8 @@ __all__ = [
     "preprocess_D_device",
     "fill_synthetic",
     "alg_flops",
+    "sse_phase",
+    "sse_phase_device",
 ]
 
 
@@ -239,6 +242,37 @@ def sse_pi(
     if timing is not None:
         timing.update(tim.as_dict())
     return _SE(lesser=out_l, greater=out_g)
+
+
+def sse_pi_chains(
+    g,
+    dh: Array,
+    nmap,
+    grid,
+    n_qz: int,
+    counter: FlopCounter | None = None,
+    hoist_invariant: bool = True,
+    point_mask: Array | None = None,
+    atom_range: tuple[int, int] | None = None,
+    *,
+    n_gpus: int | None = None,
+):
+    """Per-(q,w,a,s,i,j) phonon trace chains before the slot signs (drop-in for sse.py:332-390),
+    the entry point distsim's schemes call (distsim.py:24,227,344).
+
+    Computed by the same kernels as :func:`sse_pi` (K5-K7); K7 stores slot 1+s = i*chain as
+    (-Im, Re), so the chain is recovered exactly (no rounding) from those slots.  Returns
+    (chains_lesser, chains_greater) [Nqz, Nw, NA, NB, 3, 3]; rows outside ``atom_range`` are 0.
+    """
+    pi = sse_pi(g, dh, nmap, grid, n_qz, counter=counter, hoist_invariant=hoist_invariant,
+                point_mask=point_mask, atom_range=atom_range, n_gpus=n_gpus)
+    out = []
+    for slots in (pi.lesser, pi.greater):
+        ch = np.empty(slots.shape[:3] + (slots.shape[3] - 1, 3, 3), dtype=np.complex128)
+        ch.real = slots[:, :, :, 1:].imag
+        ch.imag = -slots[:, :, :, 1:].real
+        out.append(ch)
+    return out[0], out[1]
 
 
 def sse_phase(
@@ -648,6 +682,61 @@ def pi_device(
         _dptr(pi_l), _dptr(pi_g), _stream_ptr(stream), None,
     )
     _lib.check(rc)
+
+
+def sse_phase_device(
+    g_l, g_g, d_l, d_g, dh, nmap_idx: Array, grid, sig_l, sig_g, pi_l, pi_g, *,
+    g_atom0: int = 0, out_atom0: int = 0, atom_major: bool = False, stream=None, sync_timing: bool = False,
+) -> dict | None:
+    """The SSE phase of a Born iteration (sse.py:532-534: preprocess_D -> sse_sigma -> sse_pi)
+    on device-resident torch tensors of one GPU, no host copies (libsse ``sse_phase_device``).
+
+    g_* : G slab [Nkz, NE, gA, No, No] (or atom-major [gA, ...]) of atoms [g_atom0, g_atom0 + gA),
+          the owned atoms and all their neighbours; d_*: raw phonon tensors of the same atoms
+          [Nqz, Nw, gA, NB+1, 3, 3]; dh: [oA, NB, 3, No, No] of the owned atoms
+          [out_atom0, out_atom0 + oA); nmap_idx: the full host map [NA, NB];
+    sig_*: Sigma of the owned atoms (G's layout); pi_*: [Nqz, Nw, oA, NB+1, 3, 3].
+    A full single-GPU problem is gA = oA = NA.  Launches on ``stream`` (default: torch's current
+    stream); returns the library timing when ``sync_timing``.
+    """
+    idx = np.ascontiguousarray(nmap_idx, dtype=np.int64)
+    if idx.ndim != 2:
+        raise ValueError("neighbor map must be a 2-D integer array")
+    n_a, n_b = idx.shape
+    if atom_major:
+        g_atoms, n_kz, n_e, n_o = (int(x) for x in g_l.shape[:4])
+        o_atoms = int(sig_l.shape[0])
+    else:
+        n_kz, n_e, g_atoms, n_o = (int(x) for x in g_l.shape[:4])
+        o_atoms = int(sig_l.shape[2])
+    n_qz, n_w = int(d_l.shape[0]), int(d_l.shape[1])
+    dev = g_l.device
+    _check_dev(g_l, _electron_shape(n_kz, n_e, g_atoms, n_o, atom_major), "g_l", dev)
+    _check_dev(g_g, g_l.shape, "g_g", dev)
+    _check_dev(d_l, (n_qz, n_w, g_atoms, n_b + 1, 3, 3), "d_l", dev)
+    _check_dev(d_g, d_l.shape, "d_g", dev)
+    _check_dev(dh, (o_atoms, n_b, 3, n_o, n_o), "dh", dev)
+    _check_dev(sig_l, _electron_shape(n_kz, n_e, o_atoms, n_o, atom_major), "sig_l", dev)
+    _check_dev(sig_g, sig_l.shape, "sig_g", dev)
+    _check_dev(pi_l, (n_qz, n_w, o_atoms, n_b + 1, 3, 3), "pi_l", dev)
+    _check_dev(pi_g, pi_l.shape, "pi_g", dev)
+    fmap = grid.frequency_map
+    if len(fmap) < n_w:
+        raise ValueError(f"frequency map has {len(fmap)} entries for n_w={n_w}")
+    offs = np.array([int(fmap[w][0]) for w in range(n_w)], dtype=np.int64)
+    wts = np.array([float(fmap[w][1]) for w in range(n_w)], dtype=np.float64)
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    gs = _lib.SseSlab(g_atom0, g_atoms, int(atom_major), 0)
+    os_ = _lib.SseSlab(out_atom0, o_atoms, int(atom_major), 0)
+    tim = _lib.SseTiming()
+    rc = _lib.load().sse_phase_device(
+        _device_ctx(g_l).handle, ctypes.byref(dims), ctypes.byref(gs), ctypes.byref(os_), _dptr(g_l), _dptr(g_g),
+        _dptr(d_l), _dptr(d_g), _dptr(dh), _ptr(idx), _ptr(offs), _ptr(wts), float(grid.energy_weight),
+        _dptr(sig_l), _dptr(sig_g), _dptr(pi_l), _dptr(pi_g), _stream_ptr(stream),
+        ctypes.byref(tim) if sync_timing else None,
+    )
+    _lib.check(rc)
+    return tim.as_dict() if sync_timing else None
 
 
 def layout_transform(src, dst, to_atom_major: bool, stream=None) -> None:

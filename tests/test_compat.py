@@ -36,6 +36,8 @@ def test_patch_and_unpatch(negflow):
             assert m.sse_sigma.__doc__.startswith("B200 drop-in")
         for m in ("negflow.sse", "negflow.cli", "negflow"):
             assert sys.modules[m].sse_pi.__doc__.startswith("B200 drop-in")
+        for m in ("negflow.sse", "negflow.distsim"):
+            assert sys.modules[m].sse_pi_chains.__doc__.startswith("B200 drop-in")
         # the reference's own validation still runs first (no device work): wrong kind -> ValueError
         import numpy as np
         from negflow.gf import GreensTensor

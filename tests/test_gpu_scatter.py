@@ -1,6 +1,8 @@
 """Sigma scattered straight into the GF-layout point owners over NVLink.
 
-Two NCCL ranks (spawned processes, one GPU each): the peer-scatter epilogue
+Two ranks (spawned processes): NCCL with one GPU each, or -- so the path runs on a 1-GPU
+box too -- gloo with both processes on cuda:0 (the CUDA-IPC mappings are then same-device
+peer memory and the all-to-alls run on host copies).  The peer-scatter epilogue
 (``sse_sigma_device_scatter`` into CUDA-IPC-mapped buffers) and the fully fused
 variant that also reads G from the owners' point buffers with TMA
 (``sse_sigma_device_peer``), and Pi with G read the same way (``sse_pi_device_peer``), must equal, bitwise, Sigma computed into atom slabs
@@ -22,7 +24,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, backend="nccl"):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -33,18 +35,28 @@ def _worker(rank, world, port, q):
     from paper_1912_08810_b200.types import SimParams, build_neighbor_map
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    device = rank if backend == "nccl" else 0
+    torch.cuda.set_device(device)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", device))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         p = SimParams(n_kz=3, n_qz=2, n_E=37, n_w=13, n_A=26, n_B=4, n_orb=12)
         idx = build_neighbor_map(p.n_A, p.n_B).idx
-        prob = ShardProblem(p, rank=rank, world=world, device=rank, seed=3, grid=default_grid(p), idx=idx)
+        prob = ShardProblem(p, rank=rank, world=world, device=device, seed=3, grid=default_grid(p), idx=idx)
         prob.allocate()
         prob.fill(owned_g_only=False)
         prob.preprocess()
         prob.sigma()
-        ref = [sdist.atom_slab_to_points(prob.sig[pol], idx, p.n_kz, p.n_E) for pol in range(2)]
-        peer = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=rank)
+
+        def to_points(t):  # the all-to-all return path (gloo: on host copies)
+            if backend == "nccl":
+                return sdist.atom_slab_to_points(t, idx, p.n_kz, p.n_E)
+            return sdist.atom_slab_to_points(t.cpu().contiguous(), idx, p.n_kz, p.n_E).to(prob.device)
+
+        ref = [to_points(prob.sig[pol]) for pol in range(2)]
+        peer = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=device)
         for t in peer.tensors:
             t.fill_(float("nan"))
         torch.cuda.synchronize()
@@ -55,10 +67,10 @@ def _worker(rank, world, port, q):
         ok = all(torch.equal(peer.tensors[pol], ref[pol]) for pol in range(2))
         finite = all(bool(torch.isfinite(torch.view_as_real(t)).all()) for t in peer.tensors)
         # fully fused: G read from the point owners too (their GF-layout buffers)
-        peer_g = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=rank)
+        peer_g = sdist.PeerPointBuffers(p.n_kz, p.n_E, p.n_A, p.n_orb, device=device)
         own = slice(prob.lo - prob.glo, prob.hi - prob.glo)
         for pol in range(2):
-            peer_g.tensors[pol].copy_(sdist.atom_slab_to_points(prob.g[pol][own].contiguous(), idx, p.n_kz, p.n_E))
+            peer_g.tensors[pol].copy_(to_points(prob.g[pol][own].contiguous()))
         for t in peer.tensors:
             t.fill_(float("nan"))
         torch.cuda.synchronize()
@@ -96,18 +108,19 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_scatter_and_gather_equal_all_to_all_bitwise():
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_peer_scatter_and_gather_equal_all_to_all_bitwise(backend):
     import multiprocessing as mp
 
     import torch
 
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (the gloo case runs both ranks on one GPU)")
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, backend)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = q.get(timeout=300)

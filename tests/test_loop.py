@@ -179,3 +179,79 @@ def test_sse_phase_chunked_pipelines_bitwise(name, monkeypatch):
     for a, b in ((s1, s2), (p1, p2), (q1, q2)):
         assert np.array_equal(a.lesser, b.lesser) and np.array_equal(a.greater, b.greater)
     assert np.array_equal(p1.lesser, q1.lesser) and np.array_equal(p1.greater, q1.greater)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset", ["tiny", "small"])
+def test_device_resident_loop_replays_reference_trace(preset):
+    """self_consistent_loop_device: G / D handed over as CUDA tensors by a device GF phase (here
+    the reference's recorded gf_phase outputs, uploaded), Sigma / Pi kept in HBM between the
+    phases (sse_phase_device), every phase and the final record equal to the reference's."""
+    import torch
+
+    data, meta, p, grid, nmap = _load(preset)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    calls = []
+
+    def gf_phase_device(sigma, pi, iteration):
+        i = len(calls)
+        calls.append(i)
+        assert sigma.lesser.is_cuda and pi.greater.is_cuda
+        assert orc.parity_dev(sigma.lesser.cpu().numpy(), sigma.greater.cpu().numpy(),
+                              data[f"it{i}_sig_in_l"], data[f"it{i}_sig_in_g"]) <= TOL
+        assert orc.parity_dev(pi.lesser.cpu().numpy(), pi.greater.cpu().numpy(),
+                              data[f"it{i}_pi_in_l"], data[f"it{i}_pi_in_g"]) <= TOL
+        return (GreensTensor(cu(data[f"it{i}_ge_l"]), cu(data[f"it{i}_ge_g"])),
+                GreensTensor(cu(data[f"it{i}_gph_l"]), cu(data[f"it{i}_gph_g"])))
+
+    res = b200_loop.self_consistent_loop_device(
+        gf_phase_device, cu(data["dh"]), nmap, p, grid, max_iter=meta["iterations"], tol=0.0,
+        initial_sigma=SelfEnergyTensor(cu(data["it0_sig_in_l"]), cu(data["it0_sig_in_g"])),
+        initial_pi=SelfEnergyTensor(cu(data["it0_pi_in_l"]), cu(data["it0_pi_in_g"])))
+    assert len(calls) == meta["recorded"]
+    assert (res.iterations, res.converged) == (meta["iterations"], meta["converged"])
+    np.testing.assert_allclose(res.deltas, meta["deltas"], rtol=1e-12)
+    np.testing.assert_allclose(res.abs_deltas, meta["abs_deltas"], rtol=1e-12)
+    assert orc.parity_dev(res.sigma.lesser.cpu().numpy(), res.sigma.greater.cpu().numpy(),
+                          data["final_sigma_l"], data["final_sigma_g"]) <= TOL
+    assert orc.parity_dev(res.pi.lesser.cpu().numpy(), res.pi.greater.cpu().numpy(),
+                          data["final_pi_l"], data["final_pi_g"]) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cli_small_s2", "orb12_s5", "slide_orb12_s9"])
+def test_sse_phase_device_equals_host_phase_bitwise(name):
+    """sse_phase_device on CUDA tensors == sse_phase (host arrays) bit for bit, full problem and an
+    owned-atom shard with its halo slab (atom-major)."""
+    import torch
+
+    from paper_1912_08810_b200.sse import sse_phase, sse_phase_device
+    from tests.golden_cases import load_case
+
+    c = load_case(name)
+    p, grid = c.p, EnergyGrid(values=tuple(np.linspace(-1, 1, c.p.n_E)),
+                              frequency_map=tuple(zip(c.offsets.tolist(), c.weights.tolist())), energy_weight=0.3)
+    nmap = NeighborMap(c.idx)
+    s_ref, p_ref = sse_phase(GreensTensor(c.g_l, c.g_g), GreensTensor(c.d_l, c.d_g), c.dh, nmap, grid, p.n_qz)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    sig = [torch.empty(p.electron_shape, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    pis = [torch.empty(p.phonon_shape, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    sse_phase_device(cu(c.g_l), cu(c.g_g), cu(c.d_l), cu(c.d_g), cu(c.dh), c.idx, grid, *sig, *pis)
+    torch.cuda.synchronize()
+    assert np.array_equal(sig[0].cpu().numpy(), s_ref.lesser) and np.array_equal(sig[1].cpu().numpy(), s_ref.greater)
+    assert np.array_equal(pis[0].cpu().numpy(), p_ref.lesser) and np.array_equal(pis[1].cpu().numpy(), p_ref.greater)
+    # shard [lo, hi) with the halo slab, atom-major
+    lo, hi = 1, p.n_A - 1
+    glo, ghi = int(min(lo, c.idx[lo:hi].min())), int(max(hi, c.idx[lo:hi].max() + 1))
+    am = lambda a: cu(np.moveaxis(a[:, :, glo:ghi], 2, 0))  # noqa: E731
+    sig = [torch.empty((hi - lo, p.n_kz, p.n_E, p.n_orb, p.n_orb), dtype=torch.complex128, device="cuda")
+           for _ in range(2)]
+    pis = [torch.empty((p.n_qz, p.n_w, hi - lo, p.n_B + 1, 3, 3), dtype=torch.complex128, device="cuda")
+           for _ in range(2)]
+    sse_phase_device(am(c.g_l), am(c.g_g), cu(c.d_l[:, :, glo:ghi]), cu(c.d_g[:, :, glo:ghi]), cu(c.dh[lo:hi]),
+                     c.idx, grid, *sig, *pis, g_atom0=glo, out_atom0=lo, atom_major=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(np.moveaxis(sig[0].cpu().numpy(), 0, 2), s_ref.lesser[:, :, lo:hi])
+    assert np.array_equal(np.moveaxis(sig[1].cpu().numpy(), 0, 2), s_ref.greater[:, :, lo:hi])
+    assert np.array_equal(pis[0].cpu().numpy(), p_ref.lesser[:, :, lo:hi])
+    assert np.array_equal(pis[1].cpu().numpy(), p_ref.greater[:, :, lo:hi])
