@@ -205,6 +205,8 @@ _contexts: dict = {}
 
 def context(n_gpus: int = 1, device: int | None = None) -> Context:
     """Process-wide cached context (device buffers are reused across calls)."""
+    if device is None and n_gpus == 1:
+        device = 0  # one context (and one set of cached device buffers) per device
     key = ("dev", device) if device is not None else ("n", n_gpus)
     with _lock:
         ctx = _contexts.get(key)
