@@ -194,8 +194,9 @@ __global__ void build_operator_kernel(OperatorArgs p) {
           const int f = 2 * j + h;
           const int kk = f / fg.nt, nt = f % fg.nt;
           const int kr = 4 * kk + (lane & 3), nc = 8 * nt + (lane >> 2);
-          const bool im_row = kr >= fg.nop;
-          const int pr = im_row ? kr - fg.nop : kr;
+          // split K: rows [0, nop) real, [nop, 2 nop) imaginary; il: row 2p real, 2p + 1 imaginary
+          const bool im_row = fg.il ? (kr & 1) : kr >= fg.nop;
+          const int pr = fg.il ? kr >> 1 : (im_row ? kr - fg.nop : kr);
           const int n = nc >> 1, part = nc & 1;
           double val = 0.0;
           if (pr < no && n < no) {
@@ -274,6 +275,40 @@ __device__ __forceinline__ int vt_swz(int kap, int no, int swz) {
   return x;
 }
 
+// A operands of one 8-row tile for a stage: `row` = start of the lane's G row (complex), pcol =
+// lane & 3.  Split K: av[kk] = G[row][pcol + 4 kk] (Re -> k-step kk, Im -> k-step kk + kh);
+// il: av[j] = (double pcol + 8j, double pcol + 8j + 4) of the row's (re, im) sequence = the A
+// values of k-steps 2j and 2j + 1.  Rows that contribute nothing pass ok = false (zeros).
+template <int NO>
+__device__ __forceinline__ void load_a(double2 (&av)[frag_geom(NO).kh], const double2* row, int pcol, bool ok) {
+  constexpr FragGeom FG = frag_geom(NO);
+  if constexpr (FG.il) {
+    const double* rd = reinterpret_cast<const double*>(row) + pcol;
+#pragma unroll
+    for (int j = 0; j < FG.kh; ++j) {
+      av[j].x = ok ? rd[8 * j] : 0.0;
+      av[j].y = (ok && 2 * j + 1 < FG.ksteps) ? rd[8 * j + 4] : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int kk = 0; kk < FG.kh; ++kk) {
+      if (NO % 4 == 0) {
+        av[kk] = ok ? row[pcol + 4 * kk] : make_double2(0.0, 0.0);
+      } else {
+        av[kk] = make_double2(0.0, 0.0);
+        if (ok && pcol + 4 * kk < NO) av[kk] = row[pcol + 4 * kk];
+      }
+    }
+  }
+}
+// the lane's A value of k-step kk from load_a's registers
+template <int NO>
+__device__ __forceinline__ double a_sel(const double2 (&av)[frag_geom(NO).kh], int kk) {
+  constexpr FragGeom FG = frag_geom(NO);
+  if constexpr (FG.il) return (kk & 1) ? av[kk >> 1].y : av[kk >> 1].x;
+  return kk < FG.kh ? av[kk].x : av[kk - FG.kh].y;
+}
+
 template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32)
 sigma_dmma_kernel(SigmaArgs p) {
@@ -316,7 +351,7 @@ sigma_dmma_kernel(SigmaArgs p) {
       long long rowoff[kRowTiles];
 #pragma unroll
       for (int t = 0; t < kRowTiles; ++t)
-        rowoff[t] = lb * p.g_sa + kp * p.g_sk + (long long)e_row[t] * p.g_se + m_row[t] * NO + pcol;
+        rowoff[t] = lb * p.g_sa + kp * p.g_sk + (long long)e_row[t] * p.g_se + m_row[t] * NO;
       const double2* mf = Mf + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw) * (FV * 32) + lane;
       for (int w = 0; w < p.nw; ++w) {
         const int off = __ldg(p.off + w);
@@ -330,15 +365,10 @@ sigma_dmma_kernel(SigmaArgs p) {
           if (tile_row0 >= p.rows || (tile_row0 + 7) / NO < off) continue;
           const bool ok = v_row[t] && e_row[t] >= off;
           double2 av[KH];
-#pragma unroll
-          for (int kk = 0; kk < KH; ++kk) {
-            av[kk] = make_double2(0.0, 0.0);
-            if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO))
-              av[kk] = __ldg(G + rowoff[t] - (long long)off * p.g_se + 4 * kk);
-          }
+          load_a<NO>(av, G + rowoff[t] - (long long)off * p.g_se, pcol, ok);
 #pragma unroll
           for (int kk = 0; kk < KSTEPS; ++kk) {
-            const double a = kk < KH ? av[kk].x : av[kk - KH].y;
+            const double a = a_sel<NO>(av, kk);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               const int f = kk * NT + nt;
@@ -409,7 +439,7 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
     const int row = rbase + t * 8 + (lane >> 2);
     v_row[t] = row < p.rows;
     e_row[t] = row / NO;
-    r_off[t] = (long long)e_row[t] * p.g_se + (row - e_row[t] * NO) * NO + pcol;
+    r_off[t] = (long long)e_row[t] * p.g_se + (row - e_row[t] * NO) * NO;
   }
   // warp-uniform bounds of the warp's rows
   const int warp_rows = min(kRowTiles * 8, p.rows - rbase);
@@ -441,11 +471,7 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
 #pragma unroll
     for (int t = 0; t < kRowTiles; ++t) {
       const bool ok = v_row[t] && e_row[t] >= off;
-#pragma unroll
-      for (int kk = 0; kk < KH; ++kk) {
-        st.a[t][kk] = make_double2(0.0, 0.0);
-        if (ok && (NO % 4 == 0 || pcol + 4 * kk < NO)) st.a[t][kk] = __ldg(G + shift + r_off[t] + 4 * kk);
-      }
+      load_a<NO>(st.a[t], G + shift + r_off[t], pcol, ok);
     }
     if (++lw == p.nw) {
       lw = 0;
@@ -462,7 +488,7 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
     for (int kk = 0; kk < KSTEPS; ++kk) {
 #pragma unroll
       for (int t = 0; t < kRowTiles; ++t) {
-        const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
+        const double a = a_sel<NO>(st.a[t], kk);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int f = kk * NT + nt;
@@ -558,10 +584,15 @@ struct SlideGeom {
   static constexpr int kRows = NW * MT * 8;              // output rows per CTA
   static constexpr int kTE = (kRows + NO - 1) / NO + 1;         // max energy blocks per window
   static constexpr int kNeed = 2 * kTE + kSlideStages;          // live FIFO span bound
-  static constexpr int kRing = kNeed <= 32 ? 32 : (kNeed <= 64 ? 64 : 128);
   static constexpr int kBVec = frag_geom(NO).fv * 32;            // double2 per M stage
-  static constexpr size_t kSmem = (size_t)kSlideStages * kBVec * 16 + (size_t)kRing * NO * NO * 16 +
-                                  2 * kSlideStages * 8 + kMaxSlideNw * 4 + (size_t)NO * NO * 16;
+  static constexpr size_t smem_for(int ring) {
+    return (size_t)kSlideStages * kBVec * 16 + (size_t)ring * NO * NO * 16 + 2 * kSlideStages * 8 +
+           kMaxSlideNw * 4 + (size_t)NO * NO * 16;
+  }
+  static constexpr int kPow2 = kNeed <= 32 ? 32 : (kNeed <= 64 ? 64 : 128);
+  // a power-of-two FIFO (index by mask) when it fits, else exactly the live-span bound (No = 10)
+  static constexpr int kRing = smem_for(kPow2) <= 225 * 1024 ? kPow2 : kNeed;
+  static constexpr size_t kSmem = smem_for(kRing);
   static constexpr bool kFits = kSmem <= 225 * 1024;
 };
 
@@ -572,6 +603,8 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
   using SG = SlideGeom<NO, NW, MT>;
   constexpr int R = SG::kRing, SB = kSlideStages, BVEC = SG::kBVec, BLK = NO * NO;
+  // FIFO slot of a (non-negative) block index
+  auto fifo = [](int x) { return (R & (R - 1)) == 0 ? (x & (R - 1)) : (int)((unsigned)x % (unsigned)R); };
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* ring_b = reinterpret_cast<double2*>(smem_raw);
   double2* ring_a = ring_b + SB * BVEC;
@@ -611,7 +644,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     const int row = tile_row0(t) + (lane >> 2);
     v_row[t] = row < p.rows;
     e_row[t] = row / NO;
-    m_off[t] = (row - e_row[t] * NO) * NO + pcol;
+    m_off[t] = (row - e_row[t] * NO) * NO;
   }
   // valid tiles (first row inside the matrix) form a prefix in both mappings;
   // warp_emax = energy of the warp's last valid row (rows ascend with t)
@@ -676,7 +709,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     bulk_g2s(ring_b + slot * BVEC, mf, BVEC * 16, full + slot);
     if (p.gather_ranks == 0) {
       for (int e = hi - 1; e >= lo; --e) {
-        const int f = (sg * seg_blocks + top0 - e) & (R - 1);
+        const int f = fifo(sg * seg_blocks + top0 - e);
         bulk_g2s(ring_a + f * BLK, G + slab + (long long)e * p.g_se, BLK * 16, full + slot);
       }
     } else {  // G in the GF point layout of the owner ranks, read over NVLink (nbr = global atom ids)
@@ -685,7 +718,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
         const long long pt = (long long)kp * p.ne + e;
         while (r > 0 && pt < p.pt_lo[r]) --r;  // e descends: the owner rank only moves down
         const double2* src = p.G_rank[pol][r] + ((pt - p.pt_lo[r]) * p.scatter_na + nb_atom) * BLK;
-        const int f = (sg * seg_blocks + top0 - e) & (R - 1);
+        const int f = fifo(sg * seg_blocks + top0 - e);
         bulk_g2s(ring_a + f * BLK, src, BLK * 16, full + slot);
       }
     }
@@ -707,16 +740,9 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 #pragma unroll
       for (int tt = 0; tt < MT; ++tt) {
         const bool ok = v_row[tt] && e_row[tt] >= off;
-        const double2* src = ok ? ring_a + ((fbase - e_row[tt]) & (R - 1)) * BLK + m_off[tt] : zero_blk + pcol;
-#pragma unroll
-        for (int kk = 0; kk < KH; ++kk) {
-          if (NO % 4 == 0) {
-            st.a[tt][kk] = src[4 * kk];
-          } else {
-            st.a[tt][kk] = make_double2(0.0, 0.0);
-            if (ok && pcol + 4 * kk < NO) st.a[tt][kk] = src[4 * kk];
-          }
-        }
+        const double2* src = ok ? ring_a + fifo(fbase - e_row[tt]) * BLK + m_off[tt] : zero_blk;
+        // full rows (No % 4 == 0, il) read the zero block instead of predicating each element
+        load_a<NO>(st.a[tt], src, pcol, (NO % 4 == 0 || FG.il) ? true : ok);
       }
     }
     ++c_it;
@@ -732,7 +758,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     for (int kk = 0; kk < KSTEPS; ++kk) {
 #pragma unroll
       for (int t = 0; t < NV; ++t) {
-        const double a = kk < KH ? st.a[t][kk].x : st.a[t][kk - KH].y;
+        const double a = a_sel<NO>(st.a[t], kk);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int f = kk * NT + nt;
@@ -770,7 +796,7 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
 #pragma unroll
   for (int t = 0; t < MT; ++t) {
     if (!v_row[t]) continue;
-    double2* dst = sigma_block(p, pol, la, k, e_row[t]) + m_off[t] - pcol;
+    double2* dst = sigma_block(p, pol, la, k, e_row[t]) + m_off[t];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n = 4 * nt + (lane & 3);

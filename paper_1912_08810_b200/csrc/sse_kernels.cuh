@@ -18,17 +18,26 @@ constexpr int kRowTiles = 3;
 constexpr int kRowsPerCta = kSigmaWarps * kRowTiles * 8;
 
 // Fragment geometry of the real embedding of an No x No complex block
-// product for mma.sync.m8n8k4.f64 (DMMA.8x8x4):
-//   A' = [Re G | Im G]          rows x 2*NOP  (K' order: real half, then imag)
-//   B' = [[Re M, Im M] interleaved per column; [-Im M, Re M]]  2*NOP x 2*No
-//   C' columns interleave (Re, Im) of each output column n.
+// product for mma.sync.m8n8k4.f64 (DMMA.8x8x4).  C' columns interleave
+// (Re, Im) of each output column n; N' = 2*No padded to 8*nt.
+//  * split K (No % 4 != 2; NOP = No rounded up to 4):
+//      A' = [Re G | Im G]       rows x 2*NOP  (K' order: real half, then imag)
+//      B' = [[Re M, Im M] interleaved per column; [-Im M, Re M]]   2*NOP x N'
+//  * interleaved K (il: No % 4 == 2, e.g. No = 10): K' = 2*No exactly, no padding:
+//      A' row = the (re, im) doubles of the G row in memory order
+//      B' row 2p = (Re M_pn, Im M_pn) per column pair, row 2p+1 = (-Im M_pn, Re M_pn)
+// kh: 16-byte A registers per tile and stage (split: Re/Im of k-steps kk, kk+kh;
+// il: k-steps 2j, 2j+1); fv: B-fragment pairs per stage (fr rounded up to even).
 struct FragGeom {
-  int no, nop, ksteps, kh, nt, fr, fv;
+  int no, nop, ksteps, kh, nt, fr, fv, il;
 };
 __host__ __device__ constexpr FragGeom frag_geom(int no) {
-  return FragGeom{no, (no + 3) / 4 * 4, ((no + 3) / 4 * 4) / 2, ((no + 3) / 4 * 4) / 4,
-                  (2 * no + 7) / 8, (((no + 3) / 4 * 4) / 2) * ((2 * no + 7) / 8),
-                  (((no + 3) / 4 * 4) / 2) * ((2 * no + 7) / 8) / 2};
+  return no % 4 == 2
+             ? FragGeom{no, no, no / 2, (no / 2 + 1) / 2, (2 * no + 7) / 8, (no / 2) * ((2 * no + 7) / 8),
+                        ((no / 2) * ((2 * no + 7) / 8) + 1) / 2, 1}
+             : FragGeom{no, (no + 3) / 4 * 4, ((no + 3) / 4 * 4) / 2, ((no + 3) / 4 * 4) / 4,
+                        (2 * no + 7) / 8, (((no + 3) / 4 * 4) / 2) * ((2 * no + 7) / 8),
+                        (((no + 3) / 4 * 4) / 2) * ((2 * no + 7) / 8) / 2, 0};
 }
 
 struct OperatorArgs {

@@ -139,7 +139,11 @@ def test_all_sigma_kernels_bitwise(monkeypatch, name):
     (64, 20, 12, 5, 4),    # sliding-window kernel, two CTA tiles, window clipped at E = 0
     (25, 12, 12, 5, 4),    # sliding-window tail CTA: 12 rows, interleaved tiles, a partial tile
     (41, 14, 12, 5, 4),    # sliding-window tail CTA: 204 rows (warps with 3 / 2 valid tiles, partial tile)
-    (40, 13, 10, 6, 4),    # No = 10 (padded DMMA embedding; ring too large: pipelined kernel)
+    (40, 13, 10, 6, 4),    # No = 10: interleaved-K embedding (K' = 20), sliding window with a 72-slot FIFO
+    (33, 12, 6, 5, 4),     # No = 6: interleaved K, odd k-step count (3), sliding window
+    (19, 12, 2, 5, 2),     # No = 2: interleaved K, one k-step
+    (24, 12, 14, 4, 4),    # No = 14: interleaved K (K' = 28), ring too large: pipelined kernel
+    (300, 16, 10, 3, 2),   # No = 10 at the small config's NE / Nw: 11 row CTAs per (atom, k), tail CTA
     (31, 16, 4, 7, 4),     # No = 4, ragged last tile
     (30, 14, 12, 9, 6),    # NB = 6 neighbour slots
     (20, 13, 17, 5, 2),    # No = 17 > 16: the DFMA kernel (K3g)
