@@ -365,6 +365,7 @@ def e2e_phase(args, p, grid, idx, rank, world, local_rank, want_digest) -> dict:
                  "steps": args.e2e_steps, "warmup": args.e2e_warmup, "step_s": times,
                  "bitwise_equal_to_device_run": bool(same == 1.0),
                  "host_pack_ms": tim.get("h2d_ms"), "host_unpack_ms": tim.get("d2h_ms"),
+                 "library_gpu_span_s": (tim.get("total_ms") or 0) / 1e3,
                  "staged": tim.get("staged"), "host_threads": tim.get("host_threads")}
         if pinned:
             entry["path"] = ("sigma_host_slab -> sse_sigma_c128_slab (C ABI) from pinned torch buffers: direct DMA "

@@ -846,6 +846,8 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
     auto now_ms = [] {
       return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
+    const bool trace = getenv("SSE_STAGING_TRACE") != nullptr;  // per-chunk host timeline on stderr
+    const double t_call = now_ms();
     // strided row copies (rows x width bytes) split over the pool, ~1 MB per work item
     auto copy_rows = [&](char* dst, size_t dpitch, const char* src, size_t spitch, size_t width, size_t nrows) {
       const size_t per = std::max<size_t>(1, (1u << 20) / std::max<size_t>(width, 1));
@@ -863,6 +865,9 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
         copy_rows(Sh[p] + (lo + pc.a0 - c.hs.atom0) * blk, hs_pitch, src + p * rows * pc.n * blk, pc.n * blk,
                   pc.n * blk, rows);
       unpack_ms += now_ms() - t0;
+      if (trace)
+        fprintf(stderr, "[sse staging] unpack chunk %zu (%lld atoms): %.1f-%.1f ms\n", k, (long long)pc.n, t0 - t_call,
+                now_ms() - t_call);
     };
     const DevPtrs ptr{ds.g[0].as<double2>(), ds.g[1].as<double2>(), ds.dc[0].as<double2>(),
                       ds.dc[1].as<double2>(), ds.dh.as<double2>(), ds.s[0].as<double2>(),
@@ -888,6 +893,9 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
         }
         copy_rows(dh_st, n * dh_atom, dHh + a0 * dh_atom, n * dh_atom, n * dh_atom, 1);
         pack_ms += now_ms() - t0;
+        if (trace)
+          fprintf(stderr, "[sse staging] pack chunk %zu (%lld atoms, %lld G cols): %.1f-%.1f ms\n", ci, (long long)n,
+                  (long long)ncols, t0 - t_call, now_ms() - t_call);
         for (int p = 0; p < 2; ++p) {
           if (ncols > 0)
             CU(cudaMemcpy2DAsync((char*)ds.g[p].ptr + (pc.c0 - glo) * blk, gn * blk, g_st[p], ncols * blk, ncols * blk,
@@ -928,7 +936,10 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
         if (!out_ready[ci]) return fail(SSE_ECUDA, "event creation failed");
         CU(cudaEventRecord(out_ready[ci], ds.s_d2h));
         if (ci >= 1) {  // the previous chunk's Sigma, while this chunk computes
+          const double tw = now_ms();
           CU(cudaEventSynchronize(out_ready[ci - 1]));
+          if (trace)
+            fprintf(stderr, "[sse staging] wait D2H chunk %zu: %.1f-%.1f ms\n", ci - 1, tw - t_call, now_ms() - t_call);
           unpack(ci - 1);
         }
       } else {

@@ -142,7 +142,7 @@ def test_all_sigma_kernels_bitwise(monkeypatch, name):
     (40, 13, 10, 6, 4),    # No = 10: interleaved-K embedding (K' = 20), sliding window with a 72-slot FIFO
     (33, 12, 6, 5, 4),     # No = 6: interleaved K, odd k-step count (3), sliding window
     (19, 12, 2, 5, 2),     # No = 2: interleaved K, one k-step
-    (24, 12, 14, 4, 4),    # No = 14: interleaved K (K' = 28), ring too large: pipelined kernel
+    (24, 12, 14, 5, 4),    # No = 14: interleaved K (K' = 28), ring too large: pipelined kernel
     (300, 16, 10, 3, 2),   # No = 10 at the small config's NE / Nw: 11 row CTAs per (atom, k), tail CTA
     (31, 16, 4, 7, 4),     # No = 4, ragged last tile
     (30, 14, 12, 9, 6),    # NB = 6 neighbour slots
