@@ -52,7 +52,12 @@ def stream(seed, p, dh_scale):
     return g_l, g_g, d_l, d_g, dh
 
 
+run_case_filter = None  # "only" mode: the names to (re)generate
+
+
 def run_case(name, p, seed, dh_scale=1.0, grid=None, with_pi=False, store_dc=False, store_bf=True):
+    if run_case_filter is not None and name not in run_case_filter:
+        return
     grid = grid if grid is not None else default_grid(p)
     nmap = build_neighbor_map(p.n_A, p.n_B)
     g_l, g_g, d_l, d_g, dh = stream(seed, p, dh_scale)
@@ -175,10 +180,23 @@ def slide_cases():
              dh_scale=0.05, store_bf=False)
     run_case("paperlike_w70_s11", SimParams(n_kz=3, n_qz=2, n_E=90, n_w=70, n_A=4, n_B=2, n_orb=12), 11,
              dh_scale=0.05, store_bf=False)
+    # the paper's Pi shapes (No = 12, NB = 4, Nw = 70: K5 pi_build_dmma_kernel<12> and the split
+    # K6 v4 pi_dmma4_kernel<12,4,4,3,4,true>, 9 lag tiles) pinned to the reference's sse_pi
+    run_case("pi_paperlike_s12", SimParams(n_kz=2, n_qz=2, n_E=80, n_w=70, n_A=6, n_B=4, n_orb=12), 12,
+             dh_scale=0.05, store_bf=False, with_pi=True)
 
 
 def main():
     if sys.argv[1:] == ["slide"]:
+        slide_cases()
+        return
+    if len(sys.argv) > 2 and sys.argv[1] == "only":  # regenerate named slide cases only
+        import inspect
+
+        src = inspect.getsource(slide_cases)
+        for name in sys.argv[2:]:
+            assert f'"{name}"' in src, name
+        globals()["run_case_filter"] = set(sys.argv[2:])
         slide_cases()
         return
     scalar_kat()

@@ -26,7 +26,9 @@ from tests.golden_cases import load_case
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-10
-PI_CASES = ["test_tiny_s3", "test_tiny_s4", "cli_tiny_s1", "cli_small_s2", "general_grid_s8"]
+# pi_paperlike_s12: the paper's No = 12, NB = 4, Nw = 70 -> K5 pi_build_dmma_kernel<12> and the
+# split K6 v4 (9 lag tiles) against the reference's own sse_pi output
+PI_CASES = ["test_tiny_s3", "test_tiny_s4", "cli_tiny_s1", "cli_small_s2", "general_grid_s8", "pi_paperlike_s12"]
 
 
 def _grid(case):
@@ -46,6 +48,11 @@ def test_pi_golden_parity(name):
     out = sse_pi(GreensTensor(c.g_l, c.g_g), c.dh, NeighborMap(c.idx), _grid(c), c.p.n_qz, counter=counter)
     dev = orc.parity_dev(out.lesser, out.greater, c.arrays["pi_l"], c.arrays["pi_g"])
     assert dev <= TOL, (name, dev)
+    if name == "pi_paperlike_s12":
+        from paper_1912_08810_b200 import _lib
+
+        assert _lib.kernel_name("pi") == "pi_dmma4_kernel<12,4,4,3,4,true>", _lib.kernel_name("pi")
+        assert _lib.kernel_name("pi_build") == "pi_build_dmma_kernel<12>"
     p = c.p
     assert counter.stages == pi_tallies(True, p.n_kz, p.n_qz, p.n_E, p.n_w, p.n_A, p.n_B, p.n_orb)
 

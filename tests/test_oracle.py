@@ -38,7 +38,17 @@ def test_preprocess_matches_reference_bitwise(case):
         assert np.array_equal(dc_l, case.arrays["dc_l"])
 
 
+def _heavy(case) -> bool:
+    """Cases whose pure-Python REFERENCE-arrangement / Pi restatements take > 30 s on CPU; their
+    GPU tests compare with the stored reference outputs directly, and the restatements are
+    pinned on the other cases."""
+    p = case.p
+    return p.n_A * p.n_B * p.n_qz * p.n_w * p.n_kz * p.n_E > 400_000
+
+
 def test_sigma_reference_restatement(case):
+    if _heavy(case):
+        pytest.skip("heavy case: the oracle's REFERENCE arrangement is pinned on the smaller goldens")
     dc_l, dc_g = orc.preprocess_D(case.d_l, case.d_g, case.idx)
     out_l, out_g = orc.sigma_reference(
         case.g_l, case.g_g, dc_l, dc_g, case.dh, case.idx, case.offsets, case.weights
@@ -77,6 +87,8 @@ def test_loop_oracle_small(case):
 def test_pi_restatement(case):
     if "pi_l" not in case.arrays:
         pytest.skip("no Pi fixture for this case")
+    if _heavy(case):
+        pytest.skip("heavy case: the oracle's Pi restatement is pinned on the smaller goldens")
     ew = case.meta["energy_weight"]
     ch_l, ch_g = orc.pi_chains(case.g_l, case.g_g, case.dh, case.idx, case.offsets, ew, case.p.n_qz)
     pi_l, pi_g = orc.pi_from_chains(ch_l, ch_g)
