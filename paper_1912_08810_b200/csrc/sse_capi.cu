@@ -181,7 +181,7 @@ struct DevState {
   int device = 0;
   cudaStream_t stream = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev[6] = {};
-  DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev;
+  DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev, zero_m;
   DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2], draw[2];
   PinnedBuf stage_in[2], stage_out[2];  // host staging ring of the pageable-memory host calls
   cudaEvent_t stage_ev[2] = {};         // H2D from stage_in[b] done
@@ -278,6 +278,10 @@ int init_dev(DevState& d, int device) {
   for (auto& e : d.ev) CU(cudaEventCreate(&e));
   CU(cudaEventCreateWithFlags(&d.scratch_done, cudaEventDisableTiming));
   for (auto& e : d.stage_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // one zero M-fragment vector (the multi-momentum K3's B of an invalid (k, kp) pair)
+  const size_t zbytes = (size_t)sse::frag_geom(sse::kMaxDmmaOrb).fv * 32 * 16;
+  CHECK(d.zero_m.ensure(zbytes));
+  CU(cudaMemset(d.zero_m.ptr, 0, zbytes));
   return SSE_OK;
 }
 
@@ -305,7 +309,7 @@ void drain(DevState& ds) {
 void destroy_dev(DevState& d) {
   cudaSetDevice(d.device);
   for (DevBuf* b : {&d.g[0], &d.g[1], &d.s[0], &d.s[1], &d.dc[0], &d.dc[1], &d.dh, &d.op[0],
-                    &d.op[1], &d.nbr, &d.off, &d.wt, &d.tmp_g, &d.tmp_s, &d.pp_nbr, &d.pp_rev,
+                    &d.op[1], &d.nbr, &d.off, &d.wt, &d.tmp_g, &d.tmp_s, &d.pp_nbr, &d.pp_rev, &d.zero_m,
                     &d.pi_vt[0], &d.pi_vt[1], &d.pi_part, &d.pi_mask, &d.pi_out[0], &d.pi_out[1],
                     &d.draw[0], &d.draw[1]})
     b->release();
@@ -369,12 +373,26 @@ constexpr int64_t kPiEnergiesPerChunk = 96;
 
 // Operator chunk: bound the per-polarity operator buffer to ~1 GiB
 // (SSE_OP_CHUNK_ATOMS overrides, for experiments).
-int64_t op_chunk_atoms(const sse_dims* d) {
+// Offsets non-decreasing with steps <= 1 (default_grid's): the sliding-window K3 kernels apply.
+int offsets_slide(const sse_dims* d, const int64_t* off) {
+  for (int64_t w = 1; w < d->nw; ++w)
+    if (off[w] < off[w - 1] || off[w] > off[w - 1] + 1) return 0;
+  return 1;
+}
+
+// K2 writes combined multi-momentum fragments for this call (sse::sigma_uses_combined).
+int comb_kg_of(const sse_dims* d, const int64_t* off) {
+  if (d->norb > sse::kMaxDmmaOrb || d->nqz > 8) return 0;
+  return sse::sigma_uses_combined((int)d->norb, (int)d->nw, offsets_slide(d, off)) ? sse::kCombKG : 0;
+}
+
+int64_t op_chunk_atoms(const sse_dims* d, const int64_t* off) {
   if (const char* env = getenv("SSE_OP_CHUNK_ATOMS")) {
     const long long v = atoll(env);
     if (v > 0) return v;
   }
-  const size_t per_atom = sse::operator_bytes((int)d->norb, (int)d->nb, (int)d->nqz, (int)d->nw, 1);
+  const size_t per_atom = sse::operator_bytes((int)d->norb, (int)d->nb, (int)d->nqz, (int)d->nw, 1,
+                                              comb_kg_of(d, off), (int)d->nkz);
   return std::max<int64_t>(1, (int64_t)((1ull << 30) / std::max<size_t>(per_atom, 1)));
 }
 
@@ -447,7 +465,8 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
               const DevPtrs& p, const int64_t* off, int64_t a0, int64_t n, cudaStream_t st,
               int npol, int* launches, const ScatterCfg* sc = nullptr) {
   const int no = (int)d->norb;
-  const size_t opb = sse::operator_bytes(no, (int)d->nb, (int)d->nqz, (int)d->nw, (int)n);
+  const int comb = comb_kg_of(d, off);
+  const size_t opb = sse::operator_bytes(no, (int)d->nb, (int)d->nqz, (int)d->nw, (int)n, comb, (int)d->nkz);
   CHECK(ds.op[0].ensure(opb));
   CHECK(ds.op[1].ensure(opb));
   sse::OperatorArgs oa{};
@@ -466,6 +485,8 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   oa.chunk_atoms = (int)n;
   oa.fragment_order = no <= sse::kMaxDmmaOrb ? 1 : 0;
   oa.npol = npol;
+  oa.comb_kg = comb;
+  oa.nkz = (int)d->nkz;
   CHECK(profiled(ds, st, SSE_PROF_OPERATOR, 0.0, [&] { return sse::launch_build_operator(oa, st); }));
 
   const SlabStrides gs = strides_of(d, g), ss = strides_of(d, out);
@@ -493,11 +514,11 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   sa.s_sk = ss.sk;
   sa.s_se = ss.se;
   sa.npol = npol;
-  sa.off_slide = 1;
+  sa.zeroM = ds.zero_m.as<double2>();
+  sa.comb_kg = comb;
+  sa.off_slide = offsets_slide(d, off);
   sa.lookahead = getenv("SSE_SLIDE_LOOKAHEAD") ? atoi(getenv("SSE_SLIDE_LOOKAHEAD")) : 0;
   sa.k3_opts = getenv("SSE_K3_OPTS") ? atoi(getenv("SSE_K3_OPTS")) : 3;
-  for (int64_t w = 1; w < d->nw; ++w)
-    if (off[w] < off[w - 1] || off[w] > off[w - 1] + 1) sa.off_slide = 0;
   if (sc && sc->nranks > 0) {
     sa.scatter_ranks = sc->nranks;
     sa.scatter_na = sc->na;
@@ -521,7 +542,7 @@ int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const ss
                     const DevPtrs& p, const int64_t* nmap, const int64_t* off, const double* wt,
                     cudaStream_t st, int* launches, int npol = 2, const ScatterCfg* sc = nullptr) {
   CHECK(prepare_tables(ds, d, g, out, nmap, off, wt, st));
-  const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d), out.natoms);
+  const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d, off), out.natoms);
   for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk)
     CHECK(run_chunk(ds, d, g, out, p, off, a0, std::min<int64_t>(chunk, out.natoms - a0), st, npol,
                     launches, sc));
@@ -752,7 +773,7 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
       DevPtrs ptr{ds.tmp_g.as<double2>(), ds.tmp_g.as<double2>(), ds.dc[p].as<double2>(),
                   ds.dc[p].as<double2>(), ds.dh.as<double2>(), ds.tmp_s.as<double2>(),
                   ds.tmp_s.as<double2>()};
-      const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d), on);
+      const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d, c.off), on);
       for (int64_t a0 = 0; a0 < on; a0 += chunk)
         CHECK(run_chunk(ds, d, ga, oa, ptr, c.off, a0, std::min<int64_t>(chunk, on - a0), st, 1,
                         &launches));
@@ -771,7 +792,7 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
     CHECK(prepare_tables(ds, d, gslab, oslab, rows_nmap, c.off, c.wt, st));
     CU(cudaEventRecord(ds.ev[2], st));
     CU(cudaStreamWaitEvent(ds.s_h2d, ds.ev[2], 0));
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(op_chunk_atoms(d), (on + 7) / 8));
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(op_chunk_atoms(d, c.off), (on + 7) / 8));
     // chunk boundaries: a geometric ramp of small chunks at the start (the first chunk's H2D is
     // not hidden; each chunk's compute then covers the next one's H2D, ~3.5x faster per atom on
     // one B200) and the mirrored ramp at the end (the last chunk's D2H is not hidden)

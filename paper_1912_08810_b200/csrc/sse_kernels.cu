@@ -152,6 +152,69 @@ __global__ void build_operator_kernel(OperatorArgs p) {
     }
     return;
   }
+  if (p.comb_kg > 0) {
+    // combined multi-momentum fragments: per frequency w, M_q of every q (< kOpBlocks at a
+    // time... all Nqz fit: Nqz <= kOpBlocks is checked by the launcher) into shared memory, then
+    // for every source momentum kp and momentum group g one vector whose N' columns are
+    // [M_{q_k0} | M_{q_k0+1} | ...] with q_k = (k - kp) mod Nkz (zero if invalid)
+    double2* s_m = s_p + 9 * no2;  // [Nqz][no][no]
+    const FragGeom fg = frag_geom(no);
+    const CombGeom cg = comb_geom(no, p.comb_kg);
+    const int groups = (p.nkz + p.comb_kg - 1) / p.comb_kg;
+    const int per_vec = cg.fvc * 32;
+    for (int pol = 0; pol < p.npol; ++pol) {
+      const double2* dc_base = p.Dc[pol];
+      for (int w = 0; w < p.nw; ++w) {
+        const double wt = p.wt[w];
+        for (int x = threadIdx.x; x < p.nqz * no2; x += blockDim.x) {
+          const int q = x / no2, v = x - q * no2;
+          const double2* dc = dc_base + ((((long long)q * p.nw + w) * p.dc_natoms + a_slab) * p.nb + s) * 9;
+          double re = 0.0, im = 0.0;
+          for (int ij = 0; ij < 9; ++ij) {
+            const double2 c = dc[ij], m = s_p[ij * no2 + v];
+            re = fma(c.x, m.x, re);
+            re = fma(-c.y, m.y, re);
+            im = fma(c.x, m.y, im);
+            im = fma(c.y, m.x, im);
+          }
+          s_m[x] = make_double2(wt * re, wt * im);
+        }
+        __syncthreads();
+        const int nvec = p.nkz * groups;
+        for (int x = threadIdx.x; x < nvec * per_vec; x += blockDim.x) {
+          const int vec = x / per_vec, v = x - vec * per_vec;
+          const int kp = vec / groups, g = vec - kp * groups;
+          const int j = v >> 5, lane = v & 31;
+          double vals[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int f = 2 * j + h;
+            double val = 0.0;
+            if (f < cg.frc) {
+              const int kk = f / cg.ntc, nt = f % cg.ntc;
+              const int kr = 4 * kk + (lane & 3), c = 8 * nt + (lane >> 2);
+              const int cc = c >> 1, part = c & 1, kl = cc / no, n = cc - kl * no;
+              const int k = g * p.comb_kg + kl;
+              int q = k - kp;
+              if (q < 0) q += p.nkz;
+              const bool im_row = fg.il ? (kr & 1) : kr >= fg.nop;
+              const int pr = fg.il ? kr >> 1 : (im_row ? kr - fg.nop : kr);
+              if (kl < p.comb_kg && k < p.nkz && q < p.nqz && pr < no) {
+                const double2 m = s_m[q * no2 + pr * no + n];
+                val = !im_row ? (part == 0 ? m.x : m.y) : (part == 0 ? -m.y : m.x);
+              }
+            }
+            vals[h] = val;
+          }
+          // [atom, s, kp, g, w] vectors
+          const long long vidx = ((((long long)blockIdx.x) * p.nkz + kp) * groups + g) * p.nw + w;
+          p.M[pol][vidx * per_vec + v] = make_double2(vals[0], vals[1]);
+        }
+        __syncthreads();
+      }
+    }
+    return;
+  }
   // DMMA fragment order, kOpBlocks (q,w) blocks at a time: phase 1 computes each complex
   // M element once into shared memory (wt-scaled), phase 2 writes the real embedding
   //   B'[re-row p][2n] = Re M, B'[re-row p][2n+1] = Im M,
@@ -225,6 +288,21 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+}
+
+// The i-th momentum transfer q (i < Nqz) of output momentum k in the accumulation order all
+// Sigma kernels share: source momenta kp = (k - q) mod Nkz ascending (the multi-momentum K3
+// walks kp and serves every k of its group from the same G rows).  kp = k - q for the first
+// L = min(k + 1, Nqz) terms (q = L-1 .. 0), then kp = k - q + Nkz (q = Nqz-1 .. k+1).
+__host__ __device__ __forceinline__ void q_order(int k, int i, int nkz, int nqz, int& q, int& kp) {
+  const int L = k + 1 < nqz ? k + 1 : nqz;
+  if (i < L) {
+    q = L - 1 - i;
+    kp = k - q;
+  } else {
+    q = k + nqz - i;
+    kp = k - q + nkz;
+  }
 }
 
 // Base of the Sigma block (k, E) of chunk atom la: the slab (s_* strides), or
@@ -343,9 +421,9 @@ sigma_dmma_kernel(SigmaArgs p) {
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
 
-  for (int q = 0; q < p.nqz; ++q) {
-    int kp = (k - q) % p.nkz;
-    if (kp < 0) kp += p.nkz;
+  for (int qi = 0; qi < p.nqz; ++qi) {
+    int q, kp;
+    q_order(k, qi, p.nkz, p.nqz, q, kp);
     for (int s = 0; s < p.nb; ++s) {
       const int lb = __ldg(p.nbr + la * p.nb + s);
       long long rowoff[kRowTiles];
@@ -455,12 +533,12 @@ sigma_dmma_pipe_kernel(SigmaArgs p) {
   int lq = 0, ls = 0, lw = 0;
   long long slab = 0;           // (k', b) slab offset of the cursor's (q, s)
   const double2* mfq = nullptr;  // M fragments of the cursor's (q, s), lane-offset
-  auto setup_qs = [&]() {
-    int kp = (k - lq) % p.nkz;
-    if (kp < 0) kp += p.nkz;
+  auto setup_qs = [&]() {  // lq indexes the shared q order (q_order)
+    int q, kp;
+    q_order(k, lq, p.nkz, p.nqz, q, kp);
     const int lb = __ldg(p.nbr + la * p.nb + ls);
     slab = lb * p.g_sa + kp * p.g_sk;
-    mfq = Mf + ((long long)((la * p.nb + ls) * p.nqz + lq) * p.nw) * (FV * 32) + lane;
+    mfq = Mf + ((long long)((la * p.nb + ls) * p.nqz + q) * p.nw) * (FV * 32) + lane;
   };
   auto load = [&](OperandStage<NO>& st) {
     const int off = __ldg(offs + lw);
@@ -697,9 +775,9 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
   auto produce = [&](int t) {  // lane 0 of the owning warp
     const int slot = t % SB;
     const int sg = t / nw_eff, w = t - sg * nw_eff;
-    const int q = sg / p.nb, s = sg - q * p.nb;
-    int kp = (k - q) % p.nkz;
-    if (kp < 0) kp += p.nkz;
+    const int qi = sg / p.nb, s = sg - qi * p.nb;
+    int q, kp;
+    q_order(k, qi, p.nkz, p.nqz, q, kp);
     const long long nb_atom = __ldg(p.nbr + la * p.nb + s);
     const long long slab = nb_atom * p.g_sa + kp * p.g_sk;
     const double2* mf = Mf + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw + w) * BVEC;
@@ -801,6 +879,270 @@ sigma_dmma_slide_kernel(SigmaArgs p) {
     for (int nt = 0; nt < NT; ++nt) {
       const int n = 4 * nt + (lane & 3);
       if (n < NO) dst[n] = make_double2(-acc[t][nt][1], acc[t][nt][0]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// K3m (multi-momentum sliding window) — production kernel.  As the sliding-
+// window K3, but a CTA serves KG output momenta k at once: stage (kp, s, w)
+// stages the G rows G[kp, E - off_w, f(a,s)] ONCE and the KG M-fragment vectors
+// M[q_k = (k - kp) mod Nkz, w, a, s] side by side (a zero vector where q_k >=
+// Nqz), and each warp runs its 3 row tiles x (KG x NT) n-tiles: 162 DMMAs per
+// warp-stage at No = 12, KG = 3 (the single-momentum kernel: 54), so the
+// per-stage barrier / operand-load overhead is amortised over 3x the tensor
+// work, and the A fragments (G rows) are loaded once for KG momenta.  Stages
+// walk kp ascending, so every output accumulates in the shared q_order
+// (bitwise equal to the other K3 kernels).  B ring of kKStages stages (the
+// stage is KG times larger), FIFO of G blocks as before.
+// --------------------------------------------------------------------------
+constexpr int kKStages = 6;
+constexpr int kKLookahead = 3;
+
+template <int NO, int NW, int MT, int KG, bool COMB = false>
+struct KSlideGeom {
+  static constexpr int kRows = NW * MT * 8;
+  static constexpr int kTE = (kRows + NO - 1) / NO + 1;
+  static constexpr int kNeed = 2 * kTE + kKStages;
+  static constexpr int kBVec = frag_geom(NO).fv * 32;  // double2 per momentum and stage
+  // COMB: one combined vector (comb_geom) per stage; else KG per-q vectors side by side
+  static constexpr int kBStage = COMB ? comb_geom(NO, KG).fvc * 32 : KG * kBVec;
+  static constexpr size_t smem_for(int ring) {
+    return (size_t)kKStages * kBStage * 16 + (size_t)ring * NO * NO * 16 + 2 * kKStages * 8 + kMaxSlideNw * 4 +
+           (size_t)NO * NO * 16;
+  }
+  static constexpr int kPow2 = kNeed <= 32 ? 32 : (kNeed <= 64 ? 64 : 128);
+  static constexpr int kRing = smem_for(kPow2) <= 225 * 1024 ? kPow2 : kNeed;
+  static constexpr size_t kSmem = smem_for(kRing);
+  static constexpr bool kFits = kSmem <= 225 * 1024;
+};
+
+template <int NO, int NW, int MT, int KG, bool COMB = false>
+__global__ void __launch_bounds__(NW * 32, 1)
+sigma_dmma_kslide_kernel(SigmaArgs p) {
+  constexpr FragGeom FG = frag_geom(NO);
+  constexpr CombGeom CG = comb_geom(NO, KG);
+  constexpr int KH = FG.kh, NT = FG.nt, FV = FG.fv, FR = FG.fr;
+  constexpr int NTA = COMB ? CG.ntc : KG * NT;  // accumulator n-tiles per row tile
+  using SG = KSlideGeom<NO, NW, MT, KG, COMB>;
+  constexpr int R = SG::kRing, SB = kKStages, BVEC = SG::kBVec, BSTAGE = SG::kBStage, BLK = NO * NO;
+  auto fifo = [](int x) { return (R & (R - 1)) == 0 ? (x & (R - 1)) : (int)((unsigned)x % (unsigned)R); };
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring_b = reinterpret_cast<double2*>(smem_raw);
+  double2* ring_a = ring_b + SB * BSTAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring_a + R * BLK);
+  uint64_t* empty = full + SB;
+
+  const int pol = blockIdx.y;
+  int bx = blockIdx.x;
+  const int rc = bx % p.ctas_per_ak;
+  bx /= p.ctas_per_ak;
+  const int kg = bx % p.kgroups;
+  const int la = bx / p.kgroups;
+  const int k0 = p.k_first + kg * KG;  // output momenta k0 .. k0 + KG - 1 (those < Nkz)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cta_r0 = rc * SG::kRows;
+  const bool tail = (p.k3_opts & 1) && cta_r0 + SG::kRows > p.rows;
+  auto tile_row0 = [&](int t) { return tail ? cta_r0 + (t * NW + warp) * 8 : cta_r0 + warp * (MT * 8) + t * 8; };
+  const int pcol = lane & 3;
+  const double2* __restrict__ G = p.G[pol];
+  const double2* __restrict__ Mf = p.M[pol];
+  const int* __restrict__ offs = p.off;
+  const int e_lo = cta_r0 / NO;
+  const int e_hi = (min(cta_r0 + SG::kRows, p.rows) - 1) / NO;
+
+  int e_row[MT], m_off[MT];
+  bool v_row[MT];
+#pragma unroll
+  for (int t = 0; t < MT; ++t) {
+    const int row = tile_row0(t) + (lane >> 2);
+    v_row[t] = row < p.rows;
+    e_row[t] = row / NO;
+    m_off[t] = (row - e_row[t] * NO) * NO;
+  }
+  int n_valid = 0;
+#pragma unroll
+  for (int t = 0; t < MT; ++t) n_valid += tile_row0(t) < p.rows ? 1 : 0;
+  const int warp_emax = n_valid > 0 ? (min(tile_row0(n_valid - 1) + 8, p.rows) - 1) / NO : -1;
+
+  double acc[MT][NTA][2];
+#pragma unroll
+  for (int t = 0; t < MT; ++t)
+#pragma unroll
+    for (int n = 0; n < NTA; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+
+  int* s_off = reinterpret_cast<int*>(empty + SB);
+  for (int w = threadIdx.x; w < p.nw; w += blockDim.x) s_off[w] = offs[w];
+  double2* zero_blk = reinterpret_cast<double2*>(s_off + kMaxSlideNw);
+  for (int x = threadIdx.x; x < BLK; x += blockDim.x) zero_blk[x] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int nw_eff = p.nw;
+  if (p.k3_opts & 2)
+    while (nw_eff > SB && s_off[nw_eff - 1] > e_hi) --nw_eff;
+  const int n_it = p.nkz * p.nb * nw_eff;  // segments (kp, s), kp ascending
+  const int all_groups = (p.nkz + KG - 1) / KG;  // COMB: the vector index's group count
+
+  const int top0 = e_hi - s_off[0];
+  const bool seg_empty = top0 < 0;
+  const int seg_blocks = seg_empty ? 0 : top0 + 1 - max(0, e_lo - s_off[nw_eff - 1]);
+  auto win_low = [&](int w) { return w < 0 ? top0 + 1 : max(0, e_lo - s_off[w]); };
+
+  auto produce = [&](int t) {  // lane 0 of the owning warp
+    const int slot = t % SB;
+    const int sg = t / nw_eff, w = t - sg * nw_eff;
+    const int kp = sg / p.nb, s = sg - kp * p.nb;
+    const long long nb_atom = __ldg(p.nbr + la * p.nb + s);
+    const long long slab = nb_atom * p.g_sa + kp * p.g_sk;
+    const int hi = seg_empty ? 0 : win_low(w - 1), lo = seg_empty ? 0 : win_low(w);
+    if (t >= SB) mbar_wait(empty + slot, (uint32_t)(((t - SB) / SB) & 1));
+    mbar_arrive_expect_tx(full + slot, (uint32_t)(BSTAGE + (hi - lo) * BLK) * 16);
+    if constexpr (COMB) {
+      const double2* mf = Mf + ((((long long)(la * p.nb + s) * p.nkz + kp) * all_groups + kg) * p.nw + w) * BSTAGE;
+      bulk_g2s(ring_b + slot * BSTAGE, mf, BSTAGE * 16, full + slot);
+    } else {
+#pragma unroll
+      for (int kl = 0; kl < KG; ++kl) {
+        int q = k0 + kl - kp;
+        if (q < 0) q += p.nkz;
+        const bool ok = k0 + kl < p.nkz && q < p.nqz;
+        const double2* mf = ok ? Mf + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw + w) * BVEC : p.zeroM;
+        bulk_g2s(ring_b + slot * BSTAGE + kl * BVEC, mf, BVEC * 16, full + slot);
+      }
+    }
+    if (p.gather_ranks == 0) {
+      for (int e = hi - 1; e >= lo; --e)
+        bulk_g2s(ring_a + fifo(sg * seg_blocks + top0 - e) * BLK, G + slab + (long long)e * p.g_se, BLK * 16,
+                 full + slot);
+    } else {  // G in the GF point layout of the owner ranks, read over NVLink (nbr = global atom ids)
+      int r = p.gather_ranks - 1;
+      for (int e = hi - 1; e >= lo; --e) {
+        const long long pt = (long long)kp * p.ne + e;
+        while (r > 0 && pt < p.pt_lo[r]) --r;
+        const double2* src = p.G_rank[pol][r] + ((pt - p.pt_lo[r]) * p.scatter_na + nb_atom) * BLK;
+        bulk_g2s(ring_a + fifo(sg * seg_blocks + top0 - e) * BLK, src, BLK * 16, full + slot);
+      }
+    }
+  };
+
+  int c_it = 0, c_sg = 0, c_w = 0;
+  double2 av[MT][KH];
+  auto lds_a = [&](int off) {  // wait for the stage, then the A operands of the warp's tiles
+    const int slot = c_it % SB;
+    const int fbase = c_sg * seg_blocks + top0 + off;
+    mbar_wait(full + slot, (uint32_t)((c_it / SB) & 1));
+    if (warp_emax >= off) {
+#pragma unroll
+      for (int tt = 0; tt < MT; ++tt) {
+        const bool ok = v_row[tt] && e_row[tt] >= off;
+        const double2* src = ok ? ring_a + fifo(fbase - e_row[tt]) * BLK + m_off[tt] : zero_blk;
+        load_a<NO>(av[tt], src, pcol, (NO % 4 == 0 || FG.il) ? true : ok);
+      }
+    }
+  };
+  // the stage's DMMAs: B fragment pair j of momentum kl feeds every tile; each accumulator
+  // (tile, momentum, n-tile) still sees its k-steps in ascending order
+  auto compute_tiles = [&](int slot, auto nv) {
+    constexpr int NV = decltype(nv)::value;
+    const double2* sb = ring_b + slot * BSTAGE + lane;
+    if constexpr (COMB) {
+#pragma unroll
+      for (int j = 0; j < CG.fvc; ++j) {
+        const double2 bv = sb[j * 32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int f = 2 * j + h;
+          if (f < CG.frc) {
+            const int kk = f / CG.ntc, nt = f - (f / CG.ntc) * CG.ntc;
+            const double b = h ? bv.y : bv.x;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) dmma884_nv(acc[t][nt], a_sel<NO>(av[t], kk), b);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < FV; ++j) {
+        // keep the B loads of fragment pair j next to its DMMAs (hoisting all of them spills)
+        if (KG > 1) asm volatile("" ::: "memory");
+#pragma unroll
+        for (int kl = 0; kl < KG; ++kl) {
+          const double2 bv = sb[kl * BVEC + j * 32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int f = 2 * j + h;
+            if (f < FR) {
+              const int kk = f / NT, nt = f - (f / NT) * NT;
+              const double b = h ? bv.y : bv.x;
+#pragma unroll
+              for (int t = 0; t < NV; ++t) dmma884_nv(acc[t][kl * NT + nt], a_sel<NO>(av[t], kk), b);
+            }
+          }
+        }
+      }
+    }
+  };
+  auto release = [&](int t) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + (t % SB));
+  };
+
+  const int L = p.lookahead > 0 ? min(p.lookahead, SB - 1) : kKLookahead;
+  if (lane == 0)
+    for (int i = warp; i < L && i < n_it; i += NW) produce(i);
+  auto run = [&](auto nv) {
+    for (int it = 0; it < n_it; ++it) {
+      if (lane == 0 && it + L < n_it && (it + L) % NW == warp) produce(it + L);
+      const int off = s_off[c_w];
+      lds_a(off);
+      if (warp_emax >= off) compute_tiles(it % SB, nv);
+      release(it);
+      ++c_it;
+      if (++c_w == nw_eff) {
+        c_w = 0;
+        ++c_sg;
+      }
+    }
+  };
+  if (n_valid == MT) run(std::integral_constant<int, MT>{});
+  else if (MT > 2 && n_valid == 2) run(std::integral_constant<int, (MT > 2 ? 2 : 0)>{});
+  else if (MT > 1 && n_valid == 1) run(std::integral_constant<int, (MT > 1 ? 1 : 0)>{});
+  else run(std::integral_constant<int, 0>{});
+
+  if constexpr (COMB) {
+    // accumulator n-tile nt, lane: complex column cc = 4 nt + (lane & 3) of the group's
+    // [momentum][No] column space
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      if (!v_row[t]) continue;
+#pragma unroll
+      for (int nt = 0; nt < CG.ntc; ++nt) {
+        const int cc = 4 * nt + (lane & 3), kl = cc / NO, n = cc - kl * NO;
+        if (kl < KG && k0 + kl < p.nkz)
+          sigma_block(p, pol, la, k0 + kl, e_row[t])[m_off[t] + n] = make_double2(-acc[t][nt][1], acc[t][nt][0]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int kl = 0; kl < KG; ++kl) {
+      if (k0 + kl >= p.nkz) break;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        if (!v_row[t]) continue;
+        double2* dst = sigma_block(p, pol, la, k0 + kl, e_row[t]) + m_off[t];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int n = 4 * nt + (lane & 3);
+          if (n < NO) dst[n] = make_double2(-acc[t][kl * NT + nt][1], acc[t][kl * NT + nt][0]);
+        }
+      }
     }
   }
 }
@@ -2154,9 +2496,9 @@ __global__ void sigma_generic_kernel(SigmaArgs p, int chunk_atoms) {
     const int e = (int)(r % p.ne);
     const int k = (int)(r / p.ne);
     double re = 0.0, im = 0.0;
-    for (int q = 0; q < p.nqz; ++q) {
-      int kp = (k - q) % p.nkz;
-      if (kp < 0) kp += p.nkz;
+    for (int qi = 0; qi < p.nqz; ++qi) {
+      int q, kp;
+      q_order(k, qi, p.nkz, p.nqz, q, kp);
       for (int s = 0; s < p.nb; ++s) {
         const int lb = p.nbr[la * p.nb + s];
         const double2* mq = M + ((long long)((la * p.nb + s) * p.nqz + q) * p.nw) * no2;
@@ -2271,6 +2613,7 @@ cudaError_t launch_layout_transform(long long nkz, long long ne, long long na, l
 }
 
 cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
+  if (a.comb_kg > 0 && a.nqz > kOpBlocks) return cudaErrorInvalidValue;
   const size_t smem = (size_t)(12 + (a.fragment_order ? kOpBlocks : 0)) * a.no * a.no * sizeof(double2);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(build_operator_kernel,
@@ -2283,14 +2626,43 @@ cudaError_t launch_build_operator(const OperatorArgs& a, cudaStream_t st) {
 }
 
 // Sigma kernel selection (env SSE_SIGMA_KERNEL, read per launch):
-//   3 = TMA sliding-window, 12 warps x 3 row tiles (default when the offsets
-//       slide, i.e. non-decreasing with steps <= 1, as default_grid's do),
+//   4 = multi-momentum sliding window (default when the offsets slide, i.e. are
+//       non-decreasing with steps <= 1 as default_grid's are, and Nw >= 6),
+//   3 = single-momentum sliding window (Nw >= 12),
 //   1 = register-pipelined (used otherwise), 0 = simple.
-// All accumulate every output in the same (q, s, w, k-step) order, so they
+// All accumulate every output in the same (q_order, s, w, k-step) order, so they
 // agree bitwise (tested).
 static int sigma_kernel_choice() {
   const char* env = getenv("SSE_SIGMA_KERNEL");
-  return env ? atoi(env) : 3;
+  return env ? atoi(env) : 4;
+}
+
+template <int NO, int KG, bool COMB = false>
+static cudaError_t launch_kslide(SigmaArgs a, int chunk_atoms, int k_first, int groups, cudaStream_t st) {
+  using SG = KSlideGeom<NO, 12, 3, KG, COMB>;
+  a.ctas_per_ak = (a.rows + SG::kRows - 1) / SG::kRows;
+  a.k_first = k_first;
+  a.kgroups = groups;
+  const dim3 grid((unsigned)((long long)a.ctas_per_ak * groups * chunk_atoms), a.npol);
+  cudaError_t e = cudaFuncSetAttribute(sigma_dmma_kslide_kernel<NO, 12, 3, KG, COMB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG::kSmem);
+  if (e != cudaSuccess) return e;
+  sigma_dmma_kslide_kernel<NO, 12, 3, KG, COMB><<<grid, 12 * 32, SG::kSmem, st>>>(a);
+  return cudaGetLastError();
+}
+
+bool sigma_uses_combined(int no, int nw, int off_slide) {
+  if (no % 4 != 2 || no > kMaxDmmaOrb || !off_slide || nw < kKStages || nw > kMaxSlideNw) return false;
+  if (sigma_kernel_choice() != 4) return false;
+  const char* env = getenv("SSE_K3M_COMB");  // 0: per-momentum fragment vectors side by side
+  if (env && env[0] == '0') return false;
+  switch (no) {
+    case 2: return KSlideGeom<2, 12, 3, kCombKG, true>::kFits;
+    case 6: return KSlideGeom<6, 12, 3, kCombKG, true>::kFits;
+    case 10: return KSlideGeom<10, 12, 3, kCombKG, true>::kFits;
+    case 14: return KSlideGeom<14, 12, 3, kCombKG, true>::kFits;
+    default: return false;
+  }
 }
 
 template <int NO>
@@ -2301,29 +2673,54 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
     a.ctas_per_ak = (a.rows + rows_per_cta - 1) / rows_per_cta;
     return dim3((unsigned)((long long)a.ctas_per_ak * a.nkz * chunk_atoms), a.npol);
   };
-  const bool slide_ok = a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw && SlideGeom<NO, 12, 3>::kFits;
-  if (a.gather_ranks > 0 && !slide_ok) return cudaErrorNotSupported;  // peer gather: sliding-window K3 only
+  const bool slides = a.off_slide && a.nw <= kMaxSlideNw;
+  const bool kslide_ok = slides && a.nw >= kKStages && a.zeroM && KSlideGeom<NO, 12, 3, 3>::kFits;
+  const bool slide_ok = slides && a.nw >= kSlideStages && SlideGeom<NO, 12, 3>::kFits;
+  if (a.gather_ranks > 0 && !kslide_ok && !slide_ok) return cudaErrorNotSupported;  // peer gather: sliding K3 only
+  if (a.comb_kg > 0) {  // K2 wrote combined fragments (sigma_uses_combined)
+    if constexpr (NO % 4 == 2) {
+      if (!KSlideGeom<NO, 12, 3, kCombKG, true>::kFits || a.comb_kg != kCombKG) return cudaErrorInvalidValue;
+      note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,3,%d,comb>", NO, kCombKG);
+      return launch_kslide<NO, kCombKG, true>(a, chunk_atoms, 0, (a.nkz + kCombKG - 1) / kCombKG, st);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if ((choice == 4 || (a.gather_ranks > 0 && !slide_ok)) && kslide_ok) {
+    // momentum groups of kg, then one group of the remainder (no idle accumulators).  kg = 2 for
+    // No > 10: at 3 the 3 x 9 x 2 accumulator doubles of No = 12 exceed the 168-register budget of
+    // 12 warps (spills; paper shard 34.75 vs 35.12 TF/s at 2, 34.56 at 1); SSE_K3M_KG overrides
+    const char* kg_env = getenv("SSE_K3M_KG");
+    const int kg = kg_env && atoi(kg_env) >= 1 && atoi(kg_env) <= 3 ? atoi(kg_env) : (NO > 10 ? 2 : 3);
+    const int full = a.nkz / kg, rest = a.nkz % kg;
+    cudaError_t e = cudaSuccess;
+    if (full > 0) {
+      if (kg == 3) e = launch_kslide<NO, 3>(a, chunk_atoms, 0, full, st);
+      else if (kg == 2) e = launch_kslide<NO, 2>(a, chunk_atoms, 0, full, st);
+      else e = launch_kslide<NO, 1>(a, chunk_atoms, 0, full, st);
+    }
+    if (e == cudaSuccess && rest == 2) e = launch_kslide<NO, 2>(a, chunk_atoms, kg * full, 1, st);
+    if (e == cudaSuccess && rest == 1) e = launch_kslide<NO, 1>(a, chunk_atoms, kg * full, 1, st);
+    if (full > 0 && rest > 0)
+      note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,3,%d> (x%d momentum groups) + <%d,12,3,%d>", NO, kg, full, NO,
+                  rest);
+    else
+      note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,3,%d>", NO, full > 0 ? kg : rest);
+    return e;
+  }
   if (choice == 0 && a.gather_ranks == 0) {
     const dim3 grid = grid_for_rows(kRowsPerCta);
     note_kernel(1, "sigma_dmma_kernel<%d>", NO);
     sigma_dmma_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
-  } else if ((choice == 3 || a.gather_ranks > 0) && a.off_slide && a.nw >= kSlideStages && a.nw <= kMaxSlideNw) {
+  } else if ((choice >= 3 || a.gather_ranks > 0) && slide_ok) {
     // nw >= kSlideStages: the kSlideStages stages in flight span at most one
     // (q, s) segment boundary, so at most 2 * kTE + kSlideStages FIFO blocks
-    // are live (SlideGeom::kNeed <= kRing); shorter segments use the
-    // register-pipelined kernel.
-    if (SlideGeom<NO, 12, 3>::kFits) {
-      const dim3 grid = grid_for_rows(SlideGeom<NO, 12, 3>::kRows);
-      const size_t smem = SlideGeom<NO, 12, 3>::kSmem;
-      cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      note_kernel(1, "sigma_dmma_slide_kernel<%d,12,3>", NO);
-      sigma_dmma_slide_kernel<NO, 12, 3><<<grid, 12 * 32, smem, st>>>(a);
-      return cudaSuccess;
-    }
-    const dim3 grid = grid_for_rows(kRowsPerCta);
-    note_kernel(1, "sigma_dmma_pipe_kernel<%d>", NO);
-    sigma_dmma_pipe_kernel<NO><<<grid, kSigmaWarps * 32, 0, st>>>(a);
+    // are live (SlideGeom::kNeed <= kRing)
+    const dim3 grid = grid_for_rows(SlideGeom<NO, 12, 3>::kRows);
+    const size_t smem = SlideGeom<NO, 12, 3>::kSmem;
+    cudaFuncSetAttribute(sigma_dmma_slide_kernel<NO, 12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    note_kernel(1, "sigma_dmma_slide_kernel<%d,12,3>", NO);
+    sigma_dmma_slide_kernel<NO, 12, 3><<<grid, 12 * 32, smem, st>>>(a);
   } else {
     const dim3 grid = grid_for_rows(kRowsPerCta);
     note_kernel(1, "sigma_dmma_pipe_kernel<%d>", NO);

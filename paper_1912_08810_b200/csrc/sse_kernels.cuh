@@ -51,7 +51,22 @@ struct OperatorArgs {
   int chunk_atoms;
   int fragment_order;     // 1: DMMA fragment order, 0: compact [p][n]
   int npol;               // polarities to process (1 or 2)
+  // combined multi-momentum fragments (comb_kg > 0, see comb_geom): per (atom, s, kp, group,
+  // w) ONE fragment vector holding M[q_k = (k - kp) mod Nkz] of the group's comb_kg output
+  // momenta side by side in N (zero where q_k >= Nqz or k >= Nkz)
+  int comb_kg, nkz;
 };
+
+// Combined-fragment geometry of the multi-momentum K3 (No % 4 == 2, e.g. No = 10): N' =
+// kg * 2No padded to 8 * ntc (10: 60 -> 64 instead of 3 x 24 = 72), fvc double2 per lane.
+struct CombGeom {
+  int ntc, frc, fvc;
+};
+__host__ __device__ constexpr CombGeom comb_geom(int no, int kg) {
+  return CombGeom{(kg * 2 * no + 7) / 8, frag_geom(no).ksteps * ((kg * 2 * no + 7) / 8),
+                  (frag_geom(no).ksteps * ((kg * 2 * no + 7) / 8) + 1) / 2};
+}
+constexpr int kCombKG = 3;  // momenta per combined group
 
 // Peer scatter of Sigma: when scatter_ranks > 0 the block
 // (k, E, atom) is written straight into the (k,E)-point layout buffer of the
@@ -84,6 +99,11 @@ struct SigmaArgs {
   // point owner r; nbr holds global atom ids
   int gather_ranks;
   const double2* G_rank[2][kMaxScatter];
+  // multi-momentum K3 (set by launch_sigma): momentum groups of this launch start at k_first,
+  // kgroups of them; zeroM = one zero M-fragment vector (B of an invalid (k, kp) pair)
+  int k_first, kgroups;
+  const double2* zeroM;
+  int comb_kg;            // > 0: M holds combined fragments (OperatorArgs::comb_kg)
 };
 
 // Phonon self-energy Pi (sse.py:332-428), chains in the V form
@@ -173,8 +193,16 @@ cudaError_t launch_fill_synthetic(uint64_t seed, uint32_t tensor_id, long long a
 // 3 preprocess_D, 4 Pi operand build, 5 Pi chains, 6 Pi assembly); "" if none.
 const char* last_kernel_name(int kind);
 
+// Whether the Sigma launch for these shapes uses the multi-momentum K3 with combined fragments
+// (K2 must then write them): No % 4 == 2, offsets sliding, Nw in [6, 1024], SSE_SIGMA_KERNEL=4.
+bool sigma_uses_combined(int no, int nw, int off_slide);
+
 // Bytes of the per-chunk operator buffer (one polarity).
-inline size_t operator_bytes(int no, int nb, int nqz, int nw, int chunk_atoms) {
+inline size_t operator_bytes(int no, int nb, int nqz, int nw, int chunk_atoms, int comb_kg = 0, int nkz = 1) {
+  if (comb_kg > 0) {
+    const int groups = (nkz + comb_kg - 1) / comb_kg;
+    return (size_t)comb_geom(no, comb_kg).fvc * 32 * 16 * nb * nkz * groups * nw * chunk_atoms;
+  }
   size_t per = (no <= kMaxDmmaOrb) ? (size_t)frag_geom(no).fv * 32 : (size_t)no * no;
   return per * 16 * (size_t)nb * nqz * nw * chunk_atoms;
 }

@@ -77,6 +77,24 @@ def alg_flops(n_kz, n_qz, n_e, n_a, n_b, n_o, offsets) -> int:
     return 16 * n_a * n_b * n_kz * n_qz * n_o**3 * terms
 
 
+def _alloc_out(shape) -> Array:
+    """A zero-filled complex128 host array for a call's output (the reference allocates its outputs
+    with np.zeros, sse.py:146-147).  Large outputs are anonymous mappings with transparent huge pages
+    off: the grid-major [Nkz, NE, NA, No, No] output is written one atom-column chunk at a time, so
+    with 2 MB pages the FIRST chunk would fault (and the kernel zero) one huge page per (k, E) row --
+    8.5 GB at paper before any other chunk could be staged; 4 KB pages spread the page-zeroing over
+    the chunks, under the GPU compute.  SSE_OUT_ALLOC=numpy keeps np.zeros."""
+    nbytes = int(np.prod(shape)) * 16
+    if nbytes < (1 << 30) or os.environ.get("SSE_OUT_ALLOC", "") == "numpy":
+        return np.zeros(shape, dtype=np.complex128)
+    import mmap
+
+    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    if hasattr(mmap, "MADV_NOHUGEPAGE"):
+        buf.madvise(mmap.MADV_NOHUGEPAGE)
+    return np.frombuffer(buf, dtype=np.complex128).reshape(shape)
+
+
 def _f64(arr: Array) -> Array:
     return np.ascontiguousarray(arr, dtype=np.complex128)
 
@@ -136,8 +154,8 @@ def sse_sigma(
         for stage, n in sigma_tallies(var, n_kz, n_qz, n_e, n_w, n_a, n_b, n_o).items():
             counter.stages[stage] = counter.stages.get(stage, 0) + n
 
-    out_l = np.zeros(g_l.shape, dtype=np.complex128)
-    out_g = np.zeros(g_g.shape, dtype=np.complex128)
+    out_l = _alloc_out(g_l.shape)
+    out_g = _alloc_out(g_g.shape)
     if out_l.size == 0 or dc.lesser.size == 0:
         return SelfEnergyTensor(lesser=out_l, greater=out_g)
 
@@ -338,8 +356,8 @@ def sse_phase(
             if o.shape != shape or o.dtype != np.complex128 or not o.flags.c_contiguous:
                 raise ValueError(f"out arrays must be C-contiguous complex128 of shape {shape}")
     else:
-        sig_l = np.zeros(g_l.shape, dtype=np.complex128)
-        sig_g = np.zeros(g_l.shape, dtype=np.complex128)
+        sig_l = _alloc_out(g_l.shape)
+        sig_g = _alloc_out(g_l.shape)
         pi_l = np.zeros(d_l.shape, dtype=np.complex128)
         pi_g = np.zeros(d_l.shape, dtype=np.complex128)
     if g_l.size == 0 or d_l.size == 0:

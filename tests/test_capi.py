@@ -52,9 +52,11 @@ def test_library_is_sm100a_only():
 
 
 @pytest.mark.parametrize("kernel, dmma", [
-    ("_ZN3sse22sigma_dmma_pipe_kernelILi12EEEvNS_9SigmaArgsE", 108),  # production K3 (2 stages x 54)
+    ("_ZN3sse24sigma_dmma_kslide_kernelILi12ELi12ELi3ELi2ELb0EEEvNS_9SigmaArgsE", 108),  # production K3m (2 momenta)
+    ("_ZN3sse24sigma_dmma_kslide_kernelILi10ELi12ELi3ELi3ELb1EEEvNS_9SigmaArgsE", 120),  # K3m, No=10 combined
+    ("_ZN3sse22sigma_dmma_pipe_kernelILi12EEEvNS_9SigmaArgsE", 108),  # register-pipelined K3 (2 stages x 54)
     ("_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", 54),        # simple K3
-    ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELi3EEEvNS_9SigmaArgsE", 54),  # TMA sliding-window K3
+    ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELi3EEEvNS_9SigmaArgsE", 54),  # single-momentum sliding-window K3
     ("_ZN3sse15pi_dmma3_kernelILb0ELi12ELi4EEEvNS_6PiArgsEi", 108),            # Pi K6 v3 (paper shapes)
     ("_ZN3sse15pi_dmma4_kernelILi12ELi4ELi4ELi3ELi4ELb1EEEvNS_6PiArgsEi", 216),  # Pi K6 v4 split (default)
     ("_ZN3sse20pi_build_dmma_kernelILi12EEEvNS_11PiBuildArgsE", 72),            # Pi K5 v2

@@ -124,7 +124,7 @@ def test_all_sigma_kernels_bitwise(monkeypatch, name):
     c = load_case(name)
     args = (GreensTensor(c.g_l, c.g_g), _dc(c), c.dh, NeighborMap(c.idx), _grid(c))
     outs = []
-    for choice in ("0", "1", "3"):
+    for choice in ("0", "1", "3", "4"):
         monkeypatch.setenv("SSE_SIGMA_KERNEL", choice)
         outs.append(sse_sigma(SseVariant.BATCHED_FUSED, *args))
     for o in outs[1:]:
@@ -159,7 +159,7 @@ def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a, n_b):
     off, wt = np.array(grid.offsets), np.array(grid.weights)
     ref_l, ref_g = orc.sigma_batched_fused(g_l, g_g, dc.lesser, dc.greater, dh, nmap.idx, off, wt)
     outs = []
-    for choice in ("0", "1", "3"):
+    for choice in ("0", "1", "3", "4"):
         monkeypatch.setenv("SSE_SIGMA_KERNEL", choice)
         out = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(g_l, g_g), dc, dh, nmap, grid)
         assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice

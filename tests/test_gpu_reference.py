@@ -59,7 +59,7 @@ def test_patched_entry_points_route_to_libsse(nf):
     got = _patched(lambda: nf.sse.sse_sigma(nf.sse.SseVariant.BATCHED_FUSED, g, dc, dev.dH, nmap, grid))
     assert type(got) is nf.gf.SelfEnergyTensor
     assert _dev(got, ref) <= TOL
-    assert _lib.kernel_name("sigma").startswith("sigma_dmma_slide_kernel<12")
+    assert _lib.kernel_name("sigma").startswith("sigma_dmma_kslide_kernel<12")
     ref_pi = nf.sse.sse_pi(g, dev.dH, nmap, grid, params.n_qz)
     got_pi = _patched(lambda: nf.sse.sse_pi(g, dev.dH, nmap, grid, params.n_qz))
     assert _dev(got_pi, ref_pi) <= TOL
