@@ -210,6 +210,22 @@ int sse_ipc_handle(sse_ctx* ctx, void* dptr, unsigned char* handle);
 int sse_ipc_open(sse_ctx* ctx, const unsigned char* handle, void** out);
 int sse_ipc_close(sse_ctx* ctx, void* ptr);
 
+/* Multi-GPU Sigma inside the library, one process: the context's n_gpus devices
+ * split the atoms in contiguous ceil-division chunks (distsim.py:117-120).  sse_multi_layout
+ * writes bounds[4*i .. 4*i+3] = (lo, hi, glo, ghi) of device i: it owns atoms [lo, hi) and holds
+ * the atom-major G slab [glo, ghi) (owned + the +-reach halo).  sse_sigma_multi takes per-device
+ * device pointers (G_*[i] [ghi-glo, Nkz, NE, No, No] with the OWNED atoms filled, Dc_*[i]
+ * [Nqz, Nw, hi-lo, NB, 3, 3], dH[i] [hi-lo, NB, 3, No, No], Sig_*[i] [hi-lo, Nkz, NE, No, No]),
+ * fills every halo from the owning devices with one grouped NCCL send/recv (communicators from
+ * ncclCommInitAll over the context's devices, created on first use; libnccl.so.2 is loaded at
+ * run time) and runs the Sigma kernels of all devices concurrently.  nmap: HOST [NA, NB].
+ * Returns 3 (SSE_ECOMM) on an NCCL failure.  Asynchronous unless t != NULL (then max over devices). */
+int sse_multi_layout(sse_ctx* ctx, const sse_dims* d, const int64_t* nmap, int64_t* bounds);
+int sse_sigma_multi(sse_ctx* ctx, const sse_dims* d, double* const* G_l, double* const* G_g,
+                    const double* const* Dc_l, const double* const* Dc_g, const double* const* dH,
+                    const int64_t* nmap, const int64_t* off, const double* wt, double* const* Sig_l,
+                    double* const* Sig_g, sse_timing* t);
+
 /* Device-resident Pi of an owned atom range: g = slab with the owned atoms and
  * all their neighbours; dH [out.natoms, NB, 3, No, No]; nmap HOST [out.natoms, NB]
  * (global ids); Pi_* device [Nqz, Nw, out.natoms, NB+1, 3, 3]. */

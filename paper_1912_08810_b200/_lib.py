@@ -45,6 +45,8 @@ EXPORTED = (
     "sse_profile_begin",
     "sse_profile_end",
     "sse_kernel_name",
+    "sse_multi_layout",
+    "sse_sigma_multi",
 )
 
 PROF_KINDS = ("operator", "sigma", "layout", "preprocess", "pi_build", "pi", "pi_assemble")
@@ -148,6 +150,8 @@ def load() -> ctypes.CDLL:
         lib.sse_fill_synthetic.argtypes = [
             _P, ctypes.c_uint64, ctypes.c_uint32, i64, i64, i64, i64, i64, i64, dbl, _P, _P,
         ]
+        lib.sse_multi_layout.argtypes = [_P, pdims, _P, _P]
+        lib.sse_sigma_multi.argtypes = [_P, pdims] + [_P] * 5 + [_P, _P, _P] + [_P, _P, ptim]
         lib.sse_kernel_name.argtypes = [i32]
         lib.sse_kernel_name.restype = ctypes.c_char_p
         for name in EXPORTED:

@@ -11,6 +11,8 @@
 // Multi-GPU: contiguous atom chunks per device (distsim.py:117-120), one host
 // thread per device; each device reads its halo straight from host memory.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -126,7 +128,11 @@ class HostPool {
 
  private:
   HostPool() {
+    // all hardware threads, shared between the processes of one node when launched by torchrun
+    // (LOCAL_WORLD_SIZE ranks copy at once: oversubscribing the cores only adds switching)
     int n = (int)std::thread::hardware_concurrency();
+    if (const char* lws = getenv("LOCAL_WORLD_SIZE"))
+      if (atoi(lws) > 1) n = std::max(2, n / atoi(lws));
     if (const char* env = getenv("SSE_HOST_THREADS")) n = atoi(env);
     n = std::max(1, std::min(n, 64));
     for (int i = 0; i + 1 < n; ++i) workers_.emplace_back([this] { loop(); });
@@ -216,11 +222,52 @@ struct DevState {
 
 }  // namespace
 
+// NCCL, resolved at run time (dlopen "libnccl.so.2": the copy torch already loaded, else the
+// system one), so libsse has no link-time NCCL dependency and single-GPU use never touches it.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
 struct sse_ctx {
   std::vector<DevState> devs;
+  std::vector<ncclComm_t> comms;  // one per device (ncclCommInitAll), created on first multi-GPU call
 };
 
 namespace {
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.CommInitAll = (decltype(api.CommInitAll))dlsym(h, "ncclCommInitAll");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+  api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.CommInitAll && api.CommDestroy && api.GroupStart && api.GroupEnd && api.Send && api.Recv &&
+           api.GetErrorString;
+  return api;
+}
+
+#define NC(x)                                                                                            \
+  do {                                                                                                   \
+    ncclResult_t r_ = (x);                                                                               \
+    if (r_ != ncclSuccess) return fail(SSE_ECOMM, "NCCL error %s: %s", nc.GetErrorString(r_), #x);       \
+  } while (0)
 
 // Record a profiled launch: `launch` is a callable returning cudaError_t.
 template <class F>
@@ -1139,6 +1186,11 @@ int sse_ctx_create_on(int device, sse_ctx** out) {
 
 void sse_ctx_destroy(sse_ctx* ctx) {
   if (!ctx) return;
+  if (!ctx->comms.empty()) {
+    NcclApi& nc = nccl_api();
+    for (ncclComm_t c : ctx->comms)
+      if (c && nc.ok) nc.CommDestroy(c);
+  }
   for (auto& d : ctx->devs) destroy_dev(d);
   delete ctx;
 }
@@ -1428,6 +1480,129 @@ int sse_ipc_close(sse_ctx* ctx, void* ptr) {
   if (!ctx || ctx->devs.size() != 1) return fail(SSE_EINVAL, "invalid IPC close");
   CU(cudaSetDevice(ctx->devs[0].device));
   if (ptr) CU(cudaIpcCloseMemHandle(ptr));
+  return SSE_OK;
+}
+
+// Multi-GPU inside the library (one process): atom chunks per context device
+// (distsim.py:117-120), each device's atom-major G slab = owned atoms + the +-reach halo.
+static void multi_bounds(const sse_dims* d, const int64_t* nmap, int nd, std::vector<int64_t>& b) {
+  b.assign((size_t)nd * 4, 0);
+  const int64_t per = (d->na + nd - 1) / nd;
+  for (int i = 0; i < nd; ++i) {
+    const int64_t lo = std::min<int64_t>(i * per, d->na), hi = std::min<int64_t>((i + 1) * per, d->na);
+    int64_t glo = lo, ghi = hi;
+    for (int64_t x = lo * d->nb; x < hi * d->nb; ++x) {
+      glo = std::min(glo, nmap[x]);
+      ghi = std::max(ghi, nmap[x] + 1);
+    }
+    b[4 * i] = lo;
+    b[4 * i + 1] = hi;
+    b[4 * i + 2] = glo;
+    b[4 * i + 3] = ghi;
+  }
+}
+
+int sse_multi_layout(sse_ctx* ctx, const sse_dims* d, const int64_t* nmap, int64_t* bounds) {
+  if (!ctx || !bounds || !nmap) return fail(SSE_EINVAL, "NULL argument");
+  CHECK(validate_dims(d));
+  for (int64_t x = 0; x < d->na * d->nb; ++x)
+    if (nmap[x] < 0 || nmap[x] >= d->na)
+      return fail(SSE_EINVAL, "neighbor index %lld outside [0, %lld)", (long long)nmap[x], (long long)d->na);
+  std::vector<int64_t> b;
+  multi_bounds(d, nmap, (int)ctx->devs.size(), b);
+  std::memcpy(bounds, b.data(), b.size() * sizeof(int64_t));
+  return SSE_OK;
+}
+
+int sse_sigma_multi(sse_ctx* ctx, const sse_dims* d, double* const* G_l, double* const* G_g,
+                    const double* const* Dc_l, const double* const* Dc_g, const double* const* dH,
+                    const int64_t* nmap, const int64_t* off, const double* wt, double* const* Sig_l,
+                    double* const* Sig_g, sse_timing* t) {
+  if (!ctx || ctx->devs.empty()) return fail(SSE_EINVAL, "context is NULL");
+  CHECK(validate_dims(d));
+  CHECK(validate_grid(d, off, wt));
+  if (!G_l || !G_g || !Dc_l || !Dc_g || !dH || !nmap || !Sig_l || !Sig_g) return fail(SSE_EINVAL, "NULL tensor pointer");
+  const int nd = (int)ctx->devs.size();
+  for (int i = 0; i < nd; ++i)
+    if (!G_l[i] || !G_g[i] || !Dc_l[i] || !Dc_g[i] || !dH[i] || !Sig_l[i] || !Sig_g[i])
+      return fail(SSE_EINVAL, "NULL tensor pointer for device %d", i);
+  for (int64_t x = 0; x < d->na * d->nb; ++x)
+    if (nmap[x] < 0 || nmap[x] >= d->na)
+      return fail(SSE_EINVAL, "neighbor index %lld outside [0, %lld)", (long long)nmap[x], (long long)d->na);
+  std::vector<int64_t> b;
+  multi_bounds(d, nmap, nd, b);
+  const int64_t per = (d->na + nd - 1) / nd;
+  const size_t blk = (size_t)d->nkz * d->ne * d->norb * d->norb * 16;  // bytes per atom and polarity
+  // 1. halo exchange: every device receives its halo atoms from their owners (NCCL over NVLink)
+  if (nd > 1) {
+    NcclApi& nc = nccl_api();
+    if (!nc.ok) return fail(SSE_ECOMM, "NCCL (libnccl.so.2) could not be loaded");
+    if (ctx->comms.empty()) {
+      std::vector<int> devlist(nd);
+      for (int i = 0; i < nd; ++i) devlist[i] = ctx->devs[i].device;
+      ctx->comms.assign(nd, nullptr);
+      NC(nc.CommInitAll(ctx->comms.data(), nd, devlist.data()));
+    }
+    for (int i = 0; i < nd; ++i) {  // the previous call's use of the slabs / scratch is ordered first
+      CU(cudaSetDevice(ctx->devs[i].device));
+      CHECK(scratch_enter(ctx->devs[i], ctx->devs[i].stream));
+    }
+    double* const* Gp[2] = {G_l, G_g};
+    NC(nc.GroupStart());
+    for (int i = 0; i < nd; ++i) {
+      const int64_t lo = b[4 * i], hi = b[4 * i + 1], glo = b[4 * i + 2], ghi = b[4 * i + 3];
+      for (int64_t a0 = glo; a0 < ghi;) {
+        if (a0 >= lo && a0 < hi) {
+          a0 = hi;
+          continue;
+        }
+        const int j = (int)(a0 / per);
+        int64_t a1 = std::min<int64_t>(a0 < lo ? lo : ghi, std::min<int64_t>((j + 1) * per, d->na));
+        const int64_t jglo = b[4 * j + 2];
+        for (int pol = 0; pol < 2; ++pol) {
+          NC(nc.Recv((char*)Gp[pol][i] + (a0 - glo) * blk, (a1 - a0) * blk, ncclChar, j, ctx->comms[i],
+                     ctx->devs[i].stream));
+          NC(nc.Send((const char*)Gp[pol][j] + (a0 - jglo) * blk, (a1 - a0) * blk, ncclChar, i, ctx->comms[j],
+                     ctx->devs[j].stream));
+        }
+        a0 = a1;
+      }
+    }
+    NC(nc.GroupEnd());
+  }
+  // 2. Sigma of each device's owned atoms on its own stream (all devices run concurrently)
+  if (t) {
+    std::memset(t, 0, sizeof(*t));
+    t->flops = alg_flops(d, off, d->na);
+    t->n_devices = nd;
+  }
+  int launches = 0;
+  for (int i = 0; i < nd; ++i) {
+    DevState& ds = ctx->devs[i];
+    CU(cudaSetDevice(ds.device));
+    cudaStream_t st = ds.stream;
+    if (nd == 1) CHECK(scratch_enter(ds, st));
+    if (t) CU(cudaEventRecord(ds.ev[0], st));
+    const int64_t lo = b[4 * i], hi = b[4 * i + 1], glo = b[4 * i + 2], ghi = b[4 * i + 3];
+    if (hi <= lo) continue;
+    const sse_slab gs{glo, ghi - glo, 1, 0}, os{lo, hi - lo, 1, 0};
+    const DevPtrs p{(const double2*)G_l[i], (const double2*)G_g[i], (const double2*)Dc_l[i], (const double2*)Dc_g[i],
+                    (const double2*)dH[i], (double2*)Sig_l[i], (double2*)Sig_g[i]};
+    CHECK(sigma_on_device(ds, d, gs, os, p, nmap + lo * d->nb, off, wt, st, &launches));
+    CHECK(scratch_leave(ds, st));
+    if (t) CU(cudaEventRecord(ds.ev[1], st));
+  }
+  if (t) {
+    for (int i = 0; i < nd; ++i) {
+      DevState& ds = ctx->devs[i];
+      if (b[4 * i + 1] <= b[4 * i]) continue;
+      CU(cudaSetDevice(ds.device));
+      CU(cudaEventSynchronize(ds.ev[1]));
+      t->total_ms = std::max(t->total_ms, (double)elapsed(ds.ev[0], ds.ev[1]));
+    }
+    t->sigma_ms = t->total_ms;
+    t->kernel_launches = launches;
+  }
   return SSE_OK;
 }
 

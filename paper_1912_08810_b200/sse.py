@@ -757,6 +757,53 @@ def sse_phase_device(
     return tim.as_dict() if sync_timing else None
 
 
+def multi_layout(n_gpus: int, nmap_idx: Array) -> list[tuple[int, int, int, int]]:
+    """(lo, hi, glo, ghi) per device of the in-library multi-GPU split (``sse_multi_layout``):
+    device i owns atoms [lo, hi) and holds the atom-major G slab [glo, ghi) (owned + halo)."""
+    idx = np.ascontiguousarray(nmap_idx, dtype=np.int64)
+    n_a, n_b = idx.shape
+    dims = _lib.SseDims(1, 1, 1, 1, n_a, n_b, 1)
+    bounds = np.zeros(4 * n_gpus, dtype=np.int64)
+    ctx = _lib.context(n_gpus=n_gpus)
+    _lib.check(_lib.load().sse_multi_layout(ctx.handle, ctypes.byref(dims), _ptr(idx), _ptr(bounds)))
+    return [tuple(int(x) for x in bounds[4 * i:4 * i + 4]) for i in range(n_gpus)]
+
+
+def sigma_multi(g_l, g_g, dc_l, dc_g, dh, nmap_idx: Array, grid, out_l, out_g, *, sync_timing: bool = False):
+    """Sigma over all devices of this process in ONE library call (``sse_sigma_multi``): lists with
+    one tensor per device i (on cuda:i) in the layout of :func:`multi_layout` -- g_* [ghi-glo, Nkz,
+    NE, No, No] with the owned atoms filled (the library fills the halos from the owning devices
+    by NCCL), dc_* [Nqz, Nw, hi-lo, NB, 3, 3], dh [hi-lo, NB, 3, No, No], out_* [hi-lo, Nkz, NE, No, No]."""
+    n = len(g_l)
+    idx = np.ascontiguousarray(nmap_idx, dtype=np.int64)
+    n_a, n_b = idx.shape
+    lay = multi_layout(n, idx)
+    _, n_kz, n_e, n_o = (int(x) for x in g_l[0].shape[:4])
+    n_qz, n_w = int(dc_l[0].shape[0]), int(dc_l[0].shape[1])
+    import torch
+
+    for i, (lo, hi, glo, ghi) in enumerate(lay):
+        dev = torch.device("cuda", i)
+        _check_dev(g_l[i], (ghi - glo, n_kz, n_e, n_o, n_o), f"g_l[{i}]", dev)
+        _check_dev(g_g[i], (ghi - glo, n_kz, n_e, n_o, n_o), f"g_g[{i}]", dev)
+        _check_dev(dc_l[i], (n_qz, n_w, hi - lo, n_b, 3, 3), f"dc_l[{i}]", dev)
+        _check_dev(dc_g[i], (n_qz, n_w, hi - lo, n_b, 3, 3), f"dc_g[{i}]", dev)
+        _check_dev(dh[i], (hi - lo, n_b, 3, n_o, n_o), f"dh[{i}]", dev)
+        _check_dev(out_l[i], (hi - lo, n_kz, n_e, n_o, n_o), f"out_l[{i}]", dev)
+        _check_dev(out_g[i], (hi - lo, n_kz, n_e, n_o, n_o), f"out_g[{i}]", dev)
+    fmap = grid.frequency_map
+    offs = np.array([int(fmap[w][0]) for w in range(n_w)], dtype=np.int64)
+    wts = np.array([float(fmap[w][1]) for w in range(n_w)], dtype=np.float64)
+    arr = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])  # noqa: E731
+    dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
+    tim = _lib.SseTiming()
+    ctx = _lib.context(n_gpus=n)
+    _lib.check(_lib.load().sse_sigma_multi(
+        ctx.handle, ctypes.byref(dims), arr(g_l), arr(g_g), arr(dc_l), arr(dc_g), arr(dh), _ptr(idx), _ptr(offs),
+        _ptr(wts), arr(out_l), arr(out_g), ctypes.byref(tim) if sync_timing else None))
+    return tim.as_dict() if sync_timing else None
+
+
 def layout_transform(src, dst, to_atom_major: bool, stream=None) -> None:
     """K1 (sse.py:48-55): [Nkz,NE,NA,No,No] <-> [NA,Nkz,NE,No,No] on the GPU.
 

@@ -444,3 +444,35 @@ def test_host_staging_ring_bitwise(monkeypatch, mode):
                                   grid.offsets, grid.weights, o[0], o[1], n_a=p.n_A, g_atom0=0, out_atom0=0)
         assert tim["staged"] == 0
         assert np.array_equal(o[0].numpy(), ref[0]) and np.array_equal(o[1].numpy(), ref[1])
+
+
+def test_in_library_multi_gpu_sigma_bitwise():
+    """sse_sigma_multi: one call over all devices of the process, halos exchanged by the library
+    with NCCL (ncclCommInitAll) -- equal bit for bit to the single-device call; on one GPU it
+    runs the same path without communication."""
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    n = torch.cuda.device_count()
+    c = load_case("slide_orb12_s9")
+    p = c.p
+    dc = _dc(c)
+    full = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(c.g_l, c.g_g), dc, c.dh, NeighborMap(c.idx), _grid(c))
+    for ngpu in sorted({1, min(n, 2), n}):
+        lay = dev.multi_layout(ngpu, c.idx)
+        cu = lambda a, i: torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{i}")  # noqa: E731
+        g_l, g_g, dl, dg, dh, ol, og = [], [], [], [], [], [], []
+        for i, (lo, hi, glo, ghi) in enumerate(lay):
+            for src, dst in ((c.g_l, g_l), (c.g_g, g_g)):
+                slab = np.full((ghi - glo, p.n_kz, p.n_E, p.n_orb, p.n_orb), np.nan, dtype=np.complex128)
+                slab[lo - glo:hi - glo] = np.moveaxis(src[:, :, lo:hi], 2, 0)  # owned atoms only: halo by NCCL
+                dst.append(cu(slab, i))
+            dl.append(cu(dc.lesser[:, :, lo:hi], i))
+            dg.append(cu(dc.greater[:, :, lo:hi], i))
+            dh.append(cu(c.dh[lo:hi], i))
+            ol.append(torch.zeros((hi - lo, p.n_kz, p.n_E, p.n_orb, p.n_orb), dtype=torch.complex128, device=f"cuda:{i}"))
+            og.append(torch.zeros_like(ol[-1]))
+        dev.sigma_multi(g_l, g_g, dl, dg, dh, c.idx, _grid(c), ol, og, sync_timing=True)
+        for i, (lo, hi, _, _) in enumerate(lay):
+            assert np.array_equal(np.moveaxis(ol[i].cpu().numpy(), 0, 2), full.lesser[:, :, lo:hi]), (ngpu, i)
+            assert np.array_equal(np.moveaxis(og[i].cpu().numpy(), 0, 2), full.greater[:, :, lo:hi]), (ngpu, i)
