@@ -1984,16 +1984,24 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   unsigned* rel = reinterpret_cast<unsigned*>(empty + kPi3Slots);  // releases per slot
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx = blockIdx.x;
-  const int q = bx % p.nqz;
-  bx /= p.nqz;
+  const int m_tiles = (p.nw + 7) / 8;
+  const int n_groups = ((2 * ncol + 7) / 8 + kPi3NT - 1) / kPi3NT;
+  // q_in_warps (few lag tiles, e.g. Nw = 16: 2 tiles of 9 warps): the CTA serves every q, warp =
+  // (q, tile); its warps share the V stages (V depends on (k, E) only) and read their own G1 rows
+  int q, wg;
+  if (p.q_in_warps) {
+    q = warp / (m_tiles * n_groups);
+    wg = warp % (m_tiles * n_groups);
+  } else {
+    q = bx % p.nqz;
+    bx /= p.nqz;
+    wg = blockIdx.y * kPiWarps + warp;
+  }
   const int ec = bx % p.echunks;
   bx /= p.echunks;
   const int pol = bx % 2;
   const int la = bx / 2;
-  const int m_tiles = (p.nw + 7) / 8;
-  const int n_groups = ((2 * ncol + 7) / 8 + kPi3NT - 1) / kPi3NT;
-  const int wg = blockIdx.y * kPiWarps + warp;
-  const bool active = wg < m_tiles * n_groups;  // idle warps still take part in the barriers
+  const bool active = wg < m_tiles * n_groups && q < p.nqz;  // idle warps still take part in the barriers
   const int mt = active ? wg % m_tiles : 0, ng = active ? wg / m_tiles : 0;
   const int pcol = lane & 3;
 
@@ -2895,8 +2903,15 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
       const int groups = ((a.nw + 7) / 8) * (((2 * a.ncol + 7) / 8 + kPi3NT - 1) / kPi3NT);
-      note_kernel(5, fixed ? "pi_dmma3_kernel<%d,12,4>" : "pi_dmma3_kernel<%d,0,0>", (int)last);
-      kern<<<dim3(gx, (unsigned)((groups + kPiWarps - 1) / kPiWarps)), kPiWarps * 32, smem, st>>>(a, chunk_atoms);
+      PiArgs b = a;
+      // few lag tiles (e.g. the small config: 2) -> one CTA serves every q: 6 of 9 warps busy, not 2
+      b.q_in_warps = a.peer.ranks == 0 && groups * a.nqz <= kPiWarps;
+      note_kernel(5, fixed ? "pi_dmma3_kernel<%d,12,4>%s" : "pi_dmma3_kernel<%d,0,0>%s", (int)last,
+                  b.q_in_warps ? " (q in warps)" : "");
+      if (b.q_in_warps)
+        kern<<<dim3(gx / (unsigned)a.nqz, 1u), kPiWarps * 32, smem, st>>>(b, chunk_atoms);
+      else
+        kern<<<dim3(gx, (unsigned)((groups + kPiWarps - 1) / kPiWarps)), kPiWarps * 32, smem, st>>>(b, chunk_atoms);
       break;
     }
     case 2:

@@ -161,6 +161,7 @@ struct PiArgs {
   long long g_atom_of_chunk0;  // G-slab index of the chunk's first output atom
   int swz;                     // V column swizzle (must match K5's)
   PeerGather peer;             // ranks > 0: G1 from the point owners (K6 v3 / v4 only)
+  int q_in_warps;              // K6 v3: the CTA serves every q (warp = (q, lag tile)), set by launch_pi
 };
 struct PiAssembleArgs {
   const double2* partial;

@@ -99,6 +99,7 @@ def test_pi_hoisting_is_value_neutral():
 @pytest.mark.parametrize("n_kz, n_qz, n_e, n_w, n_a, n_b, n_o", [
     (3, 3, 30, 10, 6, 4, 12),   # the No of the paper configs
     (2, 2, 17, 5, 5, 4, 10),    # No = 10 (small config), 5 atoms (odd) with NB even
+    (3, 3, 40, 16, 6, 4, 10),   # the small config's Nw = 16 / Nqz = 3: K6 v3 with q in warps (6 of 9 warps)
     (4, 3, 9, 3, 4, 1, 5),      # NB = 1 (XOR partner slot), Nqz < Nkz
     (2, 2, 13, 5, 5, 2, 8),     # No = 8 (DMMA operand build), NB = 2
     (2, 1, 9, 4, 5, 4, 16),     # No = 16 (largest DMMA orbital count)
