@@ -342,7 +342,7 @@ def e2e_phase(args, p, grid, idx, rank, world, local_rank, want_digest) -> dict:
                     else None)
 
             def call(tim):
-                o = outs if pinned else [np.zeros(shape, dtype=np.complex128) for _ in range(2)]
+                o = outs if pinned else [dev.alloc_host(shape) for _ in range(2)]
                 tim.update(dev.sigma_host_slab(g[0], g[1], dc[0], dc[1], dh, rows, offs, wts, o[0], o[1],
                                                n_a=p.n_A, g_atom0=glo, out_atom0=lo, device=local_rank))
                 return o[0], o[1]

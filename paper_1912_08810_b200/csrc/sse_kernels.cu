@@ -2645,17 +2645,17 @@ static int sigma_kernel_choice() {
   return env ? atoi(env) : 4;
 }
 
-template <int NO, int KG, bool COMB = false>
+template <int NO, int KG, bool COMB = false, int NW = 12>
 static cudaError_t launch_kslide(SigmaArgs a, int chunk_atoms, int k_first, int groups, cudaStream_t st) {
-  using SG = KSlideGeom<NO, 12, 3, KG, COMB>;
+  using SG = KSlideGeom<NO, NW, 3, KG, COMB>;
   a.ctas_per_ak = (a.rows + SG::kRows - 1) / SG::kRows;
   a.k_first = k_first;
   a.kgroups = groups;
   const dim3 grid((unsigned)((long long)a.ctas_per_ak * groups * chunk_atoms), a.npol);
-  cudaError_t e = cudaFuncSetAttribute(sigma_dmma_kslide_kernel<NO, 12, 3, KG, COMB>,
+  cudaError_t e = cudaFuncSetAttribute(sigma_dmma_kslide_kernel<NO, NW, 3, KG, COMB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG::kSmem);
   if (e != cudaSuccess) return e;
-  sigma_dmma_kslide_kernel<NO, 12, 3, KG, COMB><<<grid, 12 * 32, SG::kSmem, st>>>(a);
+  sigma_dmma_kslide_kernel<NO, NW, 3, KG, COMB><<<grid, NW * 32, SG::kSmem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -2701,6 +2701,14 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
     const int kg = kg_env && atoi(kg_env) >= 1 && atoi(kg_env) <= 3 ? atoi(kg_env) : (NO > 10 ? 2 : 3);
     const int full = a.nkz / kg, rest = a.nkz % kg;
     cudaError_t e = cudaSuccess;
+    const char* nw_env = getenv("SSE_K3M_NW");  // experiment: 8 warps (2 per SMSP, <= 255 registers)
+    if (NO == 12 && nw_env && atoi(nw_env) == 8 && kg == 3 && full > 0) {
+      e = launch_kslide<NO, 3, false, 8>(a, chunk_atoms, 0, full, st);
+      if (e == cudaSuccess && rest == 2) e = launch_kslide<NO, 2, false, 8>(a, chunk_atoms, 3 * full, 1, st);
+      if (e == cudaSuccess && rest == 1) e = launch_kslide<NO, 1, false, 8>(a, chunk_atoms, 3 * full, 1, st);
+      note_kernel(1, "sigma_dmma_kslide_kernel<%d,8,3,3>", NO);
+      return e;
+    }
     if (full > 0) {
       if (kg == 3) e = launch_kslide<NO, 3>(a, chunk_atoms, 0, full, st);
       else if (kg == 2) e = launch_kslide<NO, 2>(a, chunk_atoms, 0, full, st);

@@ -44,6 +44,7 @@ __all__ = [
     "alg_flops",
     "sse_phase",
     "sse_phase_device",
+    "alloc_host",
 ]
 
 
@@ -77,7 +78,7 @@ def alg_flops(n_kz, n_qz, n_e, n_a, n_b, n_o, offsets) -> int:
     return 16 * n_a * n_b * n_kz * n_qz * n_o**3 * terms
 
 
-def _alloc_out(shape) -> Array:
+def alloc_host(shape) -> Array:
     """A zero-filled complex128 host array for a call's output (the reference allocates its outputs
     with np.zeros, sse.py:146-147).  Large outputs are anonymous mappings with transparent huge pages
     off: the grid-major [Nkz, NE, NA, No, No] output is written one atom-column chunk at a time, so
@@ -154,8 +155,8 @@ def sse_sigma(
         for stage, n in sigma_tallies(var, n_kz, n_qz, n_e, n_w, n_a, n_b, n_o).items():
             counter.stages[stage] = counter.stages.get(stage, 0) + n
 
-    out_l = _alloc_out(g_l.shape)
-    out_g = _alloc_out(g_g.shape)
+    out_l = alloc_host(g_l.shape)
+    out_g = alloc_host(g_g.shape)
     if out_l.size == 0 or dc.lesser.size == 0:
         return SelfEnergyTensor(lesser=out_l, greater=out_g)
 
@@ -356,8 +357,8 @@ def sse_phase(
             if o.shape != shape or o.dtype != np.complex128 or not o.flags.c_contiguous:
                 raise ValueError(f"out arrays must be C-contiguous complex128 of shape {shape}")
     else:
-        sig_l = _alloc_out(g_l.shape)
-        sig_g = _alloc_out(g_l.shape)
+        sig_l = alloc_host(g_l.shape)
+        sig_g = alloc_host(g_l.shape)
         pi_l = np.zeros(d_l.shape, dtype=np.complex128)
         pi_g = np.zeros(d_l.shape, dtype=np.complex128)
     if g_l.size == 0 or d_l.size == 0:

@@ -10,8 +10,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line():
     out = subprocess.run(
-        [sys.executable, "bench.py", "--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "0",
-         "--ref-pairs", "1"],
+        [sys.executable, "bench.py", "--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "0"],
         cwd=REPO, capture_output=True, text=True, timeout=600,
     )
     assert out.returncode == 0, out.stderr[-2000:]
