@@ -852,6 +852,7 @@ def run_gpu(args, p, grid, idx) -> None:
                 "achieved": k3_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": k3_tflops / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "traffic_source": (traffic or {}).get("capture"),
                 "k3_ms_per_launch": k3_ms_per_launch, "k3_launches_per_step": sig["launches"] / args.steps,
                 "k3_share_of_step": k3_share,
             },

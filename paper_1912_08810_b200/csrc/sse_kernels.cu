@@ -1281,7 +1281,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
   const int vt_vec = NO2 * ncol;  // double2 per point and polarity
   double2* vt = reinterpret_cast<double2*>(smem_raw);          // [2][No2][ncol]
   double2* sdh = vt + 2 * vt_vec;                               // [nb][3][No][NOP]
-  double2* sg2 = sdh + nb * 3 * NO * NOP;                       // [nb][No][NOP]
+  double2* sg2_buf = sdh + nb * 3 * NO * NOP;                   // [2][nb][No][NOP] (double-buffered)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e_groups = (p.ne + kPB2Energies - 1) / kPB2Energies;
   int bx = blockIdx.x;
@@ -1326,14 +1326,13 @@ pi_build_dmma_kernel(PiBuildArgs p) {
     bulk_s2g(out, vt + (st_ & 1) * vt_vec, (uint32_t)vt_vec * 16);
     bulk_commit();
   };
+  // one CTA barrier per (point, polarity) step: the G2 staging is double-buffered (sg2 of step t
+  // was last read in step t-2, before the previous barrier), and thread 0 waits for the V store
+  // that last read this step's V buffer BEFORE the barrier, so no thread writes it early
   for (int e = e0; e < e1; ++e) {
     for (int pol = 0; pol < 2; ++pol, ++step) {
       double2* buf = vt + (step & 1) * vt_vec;
-      __syncthreads();  // step-1's products are in its buffer; sg2 is free
-      if (threadIdx.x == 0) {
-        if (step >= 1) store_v(step - 1, pol ? e : e - 1, pol ? 0 : 1);  // previous (point, polarity)
-        if (step >= 2) bulk_wait_read<1>();  // buf's store (two steps ago) has read it
-      }
+      double2* sg2 = sg2_buf + (step & 1) * nb * NO * NOP;
 #pragma unroll
       for (int i = 0; i < kPB2Prefetch; ++i) {
         const int x = threadIdx.x + i * blockDim.x;
@@ -1341,7 +1340,9 @@ pi_build_dmma_kernel(PiBuildArgs p) {
       }
       for (int x = threadIdx.x + kPB2Prefetch * blockDim.x; x < nb * NO2; x += blockDim.x)
         sg2[(x / NO) * NOP + x % NO] = g2_elem(e, pol, x);
-      __syncthreads();
+      if (threadIdx.x == 0 && step >= 2) bulk_wait_read<0>();  // buf's store (issued last step) read it
+      __syncthreads();  // sg2 written; step-1's products are in the other V buffer
+      if (threadIdx.x == 0 && step >= 1) store_v(step - 1, pol ? e : e - 1, pol ? 0 : 1);  // previous step
       if (pol == 0) fetch(e, 1);
       else if (e + 1 < e1) fetch(e + 1, 0);
       for (int task = warp; task < tasks; task += kPB2Warps) {
@@ -2779,7 +2780,7 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
 
 template <int NO>
 static cudaError_t launch_pi_build_dmma(const PiBuildArgs& a, cudaStream_t st) {
-  const size_t smem = ((size_t)2 * NO * NO * a.nb * 9 + (size_t)a.nb * 4 * NO * (NO + 1)) * 16;
+  const size_t smem = ((size_t)2 * NO * NO * a.nb * 9 + (size_t)a.nb * 5 * NO * (NO + 1)) * 16;
   cudaError_t e = cudaFuncSetAttribute(pi_build_dmma_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPB2Energies - 1) / kPB2Energies);
@@ -2794,7 +2795,7 @@ static bool pi_build_dmma_ok(const PiBuildArgs& a) {
   const char* env = getenv("SSE_PI_BUILD");
   if (env && env[0] == '0') return false;
   if (a.no % 4 || a.no > 16) return false;
-  const size_t smem = ((size_t)2 * a.no * a.no * a.nb * 9 + (size_t)a.nb * 4 * a.no * (a.no + 1)) * 16;
+  const size_t smem = ((size_t)2 * a.no * a.no * a.nb * 9 + (size_t)a.nb * 5 * a.no * (a.no + 1)) * 16;
   return smem <= 220 * 1024;
 }
 
