@@ -1767,7 +1767,6 @@ int sse_phase_c128(sse_ctx* ctx, const sse_dims* d, const double* G_l, const dou
   const int nd = (int)ctx->devs.size();
   if (t) t->n_devices = nd;
   const int64_t per = (d->na + nd - 1) / nd;
-  const size_t blk = (size_t)d->norb * d->norb * 16;
   const size_t d_row = (size_t)(d->nb + 1) * 9 * 16, d_rows = (size_t)(d->nqz * d->nw);
   const size_t dc_row = (size_t)d->nb * 9 * 16;
   const size_t pi_row = d_row, pi_rows = d_rows;

@@ -391,7 +391,7 @@ template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32)
 sigma_dmma_kernel(SigmaArgs p) {
   constexpr FragGeom FG = frag_geom(NO);
-  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
+  constexpr int KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
   const int pol = blockIdx.y;
   int bx = blockIdx.x;
   const int rc = bx % p.ctas_per_ak;
@@ -442,7 +442,7 @@ sigma_dmma_kernel(SigmaArgs p) {
           // warp-uniform skip: tile past the end, or every row has E < off
           if (tile_row0 >= p.rows || (tile_row0 + 7) / NO < off) continue;
           const bool ok = v_row[t] && e_row[t] >= off;
-          double2 av[KH];
+          double2 av[FG.kh];
           load_a<NO>(av, G + rowoff[t] - (long long)off * p.g_se, pcol, ok);
 #pragma unroll
           for (int kk = 0; kk < KSTEPS; ++kk) {
@@ -495,7 +495,7 @@ template <int NO>
 __global__ void __launch_bounds__(kSigmaWarps * 32, 1)
 sigma_dmma_pipe_kernel(SigmaArgs p) {
   constexpr FragGeom FG = frag_geom(NO);
-  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
+  constexpr int KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
   const int pol = blockIdx.y;
   int bx = blockIdx.x;
   const int rc = bx % p.ctas_per_ak;
@@ -678,7 +678,7 @@ template <int NO, int NW, int MT>
 __global__ void __launch_bounds__(NW * 32, 1)
 sigma_dmma_slide_kernel(SigmaArgs p) {
   constexpr FragGeom FG = frag_geom(NO);
-  constexpr int KH = FG.kh, KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
+  constexpr int KSTEPS = FG.ksteps, NT = FG.nt, FV = FG.fv;
   using SG = SlideGeom<NO, NW, MT>;
   constexpr int R = SG::kRing, SB = kSlideStages, BVEC = SG::kBVec, BLK = NO * NO;
   // FIFO slot of a (non-negative) block index
@@ -2699,7 +2699,7 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
     // No > 10: at 3 the 3 x 9 x 2 accumulator doubles of No = 12 exceed the 168-register budget of
     // 12 warps (spills; paper shard 34.75 vs 35.12 TF/s at 2, 34.56 at 1); SSE_K3M_KG overrides
     const char* kg_env = getenv("SSE_K3M_KG");
-    const int kg = kg_env && atoi(kg_env) >= 1 && atoi(kg_env) <= 3 ? atoi(kg_env) : (NO > 10 ? 2 : 3);
+    const int kg = kg_env && atoi(kg_env) >= 1 && atoi(kg_env) <= 3 ? atoi(kg_env) : (NO >= 9 ? 2 : 3);
     const int full = a.nkz / kg, rest = a.nkz % kg;
     cudaError_t e = cudaSuccess;
     const char* nw_env = getenv("SSE_K3M_NW");  // experiment: 8 warps (2 per SMSP, <= 255 registers)
