@@ -168,6 +168,36 @@ def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a, n_b):
         assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
 
 
+@pytest.mark.parametrize("n_kz, n_qz, n_e, n_w, n_o, n_a", [
+    (5, 3, 30, 8, 12, 5),   # K3m: one 2-momentum group + ... (kg 2: groups {0,1}, {2,3}, remainder {4}); Nqz < Nkz
+    (4, 4, 26, 7, 10, 5),   # combined fragments (No = 10): groups {0,1,2}, {3 + 2 padded momenta}
+    (1, 1, 20, 8, 12, 4),   # Nkz = 1: a single-momentum launch
+    (7, 2, 22, 6, 4, 4),    # No = 4 (kg 3): groups {0,1,2}, {3,4,5}, remainder {6}; Nqz = 2 (most M vectors zero)
+    (2, 2, 33, 9, 6, 5),    # No = 6 combined, Nkz = 2: one padded group
+])
+def test_multi_momentum_groups_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_o, n_a):
+    """K3m's momentum grouping (full groups, remainder launches, padded combined groups, zero M
+    vectors for q >= Nqz) against the oracle, and bitwise equal to the single-momentum kernels."""
+    p = SimParams(n_kz=n_kz, n_qz=n_qz, n_E=n_e, n_w=n_w, n_A=n_a, n_B=4, n_orb=n_o)
+    g_l, g_g, d_l, d_g, dh = inputs.stream_instance(13, p, dh_scale=0.05)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    dc = CombinedD(*orc.preprocess_D(d_l, d_g, nmap.idx))
+    off, wt = np.array(grid.offsets), np.array(grid.weights)
+    ref_l, ref_g = orc.sigma_batched_fused(g_l, g_g, dc.lesser, dc.greater, dh, nmap.idx, off, wt)
+    from paper_1912_08810_b200 import _lib
+
+    outs = []
+    for choice in ("4", "1"):
+        monkeypatch.setenv("SSE_SIGMA_KERNEL", choice)
+        out = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(g_l, g_g), dc, dh, nmap, grid)
+        if choice == "4":
+            assert _lib.kernel_name("sigma").startswith("sigma_dmma_kslide_kernel"), _lib.kernel_name("sigma")
+        assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
+        outs.append(out)
+    assert np.array_equal(outs[0].lesser, outs[1].lesser) and np.array_equal(outs[0].greater, outs[1].greater)
+
+
 def test_layout_transformed_equals_grid_major_bitwise():
     """K1 round trip is lossless and the atom-major accumulation has the same order."""
     c = load_case("orb12_s5")
