@@ -1523,14 +1523,15 @@ int sse_sigma_multi(sse_ctx* ctx, const sse_dims* d, double* const* G_l, double*
   CHECK(validate_grid(d, off, wt));
   if (!G_l || !G_g || !Dc_l || !Dc_g || !dH || !nmap || !Sig_l || !Sig_g) return fail(SSE_EINVAL, "NULL tensor pointer");
   const int nd = (int)ctx->devs.size();
-  for (int i = 0; i < nd; ++i)
-    if (!G_l[i] || !G_g[i] || !Dc_l[i] || !Dc_g[i] || !dH[i] || !Sig_l[i] || !Sig_g[i])
-      return fail(SSE_EINVAL, "NULL tensor pointer for device %d", i);
   for (int64_t x = 0; x < d->na * d->nb; ++x)
     if (nmap[x] < 0 || nmap[x] >= d->na)
       return fail(SSE_EINVAL, "neighbor index %lld outside [0, %lld)", (long long)nmap[x], (long long)d->na);
   std::vector<int64_t> b;
   multi_bounds(d, nmap, nd, b);
+  for (int i = 0; i < nd; ++i)  // devices that own no atom (NA < n_gpus * chunk) may pass NULL
+    if (b[4 * i + 1] > b[4 * i] &&
+        (!G_l[i] || !G_g[i] || !Dc_l[i] || !Dc_g[i] || !dH[i] || !Sig_l[i] || !Sig_g[i]))
+      return fail(SSE_EINVAL, "NULL tensor pointer for device %d", i);
   const int64_t per = (d->na + nd - 1) / nd;
   const size_t blk = (size_t)d->nkz * d->ne * d->norb * d->norb * 16;  // bytes per atom and polarity
   // 1. halo exchange: every device receives its halo atoms from their owners (NCCL over NVLink)

@@ -785,6 +785,8 @@ def sigma_multi(g_l, g_g, dc_l, dc_g, dh, nmap_idx: Array, grid, out_l, out_g, *
 
     for i, (lo, hi, glo, ghi) in enumerate(lay):
         dev = torch.device("cuda", i)
+        if hi <= lo:  # this device owns no atom (more devices than chunks)
+            continue
         _check_dev(g_l[i], (ghi - glo, n_kz, n_e, n_o, n_o), f"g_l[{i}]", dev)
         _check_dev(g_g[i], (ghi - glo, n_kz, n_e, n_o, n_o), f"g_g[{i}]", dev)
         _check_dev(dc_l[i], (n_qz, n_w, hi - lo, n_b, 3, 3), f"dc_l[{i}]", dev)
@@ -795,7 +797,7 @@ def sigma_multi(g_l, g_g, dc_l, dc_g, dh, nmap_idx: Array, grid, out_l, out_g, *
     fmap = grid.frequency_map
     offs = np.array([int(fmap[w][0]) for w in range(n_w)], dtype=np.int64)
     wts = np.array([float(fmap[w][1]) for w in range(n_w)], dtype=np.float64)
-    arr = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])  # noqa: E731
+    arr = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() if t.numel() else None for t in ts])  # noqa: E731
     dims = _lib.SseDims(n_kz, n_qz, n_e, n_w, n_a, n_b, n_o)
     tim = _lib.SseTiming()
     ctx = _lib.context(n_gpus=n)
