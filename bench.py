@@ -8,11 +8,13 @@ sse.py:533) on the paper-scale FinFET workload (BASELINE.json configs[2]:
 NA=4864, NB=4, No=12, NE=706, Nw=70, Nkz=Nqz=3), strong-scaled over N GPUs
 by atom sharding (one process per GPU, NCCL halo exchange of G inside the
 step).  `value` = device time per step (CUDA events, inputs resident in HBM,
-max over ranks); `e2e` = the same step through the host C-ABI call
-(sse_sigma_c128_slab) from pinned host buffers with H2D/D2H inside.
-`--impl reference` times the reference's CPU algorithm (the oracle's
-BATCHED_FUSED restatement, the fastest reference arrangement) on a bounded
-sample of (atom, neighbour) pairs and extrapolates per pair.
+max over ranks).  `e2e` = the same step through the public drop-in
+`paper_1912_08810_b200.sse_sigma(...)` on pageable numpy arrays (N=1; per rank
+`sigma_host_slab` on numpy slabs for N>1), wall clock around the call, H2D/D2H
+inside; `e2e.pinned` = the same C-ABI pipeline from pinned buffers.
+`cpu_baseline` / `--impl reference` time the UNMODIFIED reference
+(negflow.sse.sse_sigma(BATCHED_FUSED), bytecode staged in oracle/_ref by
+oracle/make_ref.py) on single (atom, neighbour) pairs, x NA*NB.
 """
 
 from __future__ import annotations

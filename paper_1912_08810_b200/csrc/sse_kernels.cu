@@ -2449,227 +2449,6 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
 }
 
 // --------------------------------------------------------------------------
-// K6 v5 (fixed shapes No = 12, NB = 4): as v4, but each warp owns MT (3) 8-lag
-// m-tiles, so every B value read from shared memory feeds MT DMMAs and Nw = 65-72
-// (9 lag tiles) is 3 warps x 3 tiles with no tail CTAs (v4: 4 warps x 2 tiles +
-// a tail CTA per (atom, polarity, E-chunk) for the 9th tile).  Same per-output
-// accumulation order as every K6 variant (bitwise equal).
-// --------------------------------------------------------------------------
-template <int NOT, int NBT, int MT, int NW, int SL = kPi3Slots, int MINB = 4>
-__global__ void __launch_bounds__(NW * 32, MINB)
-pi_dmma5_kernel(PiArgs p, int chunk_atoms) {
-  constexpr int NO2 = NOT * NOT, NCOL = 9 * NBT;
-  constexpr int KHP = (NO2 + 3) / 4;
-  constexpr int QS = 2 * ((KHP + 2 * kPi3Sub - 1) / (2 * kPi3Sub));
-  static_assert(NO2 % 4 == 0 && KHP % QS == 0 && KHP / QS == kPi3Sub && 2 * NCOL <= 8 * kPi3NT,
-                "fixed-shape K6 v5 needs whole quads, uniform sub-stages and <= 9 n-tiles");
-  constexpr int SLOT = QS * 4 * NCOL;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* ring = reinterpret_cast<double2*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + SL * SLOT + kPi2Pad);
-  uint64_t* empty = full + SL;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int bx = blockIdx.x;
-  const int q = bx % p.nqz;
-  bx /= p.nqz;
-  const int ec = bx % p.echunks;
-  bx /= p.echunks;
-  const int pol = bx % 2;
-  const int la = bx / 2;
-  const int m_tiles = (p.nw + 7) / 8;
-  const int mt0 = (blockIdx.y * NW + warp) * MT;
-  const bool active = mt0 < m_tiles;
-  const int pcol = lane & 3;
-
-  for (int i = threadIdx.x; i < SL * SLOT + kPi2Pad; i += blockDim.x) ring[i] = make_double2(0.0, 0.0);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < SL; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, NW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-
-  const double2* __restrict__ G1 = pol ? p.G[1] : p.G[0];
-  const double2* __restrict__ VT = (pol ? p.VT[1] : p.VT[0]) + (long long)la * p.nkz * p.ne * NO2 * NCOL;
-  const double2* g_atom = G1 + (p.g_atom_of_chunk0 + la) * p.g_sa;
-
-  int w[MT], off[MT];
-  bool row_ok[MT];
-#pragma unroll
-  for (int t = 0; t < MT; ++t) {
-    w[t] = (mt0 + t) * 8 + (lane >> 2);
-    row_ok[t] = active && w[t] < p.nw;
-    off[t] = row_ok[t] ? __ldg(p.off + w[t]) : 0;
-  }
-  int off_min = 1 << 30;
-#pragma unroll
-  for (int t = 0; t < MT; ++t)
-    if (row_ok[t]) off_min = min(off_min, off[t]);
-#pragma unroll
-  for (int sh = 16; sh > 0; sh >>= 1) off_min = min(off_min, __shfl_xor_sync(0xffffffffu, off_min, sh));
-  const int nc0 = lane >> 2;
-  const int im = nc0 & 1;
-  const int c1 = (nc0 >> 1) ^ (((pcol >> 1) & 1) ? 2 : 0);
-  const int b_off = 2 * (p.swz ? c1 : (nc0 >> 1)) + im;
-  auto n_delta = [&](int n) -> int { return p.swz == 3 ? 2 * ((c1 ^ (n & 3)) - c1) : 0; };
-  const int b_dim = im ? -1 : 1;
-  const unsigned b_mask = im ? 0u : 0x80000000u;
-
-  double acc[MT][kPi3NT][2];
-#pragma unroll
-  for (int t = 0; t < MT; ++t)
-#pragma unroll
-    for (int u = 0; u < kPi3NT; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
-
-  const int e_lo = ec * p.e_per_chunk, e_hi = min(p.ne, e_lo + p.e_per_chunk);
-  const int ne_c = e_hi - e_lo;
-  const int n_st = p.nkz * ne_c;
-  const int n_ss = kPi3Sub * n_st;
-
-  auto produce = [&](int t) {
-    const int slot = t % SL;
-    if (t >= SL) mbar_wait(empty + slot, (uint32_t)(((t - SL) / SL) & 1));
-    const int st = t / kPi3Sub, j = t % kPi3Sub;
-    const int k = st / ne_c, e = e_lo + st % ne_c;
-    constexpr uint32_t bytes = (uint32_t)SLOT * 16;
-    mbar_arrive_expect_tx(full + slot, bytes);
-    bulk_g2s(ring + slot * SLOT, VT + (((long long)k * p.ne + e) * NO2 + j * QS * 4) * NCOL, bytes, full + slot);
-  };
-  auto row_of = [&](int t, int k, int e) -> const double2* {
-    int kp = k + q;
-    if (kp >= p.nkz) kp -= p.nkz;
-    if (!(row_ok[t] && e + off[t] < p.ne)) return kPiZeroRow + pcol;
-    if (p.peer.ranks > 0)
-      return peer_block(p.peer, pol, (long long)kp * p.ne + e + off[t], p.g_atom_of_chunk0 + la, NO2) + pcol;
-    return g_atom + (long long)kp * p.g_sk + (long long)(e + off[t]) * p.g_se + pcol;
-  };
-  const double2* cur[MT];
-  const double2* nxt[MT];
-  auto load_a = [&](int t, int kq) -> double2 {
-    const double2* r = kq < KHP ? cur[t] : nxt[t];
-    const int qq = kq < KHP ? kq : kq - KHP;
-    return __ldg(r + qq * 4);
-  };
-
-  if (threadIdx.x == 0)
-    for (int t = 0; t < SL - 1 && t < n_ss; ++t) produce(t);
-  auto stage_ke = [&](int st, int& k_, int& e_) {
-    k_ = st / ne_c;
-    e_ = e_lo + (st - k_ * ne_c);
-  };
-  {
-    int k0, e0, k1, e1;
-    stage_ke(0, k0, e0);
-    stage_ke(n_st > 1 ? 1 : 0, k1, e1);
-#pragma unroll
-    for (int t = 0; t < MT; ++t) {
-      cur[t] = row_of(t, k0, e0);
-      nxt[t] = row_of(t, k1, e1);
-    }
-  }
-  double2 a0[MT], a1[MT];
-#pragma unroll
-  for (int t = 0; t < MT; ++t) {
-    a0[t] = load_a(t, 0);
-    a1[t] = load_a(t, 1);
-  }
-  // one quad: each B value read once from shared memory, used by the warp's NV tiles
-  auto quad = [&](const double2 (&a)[MT], const double* b, auto nv) {
-    constexpr int NV = decltype(nv)::value;
-#pragma unroll
-    for (int u = 0; u < kPi3NT; ++u) {
-      if (NV > 2 && (u % 3) == 0) asm volatile("" ::: "memory");  // bound the hoisted B loads (registers)
-      const double br = b[8 * u];
-#pragma unroll
-      for (int t = 0; t < NV; ++t) dmma884_nv(acc[t][u], a[t].x, br);
-    }
-#pragma unroll
-    for (int u = 0; u < kPi3NT; ++u) {
-      if (NV > 2 && (u % 3) == 0) asm volatile("" ::: "memory");
-      const double bi = xor_sign(b[8 * u + b_dim], b_mask);
-#pragma unroll
-      for (int t = 0; t < NV; ++t) dmma884_nv(acc[t][u], a[t].y, bi);
-    }
-  };
-  // the stage loop, instantiated per count of valid tiles (warp-uniform, outside the loop)
-  auto run = [&](auto nv) {
-    constexpr int NV = decltype(nv)::value;
-    for (int ss = 0; ss < n_ss; ++ss) {
-      const int slot = ss % SL;
-      const int st = ss / kPi3Sub, j = ss - st * kPi3Sub;
-      const int kq = j * QS;
-      {
-        const int t = ss + SL - 1;
-        if (lane == 0 && t < n_ss && t % NW == warp) produce(t);
-      }
-      __syncwarp();
-      mbar_wait(full + slot, (uint32_t)((ss / SL) & 1));
-      int k, e;
-      stage_ke(st, k, e);
-      const bool live = NV > 0 && e + off_min < p.ne;
-      const double* sb = reinterpret_cast<const double*>(ring + slot * SLOT) + pcol * 2 * NCOL + b_off;
-      static_assert(QS == 6, "mode-3 swizzle deltas assume 6 quads per sub-stage");
-      const int dn0 = n_delta(kq / 3), dn1 = n_delta(kq / 3 + 1);
-      auto dq = [&](int qd) { return qd < 3 ? dn0 : dn1; };
-      if (live) {
-#pragma unroll
-        for (int pr = 0; pr < QS / 2; ++pr) {
-          quad(a0, sb + 16 * pr * NCOL + dq(2 * pr), nv);
-#pragma unroll
-          for (int tt = 0; tt < NV; ++tt) a0[tt] = load_a(tt, kq + 2 * pr + 2);
-          quad(a1, sb + (16 * pr + 8) * NCOL + dq(2 * pr + 1), nv);
-#pragma unroll
-          for (int tt = 0; tt < NV; ++tt) a1[tt] = load_a(tt, kq + 2 * pr + 3);
-        }
-      } else {
-#pragma unroll
-        for (int pr = 0; pr < QS / 2; ++pr) {
-#pragma unroll
-          for (int tt = 0; tt < NV; ++tt) {
-            a0[tt] = load_a(tt, kq + 2 * pr + 2);
-            a1[tt] = load_a(tt, kq + 2 * pr + 3);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + slot);
-      if (j == kPi3Sub - 1) {
-#pragma unroll
-        for (int tt = 0; tt < MT; ++tt) cur[tt] = nxt[tt];
-        if (st + 2 < n_st) {
-          int k2, e2;
-          stage_ke(st + 2, k2, e2);
-#pragma unroll
-          for (int tt = 0; tt < MT; ++tt) nxt[tt] = row_of(tt, k2, e2);
-        }
-      }
-    }
-  };
-  const int n_valid = active ? min(MT, m_tiles - mt0) : 0;
-  if (n_valid == MT) run(std::integral_constant<int, MT>{});
-  else if (MT > 2 && n_valid == 2) run(std::integral_constant<int, (MT > 2 ? 2 : 1)>{});
-  else if (n_valid == 1) run(std::integral_constant<int, 1>{});
-  else run(std::integral_constant<int, 0>{});
-
-  if (!active) return;
-  double2* part = p.partial + ((((long long)la * 2 + pol) * p.nqz + q) * p.echunks + ec) * p.nw * NCOL;
-#pragma unroll
-  for (int t = 0; t < MT; ++t) {
-    if (!row_ok[t]) continue;
-#pragma unroll
-    for (int u = 0; u < kPi3NT; ++u) {
-      const int c = u * 4 + (lane & 3);
-      if (c < NCOL)
-        part[(long long)w[t] * NCOL + c] =
-            make_double2(p.energy_weight * acc[t][u][0], p.energy_weight * acc[t][u][1]);
-    }
-  }
-}
-
-// --------------------------------------------------------------------------
 // K7: Pi assembly (sse.py:393-406): chain = sum of the E-chunk partials in
 // order; Pi[q,w,a,1+s] = i chain_s, Pi[q,w,a,0] = -i sum_s chain_s.
 // --------------------------------------------------------------------------
@@ -3062,8 +2841,8 @@ static size_t pi_smem(int v, int no, int ncol) {
 }
 static int pi_kernel_choice(int no, int ncol) {
   const char* env = getenv("SSE_PI_KERNEL");
-  int v = (env && env[0] >= '0' && env[0] <= '5') ? env[0] - '0' : 4;
-  if (v >= 4 && !(no == 12 && ncol == 36)) v = 3;  // v4 / v5 exist for the paper shapes only
+  int v = (env && env[0] >= '0' && env[0] <= '4') ? env[0] - '0' : 4;
+  if (v == 4 && !(no == 12 && ncol == 36)) v = 3;  // v4 exists for the paper shapes only
   if (v == 3 && (no * no + 3) / 4 < 2) v = 2;
   while (v > 0 && pi_smem(v, no, ncol) > 220 * 1024) --v;
   return v;
@@ -3073,7 +2852,7 @@ static int pi_kernel_choice(int no, int ncol) {
 int pi_vt_swizzle(int no, int ncol) {
   const int v = pi_kernel_choice(no, ncol);
   if (ncol % 4 || v < 3) return 0;
-  return v >= 4 ? 3 : 2;  // v4 / v5 (paper shapes): the mode-3 swizzle; v3: mode 2
+  return v >= 4 ? 3 : 2;  // v4 (paper shapes): the mode-3 swizzle; v3: mode 2
 }
 
 cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
@@ -3085,20 +2864,6 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
   const unsigned gx = (unsigned)((long long)chunk_atoms * 2 * a.echunks * a.nqz);
   cudaError_t e = cudaSuccess;
   switch (v) {
-    case 5: {
-      // 3 warps x 3 lag tiles per CTA, ring of 3 slots: 4 CTAs (12 warps) per SM
-      auto kern = pi_dmma5_kernel<12, 4, 3, 3, 3, 4>;
-      const size_t slot = (size_t)2 * ((((a.no * a.no + 3) / 4) + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) * 4 * a.ncol * 16;
-      const size_t smem5 = smem - (size_t)(kPi3Slots - 3) * slot;
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return e;
-      const int m_tiles = (a.nw + 7) / 8;
-      const int gy5 = (m_tiles + 8) / 9;  // 9 tiles (3 warps x 3) per CTA row
-      note_kernel(5, "pi_dmma5_kernel<12,4,3,3,3,4>");
-      kern<<<dim3(gx, (unsigned)gy5), 3 * 32, smem5, st>>>(a, chunk_atoms);
-      break;
-    }
     case 4: {
       e = cudaFuncSetAttribute(pi_dmma4_kernel<12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e == cudaSuccess)

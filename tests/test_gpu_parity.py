@@ -171,8 +171,8 @@ def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a, n_b):
 @pytest.mark.parametrize("n_kz, n_qz, n_e, n_w, n_o, n_a", [
     (5, 3, 30, 8, 12, 5),   # K3m: one 2-momentum group + ... (kg 2: groups {0,1}, {2,3}, remainder {4}); Nqz < Nkz
     (4, 4, 26, 7, 10, 5),   # combined fragments (No = 10): groups {0,1,2}, {3 + 2 padded momenta}
-    (1, 1, 20, 8, 12, 4),   # Nkz = 1: a single-momentum launch
-    (7, 2, 22, 6, 4, 4),    # No = 4 (kg 3): groups {0,1,2}, {3,4,5}, remainder {6}; Nqz = 2 (most M vectors zero)
+    (1, 1, 20, 8, 12, 5),   # Nkz = 1: a single-momentum launch
+    (7, 2, 22, 6, 4, 5),    # No = 4 (kg 3): groups {0,1,2}, {3,4,5}, remainder {6}; Nqz = 2 (most M vectors zero)
     (2, 2, 33, 9, 6, 5),    # No = 6 combined, Nkz = 2: one padded group
 ])
 def test_multi_momentum_groups_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_o, n_a):

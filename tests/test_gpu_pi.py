@@ -51,10 +51,7 @@ def test_pi_golden_parity(name):
     if name == "pi_paperlike_s12":
         from paper_1912_08810_b200 import _lib
 
-        import os
-
-        want = {"5": "pi_dmma5_kernel"}.get(os.environ.get("SSE_PI_KERNEL", ""), "pi_dmma4_kernel<12,4,4,3,4,true>")
-        assert _lib.kernel_name("pi").startswith(want), _lib.kernel_name("pi")
+        assert _lib.kernel_name("pi") == "pi_dmma4_kernel<12,4,4,3,4,true>", _lib.kernel_name("pi")
         assert _lib.kernel_name("pi_build") == "pi_build_dmma_kernel<12>"
     p = c.p
     assert counter.stages == pi_tallies(True, p.n_kz, p.n_qz, p.n_E, p.n_w, p.n_A, p.n_B, p.n_orb)
@@ -121,7 +118,7 @@ def test_pi_shapes_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w, n_a, n_b, n
     ch_l, ch_g = orc.pi_chains(g_l, g_g, dh, nmap.idx, np.array(grid.offsets), grid.energy_weight, n_qz)
     ref_l, ref_g = orc.pi_from_chains(ch_l, ch_g)
     outs = []
-    for choice in ("5", "4", "3", "2", "1", "0"):
+    for choice in ("4", "3", "2", "1", "0"):
         monkeypatch.setenv("SSE_PI_KERNEL", choice)
         out = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, n_qz)
         assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
