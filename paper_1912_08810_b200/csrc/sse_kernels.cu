@@ -1366,27 +1366,35 @@ pi_build_dmma_kernel(PiBuildArgs p) {
             dmma884_nv(u[nt], a.y, xor_sign(im ? g.x : g.y, neg));
           }
         }
-        double w[NT2][2];
+        // W in groups of WG n-tiles, each group stored right after its last DMMA, so the V-image
+        // scatter (STS) of one group overlaps the DMMAs of the next (the same per-accumulator order)
+        constexpr int WG = NT2 % 3 == 0 ? 3 : (NT2 % 2 == 0 ? 2 : 1);
 #pragma unroll
-        for (int nt = 0; nt < NT2; ++nt) w[nt][0] = w[nt][1] = 0.0;
+        for (int g0 = 0; g0 < NT2; g0 += WG) {
+          double w[WG][2];
 #pragma unroll
-        for (int kh = 0; kh < KH; ++kh) {
-          const int t = 4 * kh + kl;  // U[m][t] = u[kh] of this lane
+          for (int x = 0; x < WG; ++x) w[x][0] = w[x][1] = 0.0;
 #pragma unroll
-          for (int nt = 0; nt < NT2; ++nt) {
-            const int cc = (nt * 8 + (lane >> 2)) >> 1, i = cc / NO, n = cc % NO;
-            const double2 h = sdh[((ss * 3 + i) * NO + t) * NOP + n];
-            dmma884_nv(w[nt], u[kh][0], im ? h.y : h.x);
-            dmma884_nv(w[nt], u[kh][1], xor_sign(im ? h.x : h.y, neg));
+          for (int kh = 0; kh < KH; ++kh) {
+            const int t = 4 * kh + kl;  // U[m][t] = u[kh] of this lane
+#pragma unroll
+            for (int x = 0; x < WG; ++x) {
+              const int nt = g0 + x;
+              const int cc = (nt * 8 + (lane >> 2)) >> 1, i = cc / NO, n = cc % NO;
+              const double2 h = sdh[((ss * 3 + i) * NO + t) * NOP + n];
+              dmma884_nv(w[x], u[kh][0], im ? h.y : h.x);
+              dmma884_nv(w[x], u[kh][1], xor_sign(im ? h.x : h.y, neg));
+            }
           }
-        }
-        if (m_ok) {
+          if (m_ok) {
 #pragma unroll
-          for (int nt = 0; nt < NT2; ++nt) {
-            const int cc = nt * 4 + kl, i = cc / NO, n = cc % NO;
-            const int kap = n * NO + mp;
-            const int c = ss * 9 + i * 3 + mj;
-            buf[kap * ncol + (c ^ vt_swz(kap, NO, p.swz))] = make_double2(w[nt][0], w[nt][1]);
+            for (int x = 0; x < WG; ++x) {
+              const int nt = g0 + x;
+              const int cc = nt * 4 + kl, i = cc / NO, n = cc % NO;
+              const int kap = n * NO + mp;
+              const int c = ss * 9 + i * 3 + mj;
+              buf[kap * ncol + (c ^ vt_swz(kap, NO, p.swz))] = make_double2(w[x][0], w[x][1]);
+            }
           }
         }
       }
