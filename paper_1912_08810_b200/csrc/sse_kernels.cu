@@ -1267,7 +1267,7 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <int NO>
+template <int NO, int WG0 = 3>
 __global__ void __launch_bounds__(kPB2Warps * 32, 1)
 pi_build_dmma_kernel(PiBuildArgs p) {
   constexpr int NO2 = NO * NO, MROWS = 3 * NO, MT = (MROWS + 7) / 8;
@@ -1368,7 +1368,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
         }
         // W in groups of WG n-tiles, each group stored right after its last DMMA, so the V-image
         // scatter (STS) of one group overlaps the DMMAs of the next (the same per-accumulator order)
-        constexpr int WG = NT2 % 3 == 0 ? 3 : (NT2 % 2 == 0 ? 2 : 1);
+        constexpr int WG = NT2 % WG0 == 0 ? WG0 : (NT2 % 3 == 0 ? 3 : (NT2 % 2 == 0 ? 2 : 1));
 #pragma unroll
         for (int g0 = 0; g0 < NT2; g0 += WG) {
           double w[WG][2];
@@ -2788,12 +2788,16 @@ cudaError_t launch_sigma(const SigmaArgs& a0, int chunk_atoms, cudaStream_t st) 
 
 template <int NO>
 static cudaError_t launch_pi_build_dmma(const PiBuildArgs& a, cudaStream_t st) {
+  // W n-tile group size (SSE_PI_WG, experiments): 3 default, 1, or NT2 (one group, round-1 order)
+  const char* env = getenv("SSE_PI_WG");
+  const int wg = env ? atoi(env) : 3;
+  auto kern = wg == 1 ? pi_build_dmma_kernel<NO, 1> : (wg == 9 ? pi_build_dmma_kernel<NO, 9> : pi_build_dmma_kernel<NO, 3>);
   const size_t smem = ((size_t)2 * NO * NO * a.nb * 9 + (size_t)a.nb * 5 * NO * (NO + 1)) * 16;
-  cudaError_t e = cudaFuncSetAttribute(pi_build_dmma_kernel<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long blocks = (long long)a.chunk_atoms * a.nkz * ((a.ne + kPB2Energies - 1) / kPB2Energies);
   note_kernel(4, "pi_build_dmma_kernel<%d>", NO);
-  pi_build_dmma_kernel<NO><<<(unsigned)blocks, kPB2Warps * 32, smem, st>>>(a);
+  kern<<<(unsigned)blocks, kPB2Warps * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
