@@ -942,7 +942,9 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
                       ds.s[1].as<double2>()};
     size_t ei = 0;
     std::vector<cudaEvent_t> out_ready(plan.size(), nullptr);
-    for (size_t ci = 0; ci < plan.size(); ++ci) {
+    // H2D of chunk ci (packing it first for pageable callers); its completion event is in_ev[ci]
+    std::vector<cudaEvent_t> in_ev(plan.size(), nullptr);
+    auto issue_h2d = [&](size_t ci) -> int {
       const Piece& pc = plan[ci];
       const int64_t a0 = pc.a0, n = pc.n, ncols = pc.c1 - pc.c0;
       if (stage_in) {
@@ -988,13 +990,24 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
         CU(cudaMemcpyAsync((char*)ds.dh.ptr + a0 * dh_atom, dHh + a0 * dh_atom, n * dh_atom,
                            cudaMemcpyHostToDevice, ds.s_h2d));
       }
-      cudaEvent_t in = pipe_event(ds, ei++), done = pipe_event(ds, ei++);
-      if (!in || !done) return fail(SSE_ECUDA, "event creation failed");
-      CU(cudaEventRecord(in, ds.s_h2d));
-      CU(cudaStreamWaitEvent(st, in, 0));
+      in_ev[ci] = pipe_event(ds, ei++);
+      if (!in_ev[ci]) return fail(SSE_ECUDA, "event creation failed");
+      CU(cudaEventRecord(in_ev[ci], ds.s_h2d));
+      return SSE_OK;
+    };
+    if (!plan.empty()) CHECK(issue_h2d(0));
+    for (size_t ci = 0; ci < plan.size(); ++ci) {
+      const Piece& pc = plan[ci];
+      const int64_t a0 = pc.a0, n = pc.n;
+      cudaEvent_t done = pipe_event(ds, ei++);
+      if (!done) return fail(SSE_ECUDA, "event creation failed");
+      CU(cudaStreamWaitEvent(st, in_ev[ci], 0));
       CHECK(run_chunk(ds, d, gslab, oslab, ptr, c.off, a0, n, st, 2, &launches));
       CU(cudaEventRecord(done, st));
       CU(cudaStreamWaitEvent(ds.s_d2h, done, 0));
+      // the next chunk is packed and its H2D queued while this one computes, before the host
+      // waits for the previous chunk's Sigma (so a slow unpack never delays the GPU's input)
+      if (ci + 1 < plan.size()) CHECK(issue_h2d(ci + 1));
       if (stage_out) {
         char* dst = (char*)ds.stage_out[ci % 2].ptr;  // its previous chunk (ci-2) was unpacked at ci-1
         for (int p = 0; p < 2; ++p)

@@ -1,0 +1,9 @@
+#!/bin/bash
+# staging ring with the next chunk packed before the unpack wait: bitwise tests + paper e2e with the trace
+cd "$GRAFT_REPO_ROOT"
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_loop.py -x -q -k "staging or timing or sse_phase or golden_parity_all_variants" > gpurun_out/r2_e2e2_tests.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2_e2e2_tests.log
+SSE_STAGING_TRACE=1 timeout 900 python bench.py --steps 1 --warmup 3 --cpu-atoms 0 --pi-steps 0 --phase-device-steps 0 \
+  --e2e-steps 2 --e2e-warmup 1 > gpurun_out/r2_e2e2_trace.log 2>&1
+echo "rc=$?" >> gpurun_out/r2_e2e2_trace.log
