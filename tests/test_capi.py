@@ -178,3 +178,18 @@ def test_sse_phase_argument_errors():
         sse_phase(g, ph, dh[:, :1], nmap, grid, p.n_qz)
     with pytest.raises(ValueError, match="out arrays"):
         sse_phase(g, ph, dh, nmap, grid, p.n_qz, out=(np.zeros(3),) * 4)
+
+
+def test_alloc_host_is_a_zeroed_writable_array():
+    """The drop-in's output allocator (4 KB-page anonymous mapping for >= 1 GiB, np.zeros below)
+    returns ordinary zero-filled, writable, C-contiguous complex128 arrays like the reference's
+    np.zeros (sse.py:146-147)."""
+    from paper_1912_08810_b200.sse import alloc_host
+
+    for shape in ((3, 5, 7), (2, 1024, 1024, 33)):  # small, and just over 1 GiB
+        a = alloc_host(shape)
+        assert a.shape == shape and a.dtype == np.complex128 and a.flags.c_contiguous and a.flags.writeable
+        assert not a[0].any() and not a[-1].any()
+        a[-1, ..., -1] = 1 + 2j
+        assert a[-1, ..., -1].all()
+        del a
