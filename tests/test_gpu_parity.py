@@ -506,3 +506,33 @@ def test_in_library_multi_gpu_sigma_bitwise():
         for i, (lo, hi, _, _) in enumerate(lay):
             assert np.array_equal(np.moveaxis(ol[i].cpu().numpy(), 0, 2), full.lesser[:, :, lo:hi]), (ngpu, i)
             assert np.array_equal(np.moveaxis(og[i].cpu().numpy(), 0, 2), full.greater[:, :, lo:hi]), (ngpu, i)
+
+
+def test_device_wrappers_reject_mismatched_tensors():
+    """The C side sees raw pointers only, so the device wrappers check every tensor's shape, dtype
+    and device before the call (a mismatch raises ValueError instead of an out-of-bounds access)."""
+    torch = _torch()
+    from paper_1912_08810_b200 import sse as dev
+
+    c = load_case("orb12_s5")
+    p = c.p
+    dc = _dc(c)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    gl, gg = cu(c.g_l), cu(c.g_g)
+    ol = torch.zeros(p.electron_shape, dtype=torch.complex128, device="cuda")
+    og = torch.zeros_like(ol)
+    args = dict(n_a=p.n_A)
+    with pytest.raises(ValueError, match="out_g"):
+        dev.sigma_device(gl, gg, cu(dc.lesser), cu(dc.greater), cu(c.dh), c.idx, c.offsets, c.weights, ol,
+                         og[:, :, :-1].contiguous(), **args)
+    with pytest.raises(ValueError, match="complex128"):
+        dev.sigma_device(gl, gg.to(torch.complex64), cu(dc.lesser), cu(dc.greater), cu(c.dh), c.idx, c.offsets,
+                         c.weights, ol, og, **args)
+    with pytest.raises(ValueError, match="dst"):
+        dev.layout_transform(gl, torch.empty((1, 2, 3), dtype=torch.complex128, device="cuda"), to_atom_major=True)
+    pi = [torch.zeros((p.n_qz, p.n_w, p.n_A, p.n_B + 1, 3, 3), dtype=torch.complex128, device="cuda") for _ in range(2)]
+    with pytest.raises(ValueError, match="pi_g"):
+        dev.pi_device(gl, gg, cu(c.dh), c.idx, c.offsets, 0.1, pi[0], pi[1][:, :1].contiguous(), n_a=p.n_A,
+                      n_qz=p.n_qz)
+    with pytest.raises(ValueError, match="overruns"):
+        dev.fill_synthetic(ol, 0, 0, 0, p.n_A + 1, p.n_kz * p.n_E, p.n_orb**2, p.n_orb**2, p.n_A * p.n_orb**2)
