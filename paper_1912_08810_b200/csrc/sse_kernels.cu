@@ -1271,9 +1271,12 @@ template <int NO, int WG0 = 3>
 __global__ void __launch_bounds__(kPB2Warps * 32, 1)
 pi_build_dmma_kernel(PiBuildArgs p) {
   constexpr int NO2 = NO * NO, MROWS = 3 * NO, MT = (MROWS + 7) / 8;
-  constexpr int KH = NO / 4;         // k-steps per real/imaginary half
-  constexpr int NT1 = NO / 4;        // n-tiles of U (2No real columns)
-  constexpr int NT2 = 3 * NO / 4;    // n-tiles of W (6No real columns)
+  // No % 4 != 0 (e.g. 10, the small config): K and N padded to multiples of 4 complex (the
+  // padding reads zeros through the guards below)
+  constexpr int KH = (NO + 3) / 4;          // k-steps per real/imaginary half
+  constexpr int NT1 = (NO + 3) / 4;         // n-tiles of U (2No real columns)
+  constexpr int NT2 = (6 * NO + 7) / 8;     // n-tiles of W (6No real columns)
+  constexpr bool PAD = NO % 4 != 0;
   constexpr int NOP = NO + 1;        // padded smem row of dH / G2 blocks: the B reads (4 rows
                                      // of a quarter warp) hit distinct banks
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1358,10 +1361,11 @@ pi_build_dmma_kernel(PiBuildArgs p) {
 #pragma unroll
         for (int kh = 0; kh < KH; ++kh) {
           const int r = 4 * kh + kl;
-          const double2 a = m_ok ? dsr[r] : make_double2(0.0, 0.0);
+          const double2 a = (m_ok && (!PAD || r < NO)) ? dsr[r] : make_double2(0.0, 0.0);
 #pragma unroll
           for (int nt = 0; nt < NT1; ++nt) {
-            const double2 g = g2[r * NOP + ((nt * 8 + (lane >> 2)) >> 1)];
+            const int n = (nt * 8 + (lane >> 2)) >> 1;
+            const double2 g = (!PAD || (r < NO && n < NO)) ? g2[r * NOP + n] : make_double2(0.0, 0.0);
             dmma884_nv(u[nt], a.x, im ? g.y : g.x);
             dmma884_nv(u[nt], a.y, xor_sign(im ? g.x : g.y, neg));
           }
@@ -1381,7 +1385,8 @@ pi_build_dmma_kernel(PiBuildArgs p) {
             for (int x = 0; x < WG; ++x) {
               const int nt = g0 + x;
               const int cc = (nt * 8 + (lane >> 2)) >> 1, i = cc / NO, n = cc % NO;
-              const double2 h = sdh[((ss * 3 + i) * NO + t) * NOP + n];
+              const double2 h = (!PAD || (t < NO && cc < 3 * NO)) ? sdh[((ss * 3 + i) * NO + t) * NOP + n]
+                                                                   : make_double2(0.0, 0.0);
               dmma884_nv(w[x], u[kh][0], im ? h.y : h.x);
               dmma884_nv(w[x], u[kh][1], xor_sign(im ? h.x : h.y, neg));
             }
@@ -1393,7 +1398,7 @@ pi_build_dmma_kernel(PiBuildArgs p) {
               const int cc = nt * 4 + kl, i = cc / NO, n = cc % NO;
               const int kap = n * NO + mp;
               const int c = ss * 9 + i * 3 + mj;
-              buf[kap * ncol + (c ^ vt_swz(kap, NO, p.swz))] = make_double2(w[x][0], w[x][1]);
+              if (!PAD || cc < 3 * NO) buf[kap * ncol + (c ^ vt_swz(kap, NO, p.swz))] = make_double2(w[x][0], w[x][1]);
             }
           }
         }
@@ -2806,7 +2811,7 @@ static cudaError_t launch_pi_build_dmma(const PiBuildArgs& a, cudaStream_t st) {
 static bool pi_build_dmma_ok(const PiBuildArgs& a) {
   const char* env = getenv("SSE_PI_BUILD");
   if (env && env[0] == '0') return false;
-  if (a.no % 4 || a.no > 16) return false;
+  if (!(a.no % 4 == 0 || a.no == 10) || a.no > 16) return false;  // 10: the small config (padded K / N)
   const size_t smem = ((size_t)2 * a.no * a.no * a.nb * 9 + (size_t)a.nb * 5 * a.no * (a.no + 1)) * 16;
   return smem <= 220 * 1024;
 }
@@ -2818,6 +2823,7 @@ cudaError_t launch_pi_build(const PiBuildArgs& a, cudaStream_t st) {
     switch (a.no) {
       case 4: return launch_pi_build_dmma<4>(a, st);
       case 8: return launch_pi_build_dmma<8>(a, st);
+      case 10: return launch_pi_build_dmma<10>(a, st);
       case 12: return launch_pi_build_dmma<12>(a, st);
       case 16: return launch_pi_build_dmma<16>(a, st);
       default: break;
