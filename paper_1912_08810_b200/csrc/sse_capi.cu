@@ -589,7 +589,10 @@ int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const ss
                     const DevPtrs& p, const int64_t* nmap, const int64_t* off, const double* wt,
                     cudaStream_t st, int* launches, int npol = 2, const ScatterCfg* sc = nullptr) {
   CHECK(prepare_tables(ds, d, g, out, nmap, off, wt, st));
-  const int64_t chunk = std::min<int64_t>(op_chunk_atoms(d, off), out.natoms);
+  // balanced chunks (no small trailing launch whose CTAs would fill only part of a wave)
+  const int64_t max_chunk = std::min<int64_t>(op_chunk_atoms(d, off), out.natoms);
+  const int64_t n_chunks = (out.natoms + max_chunk - 1) / max_chunk;
+  const int64_t chunk = (out.natoms + n_chunks - 1) / n_chunks;
   for (int64_t a0 = 0; a0 < out.natoms; a0 += chunk)
     CHECK(run_chunk(ds, d, g, out, p, off, a0, std::min<int64_t>(chunk, out.natoms - a0), st, npol,
                     launches, sc));
