@@ -846,7 +846,9 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
     // chunk boundaries: a geometric ramp of small chunks at the start (the first chunk's H2D is
     // not hidden; each chunk's compute then covers the next one's H2D, ~3.5x faster per atom on
     // one B200) and the mirrored ramp at the end (the last chunk's D2H is not hidden)
-    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(8, chunk / 4));
+    // ramp starts at 25 atoms: a K3m launch of n atoms has 6n CTAs, so >= 25 fill the 148 SMs
+    // (8-atom edge chunks ran at a third of the machine; their exposed H2D was only ~2 ms shorter)
+    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(25, chunk / 4));
     std::vector<int64_t> ramp;
     for (int64_t s = edge; s < chunk; s *= 3) ramp.push_back(s);
     int64_t ramp_atoms = 0;
