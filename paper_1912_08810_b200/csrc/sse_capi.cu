@@ -189,7 +189,7 @@ struct DevState {
   cudaEvent_t ev[6] = {};
   DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev, zero_m;
   DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2], draw[2];
-  PinnedBuf stage_in[2], stage_out[2];  // host staging ring of the pageable-memory host calls
+  PinnedBuf stage_in[2], stage_out[3];  // host staging ring of the pageable-memory host calls
   cudaEvent_t stage_ev[2] = {};         // H2D from stage_in[b] done
   std::vector<unsigned char> pi_mask_host;
   // host copies of the small tables last uploaded (skip re-uploads: a pageable
@@ -367,7 +367,8 @@ void destroy_dev(DevState& d) {
   if (d.scratch_done) cudaEventDestroy(d.scratch_done);
   for (auto& e : d.stage_ev)
     if (e) cudaEventDestroy(e);
-  for (PinnedBuf* b : {&d.stage_in[0], &d.stage_in[1], &d.stage_out[0], &d.stage_out[1]}) b->release();
+  for (PinnedBuf* b : {&d.stage_in[0], &d.stage_in[1], &d.stage_out[0], &d.stage_out[1], &d.stage_out[2]})
+    b->release();
   for (cudaStream_t s : {d.stream, d.s_h2d, d.s_d2h})
     if (s) cudaStreamDestroy(s);
 }
@@ -846,9 +847,8 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
     // chunk boundaries: a geometric ramp of small chunks at the start (the first chunk's H2D is
     // not hidden; each chunk's compute then covers the next one's H2D, ~3.5x faster per atom on
     // one B200) and the mirrored ramp at the end (the last chunk's D2H is not hidden)
-    // ramp starts at 25 atoms: a K3m launch of n atoms has 6n CTAs, so >= 25 fill the 148 SMs
-    // (8-atom edge chunks ran at a third of the machine; their exposed H2D was only ~2 ms shorter)
-    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(25, chunk / 4));
+    // (a 25-atom edge measured 35 ms slower end to end: its first pack / H2D and last unpack are exposed)
+    const int64_t edge = std::max<int64_t>(1, std::min<int64_t>(8, chunk / 4));
     std::vector<int64_t> ramp;
     for (int64_t s = edge; s < chunk; s *= 3) ramp.push_back(s);
     int64_t ramp_atoms = 0;
@@ -913,7 +913,7 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
     if (stage_in)
       for (int b = 0; b < 2; ++b) CHECK(ds.stage_in[b].ensure(in_cap));
     if (stage_out)
-      for (int b = 0; b < 2; ++b) CHECK(ds.stage_out[b].ensure(out_cap));
+      for (int b = 0; b < 3; ++b) CHECK(ds.stage_out[b].ensure(out_cap));
     HostPool& pool = HostPool::get();
     double pack_ms = 0, unpack_ms = 0;
     auto now_ms = [] {
@@ -933,7 +933,7 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
     auto unpack = [&](size_t k) {  // chunk k's Sigma columns: staging -> caller rows
       const Piece& pc = plan[k];
       const double t0 = now_ms();
-      const char* src = (const char*)ds.stage_out[k % 2].ptr;
+      const char* src = (const char*)ds.stage_out[k % 3].ptr;
       for (int p = 0; p < 2; ++p)
         copy_rows(Sh[p] + (lo + pc.a0 - c.hs.atom0) * blk, hs_pitch, src + p * rows * pc.n * blk, pc.n * blk,
                   pc.n * blk, rows);
@@ -1000,8 +1000,8 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
       CU(cudaEventRecord(in_ev[ci], ds.s_h2d));
       return SSE_OK;
     };
-    if (!plan.empty()) CHECK(issue_h2d(0));
-    for (size_t ci = 0; ci < plan.size(); ++ci) {
+    // compute + D2H of chunk ci (its H2D already queued); staged outputs go to slot ci % 3
+    auto issue_compute = [&](size_t ci) -> int {
       const Piece& pc = plan[ci];
       const int64_t a0 = pc.a0, n = pc.n;
       cudaEvent_t done = pipe_event(ds, ei++);
@@ -1010,34 +1010,42 @@ int host_call_on_device_body(DevState& ds, const HostCall& c, int64_t lo, int64_
       CHECK(run_chunk(ds, d, gslab, oslab, ptr, c.off, a0, n, st, 2, &launches));
       CU(cudaEventRecord(done, st));
       CU(cudaStreamWaitEvent(ds.s_d2h, done, 0));
-      // the next chunk is packed and its H2D queued while this one computes, before the host
-      // waits for the previous chunk's Sigma (so a slow unpack never delays the GPU's input)
-      if (ci + 1 < plan.size()) CHECK(issue_h2d(ci + 1));
       if (stage_out) {
-        char* dst = (char*)ds.stage_out[ci % 2].ptr;  // its previous chunk (ci-2) was unpacked at ci-1
+        char* dst = (char*)ds.stage_out[ci % 3].ptr;  // its previous chunk (ci-3) was unpacked already
         for (int p = 0; p < 2; ++p)
           CU(cudaMemcpy2DAsync(dst + p * rows * n * blk, n * blk, (char*)ds.s[p].ptr + a0 * blk, on * blk, n * blk,
                                rows, cudaMemcpyDeviceToHost, ds.s_d2h));
         out_ready[ci] = pipe_event(ds, ei++);
         if (!out_ready[ci]) return fail(SSE_ECUDA, "event creation failed");
         CU(cudaEventRecord(out_ready[ci], ds.s_d2h));
-        if (ci >= 1) {  // the previous chunk's Sigma, while this chunk computes
-          const double tw = now_ms();
-          CU(cudaEventSynchronize(out_ready[ci - 1]));
-          if (trace)
-            fprintf(stderr, "[sse staging] wait D2H chunk %zu: %.1f-%.1f ms\n", ci - 1, tw - t_call, now_ms() - t_call);
-          unpack(ci - 1);
-        }
       } else {
         for (int p = 0; p < 2; ++p)
           CU(cudaMemcpy2DAsync(Sh[p] + (lo + a0 - c.hs.atom0) * blk, hs_pitch,
                                (char*)ds.s[p].ptr + a0 * blk, on * blk, n * blk, rows,
                                cudaMemcpyDeviceToHost, ds.s_d2h));
       }
+      return SSE_OK;
+    };
+    // The GPU is kept two chunks ahead of the host: chunks ci+1 and ci+2 are packed and queued
+    // (H2D, compute, D2H) before the host waits for chunk ci's Sigma and unpacks it, so a long
+    // unpack of a big chunk never starves the short chunks of the closing ramp.
+    const size_t nch = plan.size();
+    for (size_t ci = 0; ci < std::min<size_t>(2, nch); ++ci) {
+      CHECK(issue_h2d(ci));
+      CHECK(issue_compute(ci));
     }
-    if (stage_out && !plan.empty()) {
-      CU(cudaEventSynchronize(out_ready.back()));
-      unpack(plan.size() - 1);
+    for (size_t ci = 0; ci < nch; ++ci) {
+      if (ci + 2 < nch) {
+        CHECK(issue_h2d(ci + 2));     // input slot (ci+2) % 2: its previous H2D (chunk ci) is done early
+        CHECK(issue_compute(ci + 2));  // output slot (ci+2) % 3: chunk ci-1 was unpacked last iteration
+      }
+      if (stage_out) {
+        const double tw = now_ms();
+        CU(cudaEventSynchronize(out_ready[ci]));
+        if (trace)
+          fprintf(stderr, "[sse staging] wait D2H chunk %zu: %.1f-%.1f ms\n", ci, tw - t_call, now_ms() - t_call);
+        unpack(ci);
+      }
     }
     if (t) {
       t->h2d_ms += pack_ms;
