@@ -2900,6 +2900,17 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
+        const char* sl_env = getenv("SSE_PI_V4_SLOTS");  // experiment: a 4-slot V ring (55 KB per CTA)
+        if (split && sl_env && sl_env[0] == '4') {
+          auto both4 = pi_dmma4_kernel<12, 4, 4, 4, 4, true>;
+          e = cudaFuncSetAttribute(both4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e == cudaSuccess) e = cudaFuncSetAttribute(both4, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          if (e != cudaSuccess) return e;
+          const long long tails = (long long)chunk_atoms * 2 * a.echunks * ((a.nqz + 3) / 4);
+          note_kernel(5, "pi_dmma4_kernel<12,4,4,4,4,true>");
+          both4<<<dim3(gx + (unsigned)tails, 1u), 4 * 32, smem, st>>>(a, chunk_atoms);
+          break;
+        }
         if (split) {  // main and tail CTAs in one launch (the tail CTAs fill the last wave)
           auto both = pi_dmma4_kernel<12, 4, 4, 3, 4, true>;
           e = cudaFuncSetAttribute(both, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
