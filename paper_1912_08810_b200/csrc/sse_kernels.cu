@@ -2900,8 +2900,10 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
-        const char* sl_env = getenv("SSE_PI_V4_SLOTS");  // experiment: a 4-slot V ring (55 KB per CTA)
-        if (split && sl_env && sl_env[0] == '4') {
+        // a 4-slot V ring (55 KB per CTA, 4 CTAs per SM still fit): +0.4 % over 3 slots
+        // (`profiles/r02_ab_k6_slots.log`); SSE_PI_V4_SLOTS=3 restores the 3-slot ring
+        const char* sl_env = getenv("SSE_PI_V4_SLOTS");
+        if (split && !(sl_env && sl_env[0] == '3')) {
           auto both4 = pi_dmma4_kernel<12, 4, 4, 4, 4, true>;
           e = cudaFuncSetAttribute(both4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
           if (e == cudaSuccess) e = cudaFuncSetAttribute(both4, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
