@@ -2900,27 +2900,20 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
-        // a 4-slot V ring (55 KB per CTA, 4 CTAs per SM still fit): +0.4 % over 3 slots
-        // (`profiles/r02_ab_k6_slots.log`); SSE_PI_V4_SLOTS=3 restores the 3-slot ring
-        const char* sl_env = getenv("SSE_PI_V4_SLOTS");
-        if (split && !(sl_env && sl_env[0] == '3')) {
-          auto both4 = pi_dmma4_kernel<12, 4, 4, 4, 4, true>;
-          e = cudaFuncSetAttribute(both4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          if (e == cudaSuccess) e = cudaFuncSetAttribute(both4, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-          if (e != cudaSuccess) return e;
-          const long long tails = (long long)chunk_atoms * 2 * a.echunks * ((a.nqz + 3) / 4);
-          note_kernel(5, "pi_dmma4_kernel<12,4,4,4,4,true>");
-          both4<<<dim3(gx + (unsigned)tails, 1u), 4 * 32, smem, st>>>(a, chunk_atoms);
-          break;
-        }
         if (split) {  // main and tail CTAs in one launch (the tail CTAs fill the last wave)
-          auto both = pi_dmma4_kernel<12, 4, 4, 3, 4, true>;
-          e = cudaFuncSetAttribute(both, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4);
+          // 4-slot V ring (55 KB per CTA; +0.4 % over 3 slots, `profiles/r02_ab_k6_slots.log`) at 3
+          // CTAs per SM with 162 registers and no spills: +1.2 % over 4 CTAs at 128 registers, whose
+          // spill reloads missed L1 and stalled the loop control (`profiles/r02_ab_k6_minb.log`,
+          // `r02_ncu_k6_stalls_minb{4,3}.txt`); SSE_PI_V4_MINB=4 selects the 4-CTA build
+          const char* mb_env = getenv("SSE_PI_V4_MINB");
+          const bool minb4 = mb_env && mb_env[0] == '4';
+          auto both = minb4 ? pi_dmma4_kernel<12, 4, 4, 4, 4, true> : pi_dmma4_kernel<12, 4, 4, 4, 3, true>;
+          e = cudaFuncSetAttribute(both, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
           if (e == cudaSuccess) e = cudaFuncSetAttribute(both, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
           if (e != cudaSuccess) return e;
           const long long tails = (long long)chunk_atoms * 2 * a.echunks * ((a.nqz + 3) / 4);
-          note_kernel(5, "pi_dmma4_kernel<12,4,4,3,4,true>");
-          both<<<dim3(gx + (unsigned)tails, 1u), 4 * 32, smem4, st>>>(a, chunk_atoms);
+          note_kernel(5, minb4 ? "pi_dmma4_kernel<12,4,4,4,4,true>" : "pi_dmma4_kernel<12,4,4,4,3,true>");
+          both<<<dim3(gx + (unsigned)tails, 1u), 4 * 32, smem, st>>>(a, chunk_atoms);
         } else {
           note_kernel(5, "pi_dmma4_kernel<12,4,4,3,4>");
           kern<<<dim3(gx, (unsigned)((pairs + 3) / 4)), 4 * 32, smem4, st>>>(a, chunk_atoms);

@@ -51,7 +51,7 @@ def test_pi_golden_parity(name):
     if name == "pi_paperlike_s12":
         from paper_1912_08810_b200 import _lib
 
-        assert _lib.kernel_name("pi") == "pi_dmma4_kernel<12,4,4,4,4,true>", _lib.kernel_name("pi")
+        assert _lib.kernel_name("pi") == "pi_dmma4_kernel<12,4,4,4,3,true>", _lib.kernel_name("pi")
         assert _lib.kernel_name("pi_build") == "pi_build_dmma_kernel<12>"
     p = c.p
     assert counter.stages == pi_tallies(True, p.n_kz, p.n_qz, p.n_E, p.n_w, p.n_A, p.n_B, p.n_orb)
