@@ -1979,8 +1979,9 @@ constexpr int kPi3Slots = 4;  // ring slots: the producer runs kPi3Slots - 1 sub
 // for every warp's release (empty mbarrier).
 // NOT/NBT > 0: No and NB fixed at compile time (the paper shapes), so every
 // sub-stage is a fixed, fully unrolled run of quad pairs with no branches.
-template <bool LAST_PRODUCES, int NOT, int NBT>
-__global__ void __launch_bounds__(kPiWarps * 32, 3)
+// NW / MINB: warps per CTA and CTAs per SM (default 9 and 3 = 72 registers)
+template <bool LAST_PRODUCES, int NOT, int NBT, int NW = kPiWarps, int MINB = 3>
+__global__ void __launch_bounds__(NW * 32, MINB)
 pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int no = NOT > 0 ? NOT : p.no;
@@ -2009,7 +2010,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   } else {
     q = bx % p.nqz;
     bx /= p.nqz;
-    wg = blockIdx.y * kPiWarps + warp;
+    wg = blockIdx.y * NW + warp;
   }
   const int ec = bx % p.echunks;
   bx /= p.echunks;
@@ -2023,7 +2024,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPi3Slots; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kPiWarps);
+      mbar_init(empty + s, NW);
       rel[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2107,7 +2108,7 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
   for (int ss = 0; ss < n_ss; ++ss) {
     if (!LAST_PRODUCES) {
       const int t = ss + kPi3Slots - 1;
-      if (lane == 0 && t < n_ss && t % kPiWarps == warp) produce(t);
+      if (lane == 0 && t < n_ss && t % NW == warp) produce(t);
     }
     __syncwarp();  // reconverge before the warp-wide mma.sync
     mbar_wait(full + slot, phase);
@@ -2167,9 +2168,9 @@ pi_dmma3_kernel(PiArgs p, int chunk_atoms) {
         unsigned old;
         asm volatile("atom.acq_rel.cta.shared::cta.inc.u32 %0, [%1], %2;"
                      : "=r"(old)
-                     : "r"(smem_u32(rel + slot)), "r"((unsigned)(kPiWarps - 1))
+                     : "r"(smem_u32(rel + slot)), "r"((unsigned)(NW - 1))
                      : "memory");
-        if (old == kPiWarps - 1 && ss + kPi3Slots < n_ss) {  // last release: refill the slot
+        if (old == NW - 1 && ss + kPi3Slots < n_ss) {  // last release: refill the slot
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           produce(ss + kPi3Slots);
         }
@@ -2939,6 +2940,20 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
       PiArgs b = a;
       // few lag tiles (e.g. the small config: 2) -> one CTA serves every q: 6 of 9 warps busy, not 2
       b.q_in_warps = a.peer.ranks == 0 && groups * a.nqz <= kPiWarps;
+      // q in warps with at most 6 busy warps (the small config: 3 q x 2 lag tiles): a 6-warp CTA at
+      // 3 CTAs per SM (96 registers, no spills) instead of 9 warps at 72 registers with 3 idle and
+      // spilling: 28.0 -> 21.2 ms per 256-atom small chunk (`profiles/r02_ab_k6_small.log`);
+      // SSE_PI_QW=9 keeps the 9-warp CTA
+      const char* qw_env = getenv("SSE_PI_QW");
+      if (b.q_in_warps && !fixed && !last && groups * a.nqz <= 6 && !(qw_env && qw_env[0] == '9')) {
+        auto k6 = pi_dmma3_kernel<false, 0, 0, 6, 3>;
+        e = cudaFuncSetAttribute(k6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k6, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        note_kernel(5, "pi_dmma3_kernel<0,0,0,6,3> (q in warps)");
+        k6<<<dim3(gx / (unsigned)a.nqz, 1u), 6 * 32, smem, st>>>(b, chunk_atoms);
+        break;
+      }
       note_kernel(5, fixed ? "pi_dmma3_kernel<%d,12,4>%s" : "pi_dmma3_kernel<%d,0,0>%s", (int)last,
                   b.q_in_warps ? " (q in warps)" : "");
       if (b.q_in_warps)

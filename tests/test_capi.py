@@ -57,7 +57,8 @@ def test_library_is_sm100a_only():
     ("_ZN3sse22sigma_dmma_pipe_kernelILi12EEEvNS_9SigmaArgsE", 108),  # register-pipelined K3 (2 stages x 54)
     ("_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", 54),        # simple K3
     ("_ZN3sse23sigma_dmma_slide_kernelILi12ELi12ELi3EEEvNS_9SigmaArgsE", 54),  # single-momentum sliding-window K3
-    ("_ZN3sse15pi_dmma3_kernelILb0ELi12ELi4EEEvNS_6PiArgsEi", 108),            # Pi K6 v3 (paper shapes)
+    ("_ZN3sse15pi_dmma3_kernelILb0ELi12ELi4ELi9ELi3EEEvNS_6PiArgsEi", 108),    # Pi K6 v3 (paper shapes)
+    ("_ZN3sse15pi_dmma3_kernelILb0ELi0ELi0ELi6ELi3EEEvNS_6PiArgsEi", 54),      # Pi K6 v3, 6-warp q in warps (small)
     ("_ZN3sse15pi_dmma4_kernelILi12ELi4ELi4ELi4ELi3ELb1EEEvNS_6PiArgsEi", 216),  # Pi K6 v4 split (default: 4-slot ring, 3 CTAs / SM)
     ("_ZN3sse20pi_build_dmma_kernelILi12ELi3EEEvNS_11PiBuildArgsE", 72),       # Pi K5 v2 (W in 3-n-tile groups)
 ])
