@@ -2305,14 +2305,13 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   const int n_st = p.nkz * ne_c;
   const int n_ss = kPi3Sub * n_st;
 
-  auto produce = [&](int t) {
+  // producer: sub-stage t = (stage (kt, et), part jt) into slot t % SL
+  auto produce = [&](int t, int kt, int et, int jt) {
     const int slot = t % SL;
     if (t >= SL) mbar_wait(empty + slot, (uint32_t)(((t - SL) / SL) & 1));
-    const int st = t / kPi3Sub, j = t % kPi3Sub;
-    const int k = st / ne_c, e = e_lo + st % ne_c;
     constexpr uint32_t bytes = (uint32_t)SLOT * 16;
     mbar_arrive_expect_tx(full + slot, bytes);
-    bulk_g2s(ring + slot * SLOT, VT + (((long long)k * p.ne + e) * NO2 + j * QS * 4) * NCOL, bytes, full + slot);
+    bulk_g2s(ring + slot * SLOT, VT + (((long long)kt * p.ne + et) * NO2 + jt * QS * 4) * NCOL, bytes, full + slot);
   };
   auto row_of = [&](int t, int k, int e) -> const double2* {
     int kp = k + q;
@@ -2328,24 +2327,39 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
     const int qq = kq < KHP ? kq : kq - KHP;
     return __ldg(r + qq * 4);
   };
-
-  if (threadIdx.x == 0)
-    for (int t = 0; t < SL - 1 && t < n_ss; ++t) produce(t);
-  // loop state kept minimal (v4 runs at 128 registers): slot, phase, sub-stage j and
-  // the quad index are functions of ss; (k, e) of the stage index ss / kPi3Sub
-  auto stage_ke = [&](int st, int& k_, int& e_) {
-    k_ = st / ne_c;
-    e_ = e_lo + (st - k_ * ne_c);
+  // stage / sub-stage counters advance incrementally (no divisions in the loop; round 1 derived
+  // them from ss to save registers at 128, the 3-CTA build has room): (k, e) of a stage index
+  auto next_stage = [&](int& k_, int& e_) {
+    if (++e_ == e_hi) {
+      e_ = e_lo;
+      ++k_;
+    }
   };
+  // producer cursor: the next sub-stage to load, (kt, et, jt); thread 0 primes SL - 1 of them
+  int tp = 0, kt = 0, et = e_lo, jt = 0;
+  auto advance_t = [&]() {
+    ++tp;
+    if (++jt == kPi3Sub) {
+      jt = 0;
+      next_stage(kt, et);
+    }
+  };
+  for (; tp < SL - 1 && tp < n_ss;) {
+    if (threadIdx.x == 0) produce(tp, kt, et, jt);
+    advance_t();
+  }
+  int k2 = 0, e2 = e_lo;  // stage st + 2 (the rows the next stage switch loads)
   {
-    int k0, e0, k1, e1;
-    stage_ke(0, k0, e0);
-    stage_ke(n_st > 1 ? 1 : 0, k1, e1);
+    int k1 = 0, e1 = e_lo;
+    if (n_st > 1) next_stage(k1, e1);
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      cur[t] = row_of(t, k0, e0);
+      cur[t] = row_of(t, 0, e_lo);
       nxt[t] = row_of(t, k1, e1);
     }
+    k2 = k1;
+    e2 = e1;
+    next_stage(k2, e2);
   }
   double2 a0[2], a1[2];
 #pragma unroll
@@ -2384,23 +2398,21 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
   // is outside the loop: 29.8 vs 28.2 TF/s on a 98-atom paper shard)
   auto run = [&](auto two_c) {
     constexpr bool TWO = decltype(two_c)::value;
+    int j = 0, st = 0, e = e_lo, slot = 0;
+    uint32_t phase = 0;
     for (int ss = 0; ss < n_ss; ++ss) {
-      const int slot = ss % SL;
-      const int st = ss / kPi3Sub, j = ss - st * kPi3Sub;
       const int kq = j * QS;
-      {
-        const int t = ss + SL - 1;
-        if (lane == 0 && t < n_ss && t % NW == warp) produce(t);
+      if (tp < n_ss) {  // the producer cursor runs SL - 1 sub-stages ahead
+        if (lane == 0 && tp % NW == warp) produce(tp, kt, et, jt);
+        advance_t();
       }
       __syncwarp();
-      mbar_wait(full + slot, (uint32_t)((ss / SL) & 1));
-      int k, e;
-      stage_ke(st, k, e);
+      mbar_wait(full + slot, phase);
       const bool live = active && e + off_min < p.ne;
       const double* sb = reinterpret_cast<const double*>(ring + slot * SLOT) + pcol * 2 * NCOL + b_off;
       // the sub-stage's quads kq .. kq+5 span rows n = kq/3 (quads 0-2) and kq/3 + 1 (quads 3-5)
       static_assert(QS == 6, "mode-3 swizzle deltas assume 6 quads per sub-stage");
-      const int dn0 = n_delta(kq / 3), dn1 = n_delta(kq / 3 + 1);
+      const int dn0 = n_delta(2 * j), dn1 = n_delta(2 * j + 1);
       auto dq = [&](int qd) { return qd < 3 ? dn0 : dn1; };
       if (live && TWO) {
 #pragma unroll
@@ -2432,15 +2444,21 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
       }
       __syncwarp();  // the warp is done with the slot before lane 0 releases it
       if (lane == 0) mbar_arrive(empty + slot);
-      if (j == kPi3Sub - 1) {  // stage done: the next stage's rows become current
+      if (++slot == SL) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      if (++j == kPi3Sub) {  // stage done: the next stage's rows become current
+        j = 0;
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) cur[tt] = nxt[tt];
         if (st + 2 < n_st) {
-          int k2, e2;
-          stage_ke(st + 2, k2, e2);
 #pragma unroll
           for (int tt = 0; tt < 2; ++tt) nxt[tt] = row_of(tt, k2, e2);
         }
+        ++st;
+        if (++e == e_hi) e = e_lo;
+        next_stage(k2, e2);
       }
     }
   };
