@@ -838,6 +838,8 @@ def run_gpu(args, p, grid, idx) -> None:
 
     if rank == 0:
         traffic = load_traffic()
+        if traffic and traffic.get("launch_name") and traffic["launch_name"] not in k3_name:
+            traffic = None  # the committed capture describes another K3 build: no traffic claim
         line = {
             "metric": METRIC, "value": step_ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",

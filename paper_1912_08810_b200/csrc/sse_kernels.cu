@@ -2678,17 +2678,17 @@ static int sigma_kernel_choice() {
   return env ? atoi(env) : 4;
 }
 
-template <int NO, int KG, bool COMB = false, int NW = 12>
+template <int NO, int KG, bool COMB = false, int NW = 12, int MT = 3>
 static cudaError_t launch_kslide(SigmaArgs a, int chunk_atoms, int k_first, int groups, cudaStream_t st) {
-  using SG = KSlideGeom<NO, NW, 3, KG, COMB>;
+  using SG = KSlideGeom<NO, NW, MT, KG, COMB>;
   a.ctas_per_ak = (a.rows + SG::kRows - 1) / SG::kRows;
   a.k_first = k_first;
   a.kgroups = groups;
   const dim3 grid((unsigned)((long long)a.ctas_per_ak * groups * chunk_atoms), a.npol);
-  cudaError_t e = cudaFuncSetAttribute(sigma_dmma_kslide_kernel<NO, NW, 3, KG, COMB>,
+  cudaError_t e = cudaFuncSetAttribute(sigma_dmma_kslide_kernel<NO, NW, MT, KG, COMB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG::kSmem);
   if (e != cudaSuccess) return e;
-  sigma_dmma_kslide_kernel<NO, NW, 3, KG, COMB><<<grid, NW * 32, SG::kSmem, st>>>(a);
+  sigma_dmma_kslide_kernel<NO, NW, MT, KG, COMB><<<grid, NW * 32, SG::kSmem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -2734,6 +2734,22 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
     const int kg = kg_env && atoi(kg_env) >= 1 && atoi(kg_env) <= 3 ? atoi(kg_env) : (NO >= 9 ? 2 : 3);
     const int full = a.nkz / kg, rest = a.nkz % kg;
     cudaError_t e = cudaSuccess;
+    // No = 12, odd Nkz >= 3: momentum groups of 2, closed by ONE group of 3 at 2 row tiles per warp
+    // (164 registers, no spills) instead of a 1-momentum remainder launch: paper (Nkz = 3, one
+    // KG = 3 launch) 35.16 -> 35.46 TF/s, large (2 + 3) 35.73 -> 35.80; kheavy 2+2+2+1 vs 3+3+1:
+    // 35.43 vs 35.26, so at most one such group (`profiles/r02_ab_k3m_mt2*.log`); SSE_K3M_MT=3 or
+    // SSE_K3M_KG restore the plain groups of kg
+    const char* mt_env = getenv("SSE_K3M_MT");
+    if (NO == 12 && !kg_env && !(mt_env && atoi(mt_env) == 3) && a.nkz >= 3 && (a.nkz & 1)) {
+      const int pairs = (a.nkz - 3) / 2;
+      if (pairs > 0) e = launch_kslide<NO, 2>(a, chunk_atoms, 0, pairs, st);
+      if (e == cudaSuccess) e = launch_kslide<NO, 3, false, 12, 2>(a, chunk_atoms, 2 * pairs, 1, st);
+      if (pairs > 0)
+        note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,3,2> (x%d momentum groups) + <%d,12,2,3>", NO, pairs, NO);
+      else
+        note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,2,3>", NO);
+      return e;
+    }
     const char* nw_env = getenv("SSE_K3M_NW");  // experiment: 8 warps (2 per SMSP, <= 255 registers)
     if (NO == 12 && nw_env && atoi(nw_env) == 8 && kg == 3 && full > 0) {
       e = launch_kslide<NO, 3, false, 8>(a, chunk_atoms, 0, full, st);

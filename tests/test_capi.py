@@ -52,7 +52,8 @@ def test_library_is_sm100a_only():
 
 
 @pytest.mark.parametrize("kernel, dmma", [
-    ("_ZN3sse24sigma_dmma_kslide_kernelILi12ELi12ELi3ELi2ELb0EEEvNS_9SigmaArgsE", 108),  # production K3m (2 momenta)
+    ("_ZN3sse24sigma_dmma_kslide_kernelILi12ELi12ELi2ELi3ELb0EEEvNS_9SigmaArgsE", 162),  # production K3m, odd Nkz (3 momenta)
+    ("_ZN3sse24sigma_dmma_kslide_kernelILi12ELi12ELi3ELi2ELb0EEEvNS_9SigmaArgsE", 108),  # K3m momentum pairs
     ("_ZN3sse24sigma_dmma_kslide_kernelILi10ELi12ELi3ELi3ELb1EEEvNS_9SigmaArgsE", 120),  # K3m, No=10 combined
     ("_ZN3sse22sigma_dmma_pipe_kernelILi12EEEvNS_9SigmaArgsE", 108),  # register-pipelined K3 (2 stages x 54)
     ("_ZN3sse17sigma_dmma_kernelILi12EEEvNS_9SigmaArgsE", 54),        # simple K3

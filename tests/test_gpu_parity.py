@@ -169,7 +169,8 @@ def test_kernel_shapes_against_oracle(monkeypatch, n_e, n_w, n_o, n_a, n_b):
 
 
 @pytest.mark.parametrize("n_kz, n_qz, n_e, n_w, n_o, n_a", [
-    (5, 3, 30, 8, 12, 5),   # K3m: one 2-momentum group + ... (kg 2: groups {0,1}, {2,3}, remainder {4}); Nqz < Nkz
+    (5, 3, 30, 8, 12, 5),   # K3m No = 12, odd Nkz: group {0,1} then one 3-momentum group {2,3,4} (2 row tiles); Nqz < Nkz
+    (3, 3, 41, 12, 12, 5),  # the paper's Nkz = Nqz = 3: one 3-momentum launch; 492 rows = 2 full + 1 partial CTA
     (4, 4, 26, 7, 10, 5),   # combined fragments (No = 10): groups {0,1,2}, {3 + 2 padded momenta}
     (1, 1, 20, 8, 12, 5),   # Nkz = 1: a single-momentum launch
     (7, 2, 22, 6, 4, 5),    # No = 4 (kg 3): groups {0,1,2}, {3,4,5}, remainder {6}; Nqz = 2 (most M vectors zero)
@@ -196,6 +197,12 @@ def test_multi_momentum_groups_against_oracle(monkeypatch, n_kz, n_qz, n_e, n_w,
         assert orc.parity_dev(out.lesser, out.greater, ref_l, ref_g) <= TOL, choice
         outs.append(out)
     assert np.array_equal(outs[0].lesser, outs[1].lesser) and np.array_equal(outs[0].greater, outs[1].greater)
+    if n_o == 12 and n_kz % 2 == 1 and n_kz >= 3:  # the plain groups of 2 + a 1-momentum remainder agree bitwise
+        monkeypatch.setenv("SSE_SIGMA_KERNEL", "4")
+        monkeypatch.setenv("SSE_K3M_MT", "3")
+        out = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(g_l, g_g), dc, dh, nmap, grid)
+        assert "<12,12,3,1>" in _lib.kernel_name("sigma"), _lib.kernel_name("sigma")
+        assert np.array_equal(outs[0].lesser, out.lesser) and np.array_equal(outs[0].greater, out.greater)
 
 
 def test_layout_transformed_equals_grid_major_bitwise():
