@@ -2217,7 +2217,7 @@ constexpr int kPi4Warps = 5;
 
 // TAIL: the CTA is (atom, chain polarity, E-chunk) and warp w computes the LAST lag
 // tile for momentum q = w (all Nqz warps share the V stages); the main launch then
-// covers the first 2*NW tiles per q (paper: 8 + 1 lag tiles, 4 warps per SMSP).
+// covers the first 2*NW tiles per q (paper: 8 + 1 lag tiles; 3 CTAs of 4 warps per SM).
 template <int NOT, int NBT, int NW = kPi4Warps, int SL = kPi3Slots, int MINB = 3, bool TAIL_CTAS = false>
 __global__ void __launch_bounds__(NW * 32, MINB)
 pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
@@ -2927,7 +2927,7 @@ cudaError_t launch_pi(const PiArgs& a, int chunk_atoms, cudaStream_t st) {
       const int m_tiles = (a.nw + 7) / 8;
       const bool split = !(w4 && w4[0] == '5') && m_tiles == 9;
       if (split || (w4 && w4[0] == '4')) {
-        // 4 warps x 2 lag tiles per CTA (4 CTAs, 16 warps per SM: 4 per SMSP) for tiles 0..7,
+        // 4 warps x 2 lag tiles per CTA (3 CTAs, 12 warps per SM by default) for tiles 0..7,
         // then (split) the 9th tile of every q in one tail CTA per (atom, polarity, E-chunk)
         auto kern = pi_dmma4_kernel<12, 4, 4, 3, 4>;
         const size_t slot = (size_t)2 * ((((a.no * a.no + 3) / 4) + 2 * kPi3Sub - 1) / (2 * kPi3Sub)) * 4 * a.ncol * 16;
