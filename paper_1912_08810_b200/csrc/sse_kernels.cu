@@ -2739,24 +2739,26 @@ static cudaError_t launch_dmma(const SigmaArgs& a0, int chunk_atoms, cudaStream_
     // KG = 3 launch) 35.16 -> 35.46 TF/s, large (2 + 3) 35.73 -> 35.80; kheavy 2+2+2+1 vs 3+3+1:
     // 35.43 vs 35.26, so at most one such group (`profiles/r02_ab_k3m_mt2*.log`); SSE_K3M_MT=3 or
     // SSE_K3M_KG restore the plain groups of kg
-    const char* mt_env = getenv("SSE_K3M_MT");
-    if (NO == 12 && !kg_env && !(mt_env && atoi(mt_env) == 3) && a.nkz >= 3 && (a.nkz & 1)) {
-      const int pairs = (a.nkz - 3) / 2;
-      if (pairs > 0) e = launch_kslide<NO, 2>(a, chunk_atoms, 0, pairs, st);
-      if (e == cudaSuccess) e = launch_kslide<NO, 3, false, 12, 2>(a, chunk_atoms, 2 * pairs, 1, st);
-      if (pairs > 0)
-        note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,3,2> (x%d momentum groups) + <%d,12,2,3>", NO, pairs, NO);
-      else
-        note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,2,3>", NO);
-      return e;
-    }
-    const char* nw_env = getenv("SSE_K3M_NW");  // experiment: 8 warps (2 per SMSP, <= 255 registers)
-    if (NO == 12 && nw_env && atoi(nw_env) == 8 && kg == 3 && full > 0) {
-      e = launch_kslide<NO, 3, false, 8>(a, chunk_atoms, 0, full, st);
-      if (e == cudaSuccess && rest == 2) e = launch_kslide<NO, 2, false, 8>(a, chunk_atoms, 3 * full, 1, st);
-      if (e == cudaSuccess && rest == 1) e = launch_kslide<NO, 1, false, 8>(a, chunk_atoms, 3 * full, 1, st);
-      note_kernel(1, "sigma_dmma_kslide_kernel<%d,8,3,3>", NO);
-      return e;
+    if constexpr (NO == 12) {  // (compile-time: the No = 12 variants are instantiated only for 12)
+      const char* mt_env = getenv("SSE_K3M_MT");
+      if (!kg_env && !(mt_env && atoi(mt_env) == 3) && a.nkz >= 3 && (a.nkz & 1)) {
+        const int pairs = (a.nkz - 3) / 2;
+        if (pairs > 0) e = launch_kslide<NO, 2>(a, chunk_atoms, 0, pairs, st);
+        if (e == cudaSuccess) e = launch_kslide<NO, 3, false, 12, 2>(a, chunk_atoms, 2 * pairs, 1, st);
+        if (pairs > 0)
+          note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,3,2> (x%d momentum groups) + <%d,12,2,3>", NO, pairs, NO);
+        else
+          note_kernel(1, "sigma_dmma_kslide_kernel<%d,12,2,3>", NO);
+        return e;
+      }
+      const char* nw_env = getenv("SSE_K3M_NW");  // experiment: 8 warps (2 per SMSP, <= 255 registers)
+      if (nw_env && atoi(nw_env) == 8 && kg == 3 && full > 0) {
+        e = launch_kslide<NO, 3, false, 8>(a, chunk_atoms, 0, full, st);
+        if (e == cudaSuccess && rest == 2) e = launch_kslide<NO, 2, false, 8>(a, chunk_atoms, 3 * full, 1, st);
+        if (e == cudaSuccess && rest == 1) e = launch_kslide<NO, 1, false, 8>(a, chunk_atoms, 3 * full, 1, st);
+        note_kernel(1, "sigma_dmma_kslide_kernel<%d,8,3,3>", NO);
+        return e;
+      }
     }
     if (full > 0) {
       if (kg == 3) e = launch_kslide<NO, 3>(a, chunk_atoms, 0, full, st);
