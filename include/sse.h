@@ -319,8 +319,9 @@ int sse_profile_begin(sse_ctx* ctx);
 int sse_profile_end(sse_ctx* ctx, sse_profile* out);
 
 /* Name (with template arguments) of the kernel of kind SSE_PROF_* the library
- * launched last in this process, e.g. "sigma_dmma_slide_kernel<12,12,3>";
- * "" before the first launch of that kind or for an unknown kind. */
+ * launched last in this process, e.g. "sigma_dmma_kslide_kernel<12,12,2,3>";
+ * "" before the first launch of that kind or for an unknown kind.  Thread-safe;
+ * the returned string is valid until this thread's next call. */
 const char* sse_kernel_name(int kind);
 
 #ifdef __cplusplus

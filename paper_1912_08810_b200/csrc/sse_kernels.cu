@@ -17,19 +17,33 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <type_traits>
 
 namespace sse {
 
-// last launched kernel per kind (bench / smoke evidence of which variant ran)
+// last launched kernel per kind (bench / smoke evidence of which variant ran); the per-device
+// host threads of the multi-GPU entry points launch concurrently, so writes and reads are serialised
+// and a reader gets its own (thread-local) copy
 static char g_kernel_name[7][192];
+static std::mutex g_kernel_name_mu;
 static void note_kernel(int kind, const char* fmt, ...) {
+  char buf[sizeof(g_kernel_name[0])];
   va_list ap;
   va_start(ap, fmt);
-  vsnprintf(g_kernel_name[kind], sizeof(g_kernel_name[kind]), fmt, ap);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
   va_end(ap);
+  std::lock_guard<std::mutex> lk(g_kernel_name_mu);
+  memcpy(g_kernel_name[kind], buf, sizeof(buf));
 }
-const char* last_kernel_name(int kind) { return kind >= 0 && kind < 7 ? g_kernel_name[kind] : ""; }
+const char* last_kernel_name(int kind) {
+  thread_local char out[sizeof(g_kernel_name[0])];
+  if (kind < 0 || kind >= 7) return "";
+  std::lock_guard<std::mutex> lk(g_kernel_name_mu);
+  memcpy(out, g_kernel_name[kind], sizeof(out));
+  return out;
+}
 
 // --------------------------------------------------------------------------
 // K1: layout transform.  One warp per (k, E, a) block of blk_vec 16-byte
