@@ -35,7 +35,14 @@ sys.path.insert(0, REPO)
 
 METRIC = "SSE time per Born iteration (s) and achieved FP64 TFLOP/s at 1/2/4/8 B200 vs CPU ref"
 FP64_PEAK_TFLOPS = 36.85  # measured DMMA.8x8x4 sustained, profiles/r01_fp64_peak.json
-FP64_PEAK_SOURCE = "measured DMMA m8n8k4 sustained on this pool's B200 (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry"
+FP64_PEAK_SOURCE = ("measured DMMA m8n8k4 sustained on this pool's B200 (profiles/r01_fp64_peak.json); MEASURED_PEAKS.json "
+                    "has no FP64 entry; a DMMA-only loop later reached 37.15 TF/s (profiles/r02_dmma_k6_pattern.log), "
+                    "the nominal rate is 148 SM x 64 FMA/clk x the SM clock: `frac_vs_nominal`")
+
+
+def nominal_fp64_tflops(sm_mhz) -> float | None:
+    """148 SMs x 128 flop/clk (64 DMMA FMA per SM per clock) x the SM clock measured during the run."""
+    return 148 * 128 * sm_mhz / 1e6 if sm_mhz else None
 
 
 def launched_kernel(kind: str) -> str:
@@ -855,6 +862,8 @@ def run_gpu(args, p, grid, idx) -> None:
                 "bound": "tensor", "kernel": k3_name,
                 "achieved": k3_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": k3_tflops / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
+                "frac_vs_nominal": (k3_tflops / nominal_fp64_tflops(clk.get("sm_mhz"))
+                                    if nominal_fp64_tflops(clk.get("sm_mhz")) else None),
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                 "traffic_source": (traffic or {}).get("capture"),
                 "k3_ms_per_launch": k3_ms_per_launch, "k3_launches_per_step": sig["launches"] / args.steps,
