@@ -832,6 +832,9 @@ def run_gpu(args, p, grid, idx) -> None:
     del prob
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
+    from paper_1912_08810_b200 import _lib as sse_lib
+
+    sse_lib.context(device=local_rank).trim()  # the device legs' cached scratch (Pi operands: up to 48 GiB)
     barrier(world)
 
     e2e = None

@@ -85,6 +85,11 @@ typedef struct sse_timing {
  * them, distsim.py:117-120).  sse_ctx_create_on binds one given device. */
 int sse_ctx_create(int n_gpus, sse_ctx** out);
 int sse_ctx_create_on(int device, sse_ctx** out);
+/* Release the context's cached device scratch (per-call buffers, the Pi operand scratch of up to
+ * 2 x 24 GiB) and its pinned host staging ring, after waiting for the context's work; the next call
+ * allocates again.  For callers that need the memory between SSE phases (e.g. a device GF phase).
+ * Not part of the reference interface. */
+int sse_ctx_trim(sse_ctx* ctx);
 void sse_ctx_destroy(sse_ctx* ctx);
 const char* sse_last_error(void);
 int sse_version(void);

@@ -21,6 +21,7 @@ EXPORTED = (
     "sse_ctx_create",
     "sse_ctx_create_on",
     "sse_ctx_destroy",
+    "sse_ctx_trim",
     "sse_last_error",
     "sse_version",
     "sse_sigma_c128",
@@ -125,6 +126,7 @@ def load() -> ctypes.CDLL:
         lib.sse_ctx_create_on.argtypes = [i32, ctypes.POINTER(_P)]
         lib.sse_ctx_destroy.argtypes = [_P]
         lib.sse_ctx_destroy.restype = None
+        lib.sse_ctx_trim.argtypes = [_P]
         lib.sse_last_error.restype = ctypes.c_char_p
         lib.sse_version.restype = i32
         lib.sse_sigma_c128.argtypes = [_P, pdims, i32] + [_P] * 7 + [_P, _P, _P, ptim]
@@ -191,6 +193,12 @@ class Context:
         self.handle = handle
         self.n_gpus = 1 if device is not None else int(n_gpus)
         self.device = device
+
+    def trim(self) -> None:
+        """Hand the cached device scratch and pinned staging back (sse_ctx_trim); the next call
+        allocates again."""
+        if self.handle:
+            check(load().sse_ctx_trim(self.handle))
 
     def close(self) -> None:
         if self.handle:

@@ -619,7 +619,19 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
   }
   const int no = (int)d->norb, no2 = no * no, nb = (int)d->nb, ncol = nb * 9;
   const size_t vt_atom = (size_t)d->nkz * d->ne * no2 * ncol * 16;  // per chain polarity
-  int64_t chunk = std::max<int64_t>(1, (int64_t)((12ull << 30) / std::max<size_t>(vt_atom, 1)));
+  // VT scratch per polarity: 24 GiB when the device has room for it (free + the VT already held
+  // >= 2 x 24 GiB + 16 GiB), else 12 GiB.  Each K6 launch ends with a drain of ~2.4 ms (CTAs of
+  // ~9 ms, partially occupied SMs), so fewer, larger chunks save ~1 % of Pi at paper
+  // (`profiles/r02_ab_k6_chunk.log`); sse_ctx_trim hands the cached scratch back.
+  size_t vt_budget = 12ull << 30;
+  {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+        free_b + ds.pi_vt[0].bytes + ds.pi_vt[1].bytes >= 2 * (24ull << 30) + (16ull << 30))
+      vt_budget = 24ull << 30;
+    cudaGetLastError();
+  }
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(vt_budget / std::max<size_t>(vt_atom, 1)));
   if (const char* env = getenv("SSE_PI_CHUNK_ATOMS"))  // override, for tests and experiments
     if (atoll(env) > 0) chunk = atoll(env);
   chunk = std::min<int64_t>(chunk, out.natoms);
@@ -1207,6 +1219,24 @@ int sse_ctx_create_on(int device, sse_ctx** out) {
     return rc;
   }
   *out = ctx;
+  return SSE_OK;
+}
+
+int sse_ctx_trim(sse_ctx* ctx) {
+  if (!ctx) return fail(SSE_EINVAL, "ctx is NULL");
+  for (auto& d : ctx->devs) {
+    CU(cudaSetDevice(d.device));
+    if (d.scratch_pending) CU(cudaEventSynchronize(d.scratch_done));
+    for (cudaStream_t st : {d.stream, d.s_h2d, d.s_d2h})
+      if (st) CU(cudaStreamSynchronize(st));
+    // the large per-call buffers (the small uploaded tables stay: their host shadows skip re-uploads)
+    for (DevBuf* b : {&d.g[0], &d.g[1], &d.s[0], &d.s[1], &d.dc[0], &d.dc[1], &d.op[0], &d.op[1], &d.tmp_g,
+                      &d.tmp_s, &d.pi_vt[0], &d.pi_vt[1], &d.pi_part, &d.pi_out[0], &d.pi_out[1], &d.draw[0],
+                      &d.draw[1]})
+      b->release();
+    for (PinnedBuf* b : {&d.stage_in[0], &d.stage_in[1], &d.stage_out[0], &d.stage_out[1], &d.stage_out[2]})
+      b->release();
+  }
   return SSE_OK;
 }
 

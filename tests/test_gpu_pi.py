@@ -218,3 +218,27 @@ def test_pi_split_lag_tiles_bitwise(monkeypatch):
     for o in outs[1:]:
         assert np.array_equal(outs[0].lesser, o.lesser) and np.array_equal(outs[0].greater, o.greater)
     assert np.abs(outs[0].lesser).max() > 0
+
+
+def test_ctx_trim_then_recompute_bitwise():
+    """sse_ctx_trim hands the cached scratch back (Pi operand buffers, staging ring); the next calls
+    allocate again and give bit-identical Pi and Sigma."""
+    from paper_1912_08810_b200 import _lib
+    from paper_1912_08810_b200.sse import sse_sigma
+    from paper_1912_08810_b200.types import CombinedD, SseVariant
+
+    p = SimParams(n_kz=3, n_qz=3, n_E=30, n_w=12, n_A=5, n_B=4, n_orb=12)
+    g_l, g_g, d_l, d_g, dh = inputs.stream_instance(6, p, dh_scale=0.05)
+    nmap = build_neighbor_map(p.n_A, p.n_B)
+    grid = default_grid(p)
+    dc = CombinedD(*orc.preprocess_D(d_l, d_g, nmap.idx))
+    runs = []
+    for _ in range(2):
+        pi = sse_pi(GreensTensor(g_l, g_g), dh, nmap, grid, p.n_qz)
+        sig = sse_sigma(SseVariant.BATCHED_FUSED, GreensTensor(g_l, g_g), dc, dh, nmap, grid)
+        runs.append((pi, sig))
+        for ctx in list(_lib._contexts.values()):  # whichever contexts the drop-ins used
+            ctx.trim()
+    (pa, sa), (pb, sb) = runs
+    assert np.array_equal(pa.lesser, pb.lesser) and np.array_equal(pa.greater, pb.greater)
+    assert np.array_equal(sa.lesser, sb.lesser) and np.array_equal(sa.greater, sb.greater)
