@@ -2261,8 +2261,23 @@ pi_dmma4_kernel(PiArgs p, int chunk_atoms) {
     q = bx % p.nqz;
     bx /= p.nqz;
   }
-  const int ec = bx % p.echunks;
-  bx /= p.echunks;
+  // main CTAs of a short last E-chunk (paper: 706 = 7 x 96 + 34 energies) come last in the main
+  // grid, so the launch's final wave is packed with short CTAs (each CTA owns its partial slot:
+  // the order does not change any result)
+  int ec;
+  if (TAIL_CTAS && !TAIL && p.echunks > 1 && p.ne % p.e_per_chunk != 0) {
+    const int full_part = chunk_atoms * 2 * (p.echunks - 1);
+    if (bx < full_part) {
+      ec = bx % (p.echunks - 1);
+      bx /= p.echunks - 1;
+    } else {
+      bx -= full_part;
+      ec = p.echunks - 1;
+    }
+  } else {
+    ec = bx % p.echunks;
+    bx /= p.echunks;
+  }
   const int pol = bx % 2;
   const int la = bx / 2;
   const int m_tiles = (p.nw + 7) / 8;
