@@ -566,7 +566,7 @@ int run_chunk(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab
   sa.comb_kg = comb;
   sa.off_slide = offsets_slide(d, off);
   sa.lookahead = getenv("SSE_SLIDE_LOOKAHEAD") ? atoi(getenv("SSE_SLIDE_LOOKAHEAD")) : 0;
-  sa.k3_opts = getenv("SSE_K3_OPTS") ? atoi(getenv("SSE_K3_OPTS")) : 3;
+  sa.k3_opts = getenv("SSE_K3_OPTS") ? atoi(getenv("SSE_K3_OPTS")) : 7;
   if (sc && sc->nranks > 0) {
     sa.scatter_ranks = sc->nranks;
     sa.scatter_na = sc->na;

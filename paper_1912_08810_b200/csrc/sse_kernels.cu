@@ -949,8 +949,24 @@ sigma_dmma_kslide_kernel(SigmaArgs p) {
 
   const int pol = blockIdx.y;
   int bx = blockIdx.x;
-  const int rc = bx % p.ctas_per_ak;
-  bx /= p.ctas_per_ak;
+  // k3_opts bit 2: the partial last row CTA of every (atom, momentum group) comes after all full
+  // CTAs, so a launch's final wave is packed with short CTAs (outputs are disjoint per CTA: the
+  // order changes no result); otherwise row CTAs fastest
+  int rc;
+  const int pairs = (int)(gridDim.x / p.ctas_per_ak);
+  if ((p.k3_opts & 4) && p.ctas_per_ak > 1 && p.rows % SG::kRows != 0) {
+    const int full = pairs * (p.ctas_per_ak - 1);
+    if (bx < full) {
+      rc = bx % (p.ctas_per_ak - 1);
+      bx /= p.ctas_per_ak - 1;
+    } else {
+      rc = p.ctas_per_ak - 1;
+      bx -= full;
+    }
+  } else {
+    rc = bx % p.ctas_per_ak;
+    bx /= p.ctas_per_ak;
+  }
   const int kg = bx % p.kgroups;
   const int la = bx / p.kgroups;
   const int k0 = p.k_first + kg * KG;  // output momenta k0 .. k0 + KG - 1 (those < Nkz)

@@ -89,7 +89,8 @@ struct SigmaArgs {
   int npol;               // polarities to process (1 or 2)
   int off_slide;          // 1: offsets non-decreasing with steps <= 1 (sliding-window K3 eligible)
   int lookahead;          // sliding-window K3 producer lookahead (0 = default)
-  int k3_opts;            // sliding-window K3: bit 0 tail-CTA tile interleave, bit 1 drop empty stages
+  int k3_opts;            // sliding-window K3: bit 0 tail-CTA tile interleave, bit 1 drop empty stages,
+                          // bit 2 (K3m) partial row CTAs after the full ones
   int scatter_ranks;      // 0: write S with the s_* strides
   long long scatter_na, scatter_atom0;  // NA of the point buffers; global id of the chunk's first atom
   long long pt_lo[kMaxScatter + 1];
