@@ -190,6 +190,7 @@ struct DevState {
   DevBuf g[2], s[2], dc[2], dh, op[2], nbr, off, wt, tmp_g, tmp_s, pp_nbr, pp_rev, zero_m;
   DevBuf pi_vt[2], pi_part, pi_mask, pi_out[2], draw[2];
   PinnedBuf stage_in[2], stage_out[3];  // host staging ring of the pageable-memory host calls
+  size_t pi_vt_budget = 0;              // Pi operand scratch per polarity (0: not decided yet)
   cudaEvent_t stage_ev[2] = {};         // H2D from stage_in[b] done
   std::vector<unsigned char> pi_mask_host;
   // host copies of the small tables last uploaded (skip re-uploads: a pageable
@@ -623,14 +624,16 @@ int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_s
   // >= 2 x 24 GiB + 16 GiB), else 12 GiB.  Each K6 launch ends with a drain of ~2.4 ms (CTAs of
   // ~9 ms, partially occupied SMs), so fewer, larger chunks save ~1 % of Pi at paper
   // (`profiles/r02_ab_k6_chunk.log`); sse_ctx_trim hands the cached scratch back.
-  size_t vt_budget = 12ull << 30;
-  {
+  // (decided once per context -- cudaMemGetInfo is not free -- and again after sse_ctx_trim)
+  if (ds.pi_vt_budget == 0) {
+    ds.pi_vt_budget = 12ull << 30;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
         free_b + ds.pi_vt[0].bytes + ds.pi_vt[1].bytes >= 2 * (24ull << 30) + (16ull << 30))
-      vt_budget = 24ull << 30;
+      ds.pi_vt_budget = 24ull << 30;
     cudaGetLastError();
   }
+  const size_t vt_budget = ds.pi_vt_budget;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(vt_budget / std::max<size_t>(vt_atom, 1)));
   if (const char* env = getenv("SSE_PI_CHUNK_ATOMS"))  // override, for tests and experiments
     if (atoll(env) > 0) chunk = atoll(env);
@@ -1236,6 +1239,7 @@ int sse_ctx_trim(sse_ctx* ctx) {
       b->release();
     for (PinnedBuf* b : {&d.stage_in[0], &d.stage_in[1], &d.stage_out[0], &d.stage_out[1], &d.stage_out[2]})
       b->release();
+    d.pi_vt_budget = 0;  // re-decided against the then free memory
   }
   return SSE_OK;
 }
