@@ -603,7 +603,7 @@ int sigma_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const ss
 
 // Phonon self-energy Pi (sse_pi, sse.py:409-428) for the owned atoms of `out`:
 // K5 operand build (VT) -> K6 DMMA chains (partials per E-chunk) -> K7 assembly,
-// in atom chunks bounded by a ~16 GiB VT scratch.  Pi_* are device
+// in atom chunks bounded by the VT scratch (12 or 24 GiB per polarity).  Pi_* are device
 // [Nqz, Nw, out.natoms, NB+1, 3, 3]; mask: host [Nkz*NE] or NULL.
 int pi_on_device(DevState& ds, const sse_dims* d, const sse_slab& g, const sse_slab& out,
                  const double2* G_l, const double2* G_g, const double2* dH, const int64_t* nmap,
