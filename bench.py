@@ -196,6 +196,13 @@ def run_reference(args, p, grid, idx) -> None:
         return
     from oracle.ref import import_negflow
 
+    # all host cores for the reference's BLAS, also under torchrun (which sets OMP_NUM_THREADS=1)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        _blas_limit = threadpool_limits(limits=os.cpu_count(), user_api="blas")  # noqa: F841 (kept alive)
+    except Exception:
+        pass
     nf = import_negflow()
     pairs = sample_pairs(p)
     for i in range(args.warmup):
